@@ -1,0 +1,236 @@
+// api.cu -- the C ABI (include/gcm.h): argument validation, the per-(device,
+// stream) workspace cache, algorithm dispatch and the failure report.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "internal.h"
+
+namespace gcm {
+
+gcm_status_t check_cuda(cudaError_t e) {
+    if (e == cudaSuccess) return GCM_OK;
+    if (e == cudaErrorMemoryAllocation) return GCM_ENOMEM;
+    return GCM_ECUDA;
+}
+
+namespace {
+
+std::mutex g_ws_mutex;
+std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+
+__global__ void info_finalize_kernel(const unsigned long long *key, gcm_info_t *info, int64_t count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const unsigned long long kv = key[i];
+    gcm_info_t r;
+    if (kv == kInfoNone) {
+        r.code = 0;
+        r.col = 0;
+        r.row = 0;
+    } else {
+        r.code = (kv & 1ull) ? 1 : 2;
+        r.col = (int32_t)(kv >> 41);
+        r.row = (int64_t)((kv >> 1) & ((1ull << 40) - 1));
+    }
+    info[i] = r;
+}
+
+gcm_status_t validate(const double *L, int64_t n, int64_t ldl, const double *V, int64_t k, int sigma) {
+    if (n < 0 || k < 0 || ldl < std::max<int64_t>(1, n)) return GCM_EINVAL;
+    if (sigma != 1 && sigma != -1) return GCM_EINVAL;
+    if (n > 0 && k > 0 && (L == nullptr || V == nullptr)) return GCM_EINVAL;
+    if (n >= (1ll << 40) || k >= (1ll << 22)) return GCM_EINVAL;
+    return GCM_OK;
+}
+
+gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
+    if (algo != GCM_ALGO_AUTO) return algo;
+    const char *env = std::getenv("GCM_ALGO");
+    if (env && std::strcmp(env, "sweep") == 0) return GCM_ALGO_SWEEP;
+    if (env && std::strcmp(env, "blocked") == 0) return GCM_ALGO_BLOCKED;
+    (void)n;
+    (void)k;
+    return GCM_ALGO_SWEEP;
+}
+
+}  // namespace
+
+gcm_status_t get_workspace(cudaStream_t stream, size_t bytes, size_t nkeys, Workspace **out) {
+    int dev = 0;
+    gcm_status_t st = check_cuda(cudaGetDevice(&dev));
+    if (st != GCM_OK) return st;
+    const size_t key_bytes = ((nkeys * sizeof(unsigned long long) + 255) / 256) * 256;
+    const size_t need = key_bytes + ((bytes + 255) / 256) * 256;
+    std::lock_guard<std::mutex> lock(g_ws_mutex);
+    Workspace &ws = g_ws[{dev, stream}];
+    if (ws.bytes < need) {
+        if (ws.key) {
+            // the old buffer may still be in use by work queued on this stream
+            st = check_cuda(cudaStreamSynchronize(stream));
+            if (st != GCM_OK) return st;
+            cudaFree(ws.key);
+            ws = Workspace{};
+        }
+        const size_t alloc = need + need / 4;
+        void *p = nullptr;
+        st = check_cuda(cudaMalloc(&p, alloc));
+        if (st != GCM_OK) return st;
+        ws.key = static_cast<unsigned long long *>(p);
+        ws.bytes = alloc;
+    }
+    ws.panels = reinterpret_cast<double *>(reinterpret_cast<char *>(ws.key) + key_bytes);
+    ws.extra = ws.panels;
+    *out = &ws;
+    return GCM_OK;
+}
+
+gcm_status_t finalize_info(const unsigned long long *key, gcm_info_t *d_info, int64_t count, cudaStream_t stream) {
+    if (!d_info || count <= 0) return GCM_OK;
+    const int threads = 128;
+    const unsigned grid = (unsigned)((count + threads - 1) / threads);
+    info_finalize_kernel<<<grid, threads, 0, stream>>>(key, d_info, count);
+    return check_cuda(cudaGetLastError());
+}
+
+static gcm_status_t modify_impl(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
+                                gcm_info_t *d_info, gcm_algo_t algo, cudaStream_t stream) {
+    gcm_status_t st = validate(L, n, ldl, V, k, sigma);
+    if (st != GCM_OK) return st;
+    if (n == 0 || k == 0) {
+        if (d_info) return check_cuda(cudaMemsetAsync(d_info, 0, sizeof(gcm_info_t), stream));
+        return GCM_OK;
+    }
+    algo = pick_algo(n, k, algo);
+    const int64_t nblk = (n + kD - 1) / kD;
+    size_t bytes = (size_t)nblk * panel_doubles((int)std::min<int64_t>(k, kKMax)) * sizeof(double);
+    if (algo == GCM_ALGO_BLOCKED) bytes = std::max(bytes, blocked_workspace_bytes(n, k));
+    Workspace *ws = nullptr;
+    st = get_workspace(stream, bytes, 1, &ws);
+    if (st != GCM_OK) return st;
+    st = check_cuda(cudaMemsetAsync(ws->key, 0xff, sizeof(unsigned long long), stream));
+    if (st != GCM_OK) return st;
+    if (algo == GCM_ALGO_BLOCKED)
+        st = modify_blocked(L, n, ldl, V, k, sigma, ws->key, stream);
+    else
+        st = modify_sweep(L, n, ldl, V, k, sigma, ws->key, ws->panels, stream);
+    if (st != GCM_OK) return st;
+    return finalize_info(ws->key, d_info, 1, stream);
+}
+
+}  // namespace gcm
+
+using namespace gcm;
+
+extern "C" {
+
+gcm_status_t gcm_modify(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma, gcm_stream_t stream) {
+    return modify_impl(L, n, ldl, V, k, sigma, nullptr, GCM_ALGO_AUTO, (cudaStream_t)stream);
+}
+
+gcm_status_t gcm_modify_info(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma, gcm_info_t *d_info,
+                             gcm_stream_t stream) {
+    return modify_impl(L, n, ldl, V, k, sigma, d_info, GCM_ALGO_AUTO, (cudaStream_t)stream);
+}
+
+gcm_status_t gcm_modify_ex(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma, gcm_info_t *d_info,
+                           gcm_algo_t algo, gcm_stream_t stream) {
+    if (algo != GCM_ALGO_AUTO && algo != GCM_ALGO_SWEEP && algo != GCM_ALGO_BLOCKED) return GCM_EINVAL;
+    return modify_impl(L, n, ldl, V, k, sigma, d_info, algo, (cudaStream_t)stream);
+}
+
+gcm_status_t gcm_modify_host(double *L_host, int64_t n, int64_t ldl, double *V_host, int64_t k, int sigma,
+                             gcm_info_t *h_info) {
+    gcm_status_t st = validate(L_host, n, ldl, V_host, k, sigma);
+    if (st != GCM_OK) return st;
+    if (n == 0 || k == 0) {
+        if (h_info) std::memset(h_info, 0, sizeof(*h_info));
+        return GCM_OK;
+    }
+    static std::mutex m;
+    static std::map<int, std::pair<cudaStream_t, void *>> bufs;  // device -> (stream, buffer)
+    static std::map<int, size_t> cap;
+    std::lock_guard<std::mutex> lock(m);
+    int dev = 0;
+    st = check_cuda(cudaGetDevice(&dev));
+    if (st != GCM_OK) return st;
+    auto &slot = bufs[dev];
+    if (!slot.first) {
+        st = check_cuda(cudaStreamCreateWithFlags(&slot.first, cudaStreamNonBlocking));
+        if (st != GCM_OK) return st;
+    }
+    const size_t lbytes = (size_t)n * ldl * sizeof(double), vbytes = (size_t)n * k * sizeof(double);
+    const size_t need = lbytes + vbytes + 256 + sizeof(gcm_info_t);
+    if (cap[dev] < need) {
+        if (slot.second) cudaFree(slot.second);
+        slot.second = nullptr;
+        st = check_cuda(cudaMalloc(&slot.second, need));
+        if (st != GCM_OK) return st;
+        cap[dev] = need;
+    }
+    cudaStream_t s = slot.first;
+    char *base = static_cast<char *>(slot.second);
+    double *dL = reinterpret_cast<double *>(base);
+    double *dV = reinterpret_cast<double *>(base + lbytes);
+    gcm_info_t *dinfo = reinterpret_cast<gcm_info_t *>(base + ((lbytes + vbytes + 255) / 256) * 256);
+    st = check_cuda(cudaMemcpyAsync(dL, L_host, lbytes, cudaMemcpyHostToDevice, s));
+    if (st == GCM_OK) st = check_cuda(cudaMemcpyAsync(dV, V_host, vbytes, cudaMemcpyHostToDevice, s));
+    if (st == GCM_OK) st = modify_impl(dL, n, ldl, dV, k, sigma, dinfo, GCM_ALGO_AUTO, s);
+    if (st == GCM_OK) st = check_cuda(cudaMemcpyAsync(L_host, dL, lbytes, cudaMemcpyDeviceToHost, s));
+    if (st == GCM_OK) st = check_cuda(cudaMemcpyAsync(V_host, dV, vbytes, cudaMemcpyDeviceToHost, s));
+    if (st == GCM_OK && h_info)
+        st = check_cuda(cudaMemcpyAsync(h_info, dinfo, sizeof(gcm_info_t), cudaMemcpyDeviceToHost, s));
+    const gcm_status_t sync = check_cuda(cudaStreamSynchronize(s));
+    return st != GCM_OK ? st : sync;
+}
+
+gcm_status_t gcm_modify_batched(double *L, int64_t n, int64_t ldl, int64_t strideL, double *V, int64_t strideV,
+                                int64_t k, int sigma, int64_t batch, gcm_info_t *d_info, gcm_stream_t stream) {
+    if (batch < 0) return GCM_EINVAL;
+    gcm_status_t st = validate(L, n, ldl, V, k, sigma);
+    if (st != GCM_OK) return st;
+    if (batch > 1 && (strideL < ldl * n || strideV < n * k)) return GCM_EINVAL;
+    if (batch == 0) return GCM_OK;
+    if (n == 0 || k == 0) {
+        if (d_info) return check_cuda(cudaMemsetAsync(d_info, 0, sizeof(gcm_info_t) * batch, (cudaStream_t)stream));
+        return GCM_OK;
+    }
+    return modify_batched(L, n, ldl, strideL, V, strideV, k, sigma, batch, d_info, (cudaStream_t)stream);
+}
+
+const char *gcm_status_string(gcm_status_t s) {
+    switch (s) {
+        case GCM_OK: return "GCM_OK";
+        case GCM_EINVAL: return "GCM_EINVAL: invalid argument";
+        case GCM_ECUDA: return "GCM_ECUDA: CUDA launch or runtime error";
+        case GCM_ENOMEM: return "GCM_ENOMEM: device allocation failed";
+        case GCM_ENCCL: return "GCM_ENCCL: NCCL error";
+        case GCM_ENOTSUP: return "GCM_ENOTSUP: not supported in this build";
+    }
+    return "unknown gcm status";
+}
+
+gcm_status_t gcm_release_workspace(void) {
+    std::lock_guard<std::mutex> lock(g_ws_mutex);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : g_ws) {
+        if (kv.second.key) {
+            cudaSetDevice(kv.first.first);
+            cudaStreamSynchronize(kv.first.second);
+            cudaFree(kv.second.key);
+        }
+    }
+    g_ws.clear();
+    cudaSetDevice(cur);
+    return GCM_OK;
+}
+
+const char *gcm_version(void) { return "gcm 0.1 sm_100a"; }
+
+}  // extern "C"

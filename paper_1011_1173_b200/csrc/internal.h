@@ -1,0 +1,56 @@
+// internal.h -- shared host/device declarations of the gcm library (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gcm.h"
+
+namespace gcm {
+
+// Row-block height D of the sweep: one diagonal chain block / one Apply panel
+// covers D rows (the paper's fixed BlocksPerKernel x
+// ThreadsPerBlock = 896, is Fermi-era prior art).
+constexpr int kD = 64;
+// Widest rank handled in one pass; larger k runs as ceil(k/kKMax) sequential
+// passes over the same L (k sequential rank-1 sweeps, R3).
+constexpr int kKMax = 64;
+
+// Per-row-block coefficient panel (fp64, in global memory, L2-resident):
+//   gd[(j*k + e)*2 + 0] = gamma_{j,e}   gd[(j*k + e)*2 + 1] = delta_{j,e}
+//   rho[j]  at offset 2*D*k,  nu[e] at offset 2*D*k + D.
+// gamma/delta/rho/nu are the rotation (c_{j,e}, s_{j,e}) of PAPER.md 44-49
+// restated for the scaled 2-FMA Apply.
+__host__ __device__ inline int64_t panel_doubles(int k) { return 2ll * kD * k + kD + k; }
+
+// Failure key: atomicMin over ((e << 41) | (row << 1) | (code == 2 ? 0 : 1)),
+// i.e. lexicographic (e, row) with code 2 first at equal (e, row).
+__host__ __device__ inline unsigned long long info_key(int64_t e, int64_t row, int code) {
+    return ((unsigned long long)e << 41) | ((unsigned long long)row << 1) | (code == 2 ? 0ull : 1ull);
+}
+constexpr unsigned long long kInfoNone = ~0ull;
+
+struct Workspace {
+    double *panels = nullptr;          // NB panels
+    unsigned long long *key = nullptr; // failure key (batched: one per factor)
+    void *extra = nullptr;             // algorithm-specific scratch
+    size_t bytes = 0;
+};
+
+// Returns a workspace of at least `bytes` bytes (+ key) for (current device, stream).
+gcm_status_t get_workspace(cudaStream_t stream, size_t bytes, size_t nkeys, Workspace **ws);
+
+gcm_status_t check_cuda(cudaError_t e);
+
+// algorithms (enqueue only; arguments already validated, n > 0, k > 0)
+gcm_status_t modify_sweep(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
+                          unsigned long long *key, double *panels, cudaStream_t stream);
+gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
+                            unsigned long long *key, cudaStream_t stream);
+size_t blocked_workspace_bytes(int64_t n, int64_t k);
+gcm_status_t modify_batched(double *L, int64_t n, int64_t ldl, int64_t strideL, double *V,
+                            int64_t strideV, int64_t k, int sigma, int64_t batch,
+                            gcm_info_t *d_info, cudaStream_t stream);
+gcm_status_t finalize_info(const unsigned long long *key, gcm_info_t *d_info, int64_t count,
+                           cudaStream_t stream);
+
+}  // namespace gcm

@@ -1,0 +1,109 @@
+// rot.cuh -- device building blocks of the sweep: the row Compute (diagonal
+// chain) and the scaled 2-FMA Apply.  Shared by every algorithm of the library.
+//
+// Paper, for row j, update column e, column m > j:
+//   Compute: w = sqrt(d^2 + sigma v^2), c = w/d, s = v/d, L_jj <- w
+//   Apply:   L_jm <- (L_jm + sigma s V_me)/c ;  V_me <- c V_me - s L_jm(new)
+// Restatement used here (exact in real arithmetic,
+// rounding-only differences; keeps the paper's mixed form: V uses the NEW L):
+//   x_{j,e}   = L_jj^2 + sigma sum_{e'<=e} v_{j,e'}^2  (= w_{j,e}^2, no sqrt on the chain)
+//   mu_{j,e}  = prod_{rows j' of the block, j'<=j} w_{j',e-1}/w_{j',e} = prod 1/c
+//   Vt        = mu_{j-1,e} V   (scaled V state; mu = 1 at the start of a row block)
+//   Lh        = (w_{j,e}/L_jj) L^{(e)}  (scaled L, starts as the raw L_jm)
+//   Apply(j,e,m):  Lh += gamma_{j,e} Vt_e ;  Vt_e -= delta_{j,e} Lh      (2 FMA)
+//   with gamma = sigma vt IM_{j-1,e} / L_jj,  delta = vt L_jj / x_{j,e},
+//   IM = 1/mu^2, vt = mu_{j-1,e} v_{j,e};  finally L_jm = Lh * rho_j,
+//   rho_j = L_jj / w_{j,k-1};  at the end of the block V = Vt * nu_e,
+//   nu_e = sqrt(IM_{last,e}) = 1/mu_{last,e}.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace gcm {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ void record_failure(unsigned long long *key, int64_t e, int64_t row, int code) {
+    atomicMin(key, info_key(e, row, code));
+}
+
+// Row Compute for one row j, executed by ONE full warp (lane = update column
+// within a chunk of 32).  Inputs: d0 = L_jj on entry, vrow[e] = vt_{j,e}
+// (scaled residual, shared memory), IM[e] = 1/mu^2_{j-1,e} (shared, updated
+// in place to 1/mu^2_{j,e}).  Outputs: cs[e] = (gamma, delta) in shared memory,
+// optionally mirrored to gpanel[2e..2e+1] (global), V_exit[e*ldv] = v_{j,e}
+// (true residual, PAPER.md 105) if vexit != nullptr.  Returns w = L~_jj on all
+// lanes.  grow = global row index, ebase = index of update column 0 of this
+// pass (for failure reports).
+__device__ __forceinline__ double compute_row_warp(int lane, double d0, const double *vrow, double *IM,
+                                                   double2 *cs, double *gpanel, double *vexit, int64_t ldv,
+                                                   int k, int sigma, int64_t grow, int64_t ebase,
+                                                   unsigned long long *key) {
+    double d = d0;
+    if (!(d > 0.0)) {  // non-positive pivot on entry (R5)
+        if (lane == 0) record_failure(key, ebase, grow, 2);
+        d = __longlong_as_double(0x7ff8000000000000ll);
+    }
+    const double invd = 1.0 / d;
+    double base = d * d;       // x_{j,-1}
+    double rbase = invd * invd;
+    for (int c0 = 0; c0 < k; c0 += 32) {
+        const int e = c0 + lane;
+        const bool valid = e < k;
+        const double vt = valid ? vrow[e] : 0.0;
+        const double im = valid ? IM[e] : 1.0;
+        const double a = sigma > 0 ? vt * im : -(vt * im);  // sigma vt IM
+        // inclusive scan over lanes of a*vt  ->  x_{j,e} = x_{j,c0-1} + scan
+        double s = a * vt;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double y = __shfl_up_sync(kFull, s, off);
+            if (lane >= off) s += y;
+        }
+        double x = base + s;
+        const bool bad = valid && !(x > 0.0);
+        const unsigned badmask = __ballot_sync(kFull, bad);
+        if (badmask) {
+            const int first = __ffs(badmask) - 1;
+            if (lane == first) record_failure(key, ebase + e, grow, 1);
+            if (lane >= first) x = __longlong_as_double(0x7ff8000000000000ll);
+        }
+        const double rx = 1.0 / x;
+        double rxp = __shfl_up_sync(kFull, rx, 1);
+        if (lane == 0) rxp = rbase;
+        if (valid) {
+            const double gam = a * invd;
+            const double del = vt * d * rx;
+            IM[e] = im * x * rxp;
+            cs[e] = make_double2(gam, del);
+            if (gpanel) {
+                gpanel[2 * e] = gam;
+                gpanel[2 * e + 1] = del;
+            }
+            if (vexit) vexit[(int64_t)e * ldv] = vt * sqrt(im);
+        }
+        base = __shfl_sync(kFull, x, 31);
+        rbase = __shfl_sync(kFull, rx, 31);
+    }
+    return sqrt(base);
+}
+
+// Apply the k rotations of one row (coefficients cs[0..k-1] in shared memory)
+// to one (L element, V state) pair held by this thread; returns the final L.
+template <int KMAX>
+__device__ __forceinline__ double apply_row(double l, double (&v)[KMAX], const double2 *cs, double rho, int k) {
+#pragma unroll
+    for (int e = 0; e < KMAX; ++e) {
+        if (e < k) {
+            const double2 gd = cs[e];
+            l = fma(gd.x, v[e], l);
+            v[e] = fma(-gd.y, l, v[e]);
+        }
+    }
+    return l * rho;
+}
+
+}  // namespace gcm
