@@ -50,7 +50,7 @@ def lib():
     """Load libgcm.so.  Raises if it is missing: there is no CPU fallback."""
     global _lib
     if _lib is None:
-        path = _build.LIB
+        path = os.environ.get("GCM_LIB_PATH", _build.LIB)  # experiments may point at a variant build
         if not os.path.exists(path):
             raise RuntimeError(
                 f"{path} is missing: build it with `python -m paper_1011_1173_b200._build` "

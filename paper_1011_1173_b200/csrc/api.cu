@@ -81,8 +81,12 @@ gcm_status_t get_workspace(cudaStream_t stream, size_t bytes, size_t nkeys, Work
         void *p = nullptr;
         st = check_cuda(cudaMalloc(&p, alloc));
         if (st != GCM_OK) return st;
+        // device flags compare against a per-call epoch: start from all-zero
+        st = check_cuda(cudaMemsetAsync(p, 0, alloc, stream));
+        if (st != GCM_OK) return st;
         ws.key = static_cast<unsigned long long *>(p);
         ws.bytes = alloc;
+        ws.epoch = 0;
     }
     ws.panels = reinterpret_cast<double *>(reinterpret_cast<char *>(ws.key) + key_bytes);
     ws.extra = ws.panels;

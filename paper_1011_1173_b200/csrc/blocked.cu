@@ -1,8 +1,923 @@
-// blocked.cu -- GCM_ALGO_BLOCKED (chain-shortened single-factor path). Not yet built.
+// blocked.cu -- GCM_ALGO_BLOCKED: the chain-shortened single-factor path.
+//
+// The paper's sweep (CholeskyModifyA, PAPER.md 24-30) has a serial chain of
+// n + k - 1 Compute links (each a sqrt/div) because row block b cannot start
+// before the V entries of its columns have been rotated by every earlier row.
+// Those V states have a closed form:
+//
+//   P = L^{-T} V,  G_b = P_{<b}^T P_{<b},  U_b = chol_lower(I + sigma G_b),
+//   V-state of column m at the start of row block b  =  U_b^{-1} r_m^{(b)},
+//   r_m^{(b)} = v_m - sum_{i < bD} L_{i,m} p_i  (the forward-substitution residual),
+//
+// which is exact (U_b^{-1} is the product of the lower-triangular k x k maps the
+// rotations of rows < bD induce on V, the unique one with U^{-T}... = (I+sigma G)^{-1}).
+// So every diagonal block runs the paper's Compute/Apply sweep INDEPENDENTLY
+// (same rotations, same V_exit up to rounding) and every off-diagonal D x D tile
+// is an independent Apply task.  The only serial chain left is the triangular
+// solve for P, whose links are one FMA + one MUL instead of a sqrt/div chain.
+//
+// Kernels (one pass per <= 32 update columns; k > 32 runs ceil(k/32) passes =
+// sequential rank-32 modifications, R3):
+//   trsv_kernel        persistent, cooperative: CTAs 0..NC-1 = the chains (P in
+//                      32-row blocks, kRPC right-hand sides each, lookahead
+//                      kLookC blocks), CTAs NC.. = strip owners
+//                      (right-looking residual updates + Apply checkpoints) and
+//                      diagonal-block inverses; device flags, no per-block launch.
+//   gram_kernel        Q_b = P_b^T P_b per 64-row block.
+//   bdiag_kernel       per 64-block (all in parallel): G_b, U_b, V-state, in-block
+//                      sweep (rot.cuh block_sweep) -> coefficient panel, V_exit, L~_bb.
+//   bapply_kernel      per (tile segment, column strip): V-state from the
+//                      checkpoint, then the scaled 2-FMA Apply of the panels.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "internal.h"
+#include "rot.cuh"
+
 namespace gcm {
-size_t blocked_workspace_bytes(int64_t, int64_t) { return 0; }
-gcm_status_t modify_blocked(double *, int64_t, int64_t, double *, int64_t, int, unsigned long long *, cudaStream_t) {
-    return GCM_ENOTSUP;
+
+namespace {
+
+constexpr int kDT = 32;            // rows per triangular-solve block
+constexpr int kTrsvThreads = 256;
+constexpr int kBKMax = 32;         // update columns per pass
+constexpr int kApplyT = 64;        // threads per apply CTA (= kD columns)
+
+struct Layout {
+    int64_t n;
+    int k;
+    int NT, NB, CI;
+    int64_t nchk;
+    size_t P, rcur, rchain, MX, chk, Q, G, U, panels, flags, total;
+};
+
+__host__ __device__ inline int64_t chk_count_before(int64_t s, int CI) {
+    // sum_{s'=1}^{s-1} ceil(s'/CI)
+    const int64_t S = s - 1;
+    if (S <= 0) return 0;
+    const int64_t q = S / CI, r = S % CI;
+    return CI * q * (q + 1) / 2 + (q + 1) * r;
 }
+
+Layout make_layout(int64_t n, int k, size_t chk_budget) {
+    Layout l{};
+    l.n = n;
+    l.k = k;
+    l.NT = (int)((n + kDT - 1) / kDT);
+    l.NB = (int)((n + kD - 1) / kD);
+    l.CI = 1;
+    for (;;) {
+        l.nchk = chk_count_before(l.NB, l.CI);
+        if ((size_t)l.nchk * kD * k * sizeof(double) <= chk_budget || l.CI >= l.NB) break;
+        l.CI *= 2;
+    }
+    size_t o = 0;
+    auto take = [&](size_t doubles) {
+        const size_t at = o;
+        o += ((doubles * sizeof(double) + 255) / 256) * 256;
+        return at;
+    };
+    l.P = take((size_t)n * k);
+    l.rcur = take((size_t)l.NT * kDT * k);
+    l.rchain = take((size_t)l.NT * kDT * k);
+    l.MX = take((size_t)l.NT * 2 * kDT * kDT);
+    l.chk = take((size_t)l.nchk * kD * k);
+    l.Q = take((size_t)l.NB * k * k);
+    l.G = take((size_t)l.NB * k * k);
+    l.U = take((size_t)l.NB * k * k);
+    l.panels = take((size_t)l.NB * panel_doubles(k));
+    l.flags = take((2ull * l.NT * sizeof(unsigned) + 16 * sizeof(unsigned long long) + 7) / 8);  // prog[16], rflag, lflag
+    l.total = o;
+    return l;
+}
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+#ifdef GCM_TRACE
+__device__ long long g_trace[4096 * 8];
+#define TRACE(slot, tb) (blockIdx.x == 0 ? (void)(g_trace[(tb) * 8 + (slot)] = clock64()) : (void)0)
+#else
+#define TRACE(slot, tb) ((void)0)
+#endif
+
+constexpr size_t kChkBudget = 2ull << 30;  // bytes of Apply checkpoints before CI doubles
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// CTA-wide wait until *f == epoch (thread 0 spins; acquire, then barrier).
+__device__ __forceinline__ void cta_wait(const unsigned *f, unsigned epoch, bool sleep) {
+    if (threadIdx.x == 0) {
+        while (ld_acquire(f) != epoch) {
+            if (sleep) __nanosleep(64);
+        }
+    }
+    __syncthreads();
+}
+// CTA-wide publish: every thread's prior global stores, then *f = epoch.
+__device__ __forceinline__ void cta_publish(unsigned *f, unsigned epoch) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(f, epoch);
+    }
+}
+
+struct TrsvArgs {
+    const double *L;
+    int64_t n, ldl;
+    const double *V;  // this pass's first column (ld n)
+    int k;
+    double *P, *rcur, *rchain, *chk;
+    double *MX;       // per 32-block: M^T (row-major) then X (row-major), X = L_bb^{-1}, M = X^T L_{b-1,b}^T
+    bool bulk_ok;     // L 16-byte aligned and ldl even: TMA bulk copies of column segments
+    int CI;
+    int NC;           // chain CTAs (each solves kRPC right-hand sides)
+    unsigned long long *prog;  // [NC] chain progress: (epoch << 32) | blocks published
+    unsigned *rflag, *lflag;
+    unsigned epoch;
+};
+
+constexpr int kRPC = 2;                 // right-hand sides per chain CTA
+#ifndef GCM_LOOKC
+#define GCM_LOOKC 4
+#endif
+constexpr int kLookC = GCM_LOOKC;       // blocks of lookahead the chain absorbs
+constexpr int kPrepWarps = 4;           // chain CTA warps: 0..kRPC-1 critical, then prep, publisher, loader
+constexpr int kPrepThreads = kPrepWarps * 32;
+constexpr int kSvcWarp = kRPC + kPrepWarps;  // publisher warp; kSvcWarp + 1 = loader warp
+constexpr int kSeg = (kLookC - 1) * kDT;  // rows of the prepared part of a lookahead segment
+constexpr int kLdS = kSeg + 2;            // smem stride of a segment column (even: 16-byte bulk copies)
+constexpr int kLdT = kDT + 1;
+constexpr int kHelpMaxOwn = 4;          // strips whose residual a helper keeps in shared memory
+static_assert((kSvcWarp + 2) * 32 <= kTrsvThreads, "chain CTA needs publisher and loader warps");
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred P;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem_dst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Shared-memory plan of a chain CTA (doubles).  A "stage" holds the operands of
+// one row block tb: the lookahead segment (rows (tb-kLookC)*32 .. (tb-1)*32-1 of
+// the block's 32 columns), M_tb^T and X_tb (row-major).  Three stages rotate.
+struct ChainSmem {
+    static constexpr int seg = kDT * kLdS;
+    static constexpr int stage = seg + 2 * kDT * kDT;
+    static constexpr int off_stage = 0;                                   // [3][stage]
+    static constexpr int off_pwin = off_stage + 3 * stage;                // [kLookC][kDT][kRPC]
+    static constexpr int off_part = off_pwin + kLookC * kDT * kRPC;       // [kPrepWarps][kDT][kRPC]
+    static constexpr int off_acc = off_part + kPrepWarps * kDT * kRPC;    // [kDT][kRPC]
+    static constexpr int off_prepx = off_acc + kDT * kRPC;                // [2][kDT][kRPC]
+    static constexpr int off_bar = off_prepx + 2 * kDT * kRPC;            // 3 mbarriers (u64)
+    static constexpr int total = off_bar + 4;
+};
+
+// ---------------------------------------------------------------- chain CTA
+// CTA c solves L^T p = v for the right-hand sides e = kRPC*c .. kRPC*c+kRPC-1,
+// 32 rows (one block tb) per step:
+//   critical warps (one per RHS, lane = row j):  p_tb = prepX_tb - M_tb p_{tb-1}
+//        with M_tb = X_tb^T L_{tb-1,tb}^T precomputed by the helpers (X_tb = L_tb,tb^{-1});
+//   prep warps: prepX_{tb+1} = X_{tb+1}^T ( r^{(tb+1-kLookC)} - sum_{i=2..kLookC} L_{tb+1-i,tb+1}^T p_{tb+1-i} ),
+//        r^{(.)} handed over by the helper owning strip tb+1;
+//   service warp: publishes progress and streams block tb+3's operands with TMA
+//        bulk copies (one per column segment) on a per-stage mbarrier.
+// The k right-hand sides are independent, so chain CTAs never talk to each other.
+__device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
+    using S = ChainSmem;
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int NT = (int)((a.n + kDT - 1) / kDT);
+    const int k = a.k;
+    const int e0 = c * kRPC;
+    double *pwin = smem + S::off_pwin;
+    double *part = smem + S::off_part;
+    double *accs = smem + S::off_acc;
+    double *prepx = smem + S::off_prepx;
+    unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + S::off_bar);
+    auto stage_of = [&](int tb) { return smem + S::off_stage + (tb % 3) * S::stage; };
+    const bool bulk = a.bulk_ok;
+
+    // service warp: bring block tb's operands into stage tb % 3
+    auto issue_loads = [&](int tb) {
+        double *st = stage_of(tb);
+        unsigned long long *bar = bars + (tb % 3);
+        const int64_t c0 = (int64_t)tb * kDT;
+        const int nc = (int)imin64(kDT, a.n - c0);
+        const int64_t rs = (int64_t)(tb - kLookC) * kDT;  // first segment row (may be < 0)
+        const int skip = rs < 0 ? (int)imin64(-rs, kSeg) : 0;
+        if (lane == 0)
+            while (ld_acquire(a.lflag + tb) != a.epoch) {
+            }
+        __syncwarp();
+        if (bulk) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // helpers' generic stores -> TMA reads
+                const unsigned segb = (unsigned)(kSeg - skip) * 8u;
+                const unsigned bytes = (unsigned)nc * segb + 2u * kDT * kDT * 8u;
+                mbar_arrive_expect_tx(bar, bytes);
+                if (segb)
+                    for (int j = 0; j < nc; ++j)
+                        bulk_g2s(st + j * kLdS + skip, a.L + (rs + skip) + (c0 + j) * a.ldl, segb, bar);
+                bulk_g2s(st + S::seg, a.MX + (int64_t)tb * 2 * kDT * kDT, 2u * kDT * kDT * 8u, bar);
+            }
+        } else {
+            for (int j = 0; j < nc; ++j)
+                for (int r = skip + lane; r < kSeg; r += 32)
+                    cp_async8(st + j * kLdS + r, a.L + (rs + r) + (c0 + j) * a.ldl);
+            for (int i = lane; i < 2 * kDT * kDT; i += 32)
+                cp_async8(st + S::seg + i, a.MX + (int64_t)tb * 2 * kDT * kDT + i);
+            cp_async_commit();
+            cp_async_wait_all();
+            mbar_arrive(bar);
+        }
+    };
+
+    // critical warps count published p blocks here (monotonic; a named barrier
+    // could be overrun because the critical warps may run two steps ahead of the
+    // service warp)
+    volatile unsigned *pcount = reinterpret_cast<volatile unsigned *>(bars + 3);
+    if (t == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init(bars + i, bulk ? 1u : 32u);
+        *pcount = 0u;
+    }
+    __syncthreads();
+    if (warp == kSvcWarp + 1)
+        for (int tb = 0; tb < 3 && tb < NT; ++tb) issue_loads(tb);
+
+    // prep warps: prepX for block tb (needs p up to tb-2, i.e. <= step tb-1 of the critical warps)
+    const int pt = t - kRPC * 32;
+    auto do_prep = [&](int tb) {
+        const double *st = stage_of(tb);
+        mbar_wait(bars + (tb % 3), (unsigned)((tb / 3) & 1));
+        if (pt == 0) TRACE(3, tb - 1);
+        const int pw = pt >> 5, j = lane;
+        // tasks: (lookahead block i = 2..kLookC, half h of its 32 rows); lane j = column
+        constexpr int kTasks = 2 * (kLookC - 1);
+        double acc[kRPC];
+#pragma unroll
+        for (int w = 0; w < kRPC; ++w) acc[w] = 0.0;
+        for (int task = pw; task < kTasks; task += kPrepWarps) {
+            const int i = 2 + (task >> 1), h = task & 1;
+            const int blk = tb - i;
+            if (blk < 0) continue;
+            // segment rows of block blk start at (kLookC - i) * 32
+            const double *col = st + j * kLdS + (kLookC - i) * kDT + h * 16;
+            const double *pp = pwin + ((blk % kLookC) * kDT + h * 16) * kRPC;
+            double s0[kRPC], s1[kRPC];
+#pragma unroll
+            for (int w = 0; w < kRPC; ++w) s0[w] = s1[w] = 0.0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int m = (q + j) & 15;  // per-lane rotation: spreads the even-stride reads over banks
+                const double l = col[m];
+#pragma unroll
+                for (int w = 0; w < kRPC; ++w) {
+                    if (q & 1) s1[w] = fma(-l, pp[m * kRPC + w], s1[w]);
+                    else s0[w] = fma(-l, pp[m * kRPC + w], s0[w]);
+                }
+            }
+#pragma unroll
+            for (int w = 0; w < kRPC; ++w) acc[w] += s0[w] + s1[w];
+        }
+#pragma unroll
+        for (int w = 0; w < kRPC; ++w) part[(pw * kDT + j) * kRPC + w] = acc[w];
+        if (pt == 0) TRACE(4, tb - 1);
+        if (pt == 0)
+            while (ld_acquire(a.rflag + tb) != a.epoch) {
+            }
+        if (pt == 0) TRACE(5, tb - 1);
+        named_bar(2, kPrepThreads);
+        if (pt < kDT * kRPC) {
+            const int jj = pt / kRPC, w = pt % kRPC;
+            const int e = e0 + w;
+            const int64_t row = (int64_t)tb * kDT + jj;
+            double acc = (e < k && row < a.n) ? __ldcg(a.rchain + (int64_t)tb * kDT * k + (int64_t)jj * k + e) : 0.0;
+#pragma unroll
+            for (int q = 0; q < kPrepWarps; ++q) acc += part[(q * kDT + jj) * kRPC + w];
+            accs[jj * kRPC + w] = acc;
+        }
+        named_bar(2, kPrepThreads);
+        if (pt < kDT * kRPC) {  // prepX[j][w] = sum_q X(q, j) acc[q][w]   (X row-major in the stage)
+            const int jj = pt % kDT, w = pt / kDT;
+            const double *X = st + S::seg + kDT * kDT;
+            double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < kDT; q += 2) {
+                x0 = fma(X[q * kDT + jj], accs[q * kRPC + w], x0);
+                x1 = fma(X[(q + 1) * kDT + jj], accs[(q + 1) * kRPC + w], x1);
+            }
+            prepx[(tb & 1) * kDT * kRPC + jj * kRPC + w] = x0 + x1;
+        }
+    };
+
+    double mrow[kDT];  // critical warps: row j of M_tb in registers
+    if (warp >= kRPC && warp < kSvcWarp) do_prep(0);
+    if (warp < kRPC) {
+        const double *st = stage_of(0);
+        mbar_wait(bars + 0, 0u);
+#pragma unroll
+        for (int m = 0; m < kDT; ++m) mrow[m] = st[S::seg + m * kDT + lane];  // M^T stored: (m, j)
+    }
+    if (warp < kSvcWarp) named_bar(1, kSvcWarp * 32);  // B_0
+
+    if (warp == kSvcWarp) {  // publisher: no memory traffic of its own, so its fence is cheap
+        for (int tb = 0; tb < NT; ++tb) {
+            if (lane == 0) {
+                while (*pcount < (unsigned)(kRPC * (tb + 1))) {
+                }
+                __threadfence();
+                st_release64(a.prog + c, ((unsigned long long)a.epoch << 32) | (unsigned)(tb + 1));
+            }
+            __syncwarp();
+        }
+        return;
+    }
+    if (warp == kSvcWarp + 1) {  // loader: block tb+3 into stage tb%3 once step tb is under way
+        for (int tb = 0; tb + 3 < NT; ++tb) {
+            if (lane == 0)
+                while (*pcount < (unsigned)(kRPC * (tb + 1))) {
+                }
+            __syncwarp();
+            issue_loads(tb + 3);
+            if (lane == 0) TRACE(7, tb);
+        }
+        return;
+    }
+    if (warp > kSvcWarp + 1) return;
+    for (int tb = 0; tb < NT; ++tb) {
+        if (warp < kRPC) {
+            const int w = warp, j = lane;
+            if (t == 0) TRACE(0, tb);
+            double a0 = prepx[(tb & 1) * kDT * kRPC + j * kRPC + w], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (tb > 0) {
+                const double *pprev = pwin + ((tb - 1) % kLookC) * kDT * kRPC + w;
+#pragma unroll
+                for (int m = 0; m < kDT; m += 4) {
+                    a0 = fma(-mrow[m], pprev[m * kRPC], a0);
+                    a1 = fma(-mrow[m + 1], pprev[(m + 1) * kRPC], a1);
+                    a2 = fma(-mrow[m + 2], pprev[(m + 2) * kRPC], a2);
+                    a3 = fma(-mrow[m + 3], pprev[(m + 3) * kRPC], a3);
+                }
+            }
+            const double p = (a0 + a1) + (a2 + a3);
+            pwin[((tb % kLookC) * kDT + j) * kRPC + w] = p;
+            const int e = e0 + w;
+            const int64_t row = (int64_t)tb * kDT + j;
+            if (e < k && row < a.n) a.P[row * k + e] = p;
+            if (t == 0) TRACE(1, tb);
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                atomicAdd(const_cast<unsigned *>(pcount), 1u);
+            }
+            if (tb + 1 < NT) {  // M_{tb+1} row into registers while the prep warps finish
+                const double *st = stage_of(tb + 1);
+                mbar_wait(bars + ((tb + 1) % 3), (unsigned)(((tb + 1) / 3) & 1));
+#pragma unroll
+                for (int m = 0; m < kDT; ++m) mrow[m] = st[S::seg + m * kDT + lane];
+            }
+        } else if (tb + 1 < NT) {
+            if (pt == 0) TRACE(2, tb);
+            do_prep(tb + 1);
+            if (pt == 0) TRACE(6, tb);
+        }
+        named_bar(1, kSvcWarp * 32);  // B_{tb+1}: p_tb and prepX_{tb+1} ready
+    }
+}
+
+// ---------------------------------------------------------------- helper CTAs
+template <int KB>
+__device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
+    constexpr int NQ = (kDT * KB + kTrsvThreads - 1) / kTrsvThreads;
+    double *Lb = smem;                      // [kDT][kLdT]
+    double *Pt = Lb + kDT * kLdT;           // [kDT][max(KB, kLdT)]  (P block; X during J1)
+    double *rs = Pt + kDT * (KB > kLdT ? KB : kLdT);  // [kHelpMaxOwn][kDT][KB] residuals of owned strips
+    const int t = threadIdx.x;
+    const int k = a.k;
+    const int NT = (int)((a.n + kDT - 1) / kDT);
+
+    // J1: per 32-block tb: X = L_tb,tb^{-1} (upper) and M = X^T L_{tb-1,tb}^T, the
+    // operands of the chain's critical step  p_tb = X^T prep - M p_{tb-1}.
+    for (int tb = h; tb < NT; tb += H) {
+        const int64_t r0 = (int64_t)tb * kDT;
+        const int nr = (int)imin64(kDT, a.n - r0);
+        double *Xs = Pt;  // reuse: [kDT][kLdT]  Xs[q][j] = X(q, j)   (needs kDT*kLdT <= kDT*KB + ... see smem plan)
+        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
+            const int c = idx / kDT, m = idx % kDT;
+            double v = 0.0;
+            if (c < nr && m <= c) v = a.L[(r0 + m) + (r0 + c) * a.ldl];
+            else if (c >= nr && m == c) v = 1.0;  // identity padding
+            Lb[c * kLdT + m] = v;
+        }
+        __syncthreads();
+        if (t < kDT) {
+            const int c = t;
+            double x[kDT];
+#pragma unroll
+            for (int j = kDT - 1; j >= 0; --j) {
+                double s = (j == c) ? 1.0 : 0.0;
+#pragma unroll
+                for (int m = j + 1; m < kDT; ++m) s = fma(-Lb[m * kLdT + j], m <= c ? x[m] : 0.0, s);
+                x[j] = j <= c ? s / Lb[j * kLdT + j] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < kDT; ++j) Xs[j * kLdT + c] = x[j];
+        }
+        __syncthreads();
+        // Lb <- L tile (rows of block tb-1, columns of block tb):  Lb[q][m] = L(row (tb-1)*32+m, col tb*32+q)
+        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
+            const int q = idx / kDT, m = idx % kDT;
+            Lb[q * kLdT + m] = (tb > 0 && q < nr) ? a.L[(r0 - kDT + m) + (r0 + q) * a.ldl] : 0.0;
+        }
+        __syncthreads();
+        double *mx = a.MX + (int64_t)tb * 2 * kDT * kDT;
+        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
+            const int m = idx / kDT, j = idx % kDT;  // M(j, m) = sum_q X(q, j) L(m, q)
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+            for (int q = 0; q < kDT; q += 2) {
+                s0 = fma(Xs[q * kLdT + j], Lb[q * kLdT + m], s0);
+                s1 = fma(Xs[(q + 1) * kLdT + j], Lb[(q + 1) * kLdT + m], s1);
+            }
+            mx[m * kDT + j] = s0 + s1;                        // M^T row-major: (m, j)
+            mx[kDT * kDT + m * kDT + j] = Xs[m * kLdT + j];   // X row-major: (q=m, j)
+        }
+        cta_publish(a.lflag + tb, a.epoch);
+    }
+
+    // J2: column strips s = h, h+H, ...
+    auto rptr = [&](int i, int s) -> double * {  // residual of owned strip #i (smem or global)
+        return i < kHelpMaxOwn ? rs + i * kDT * KB : a.rcur + (int64_t)s * kDT * k;
+    };
+    auto rstride = [&](int i) { return i < kHelpMaxOwn ? KB : k; };
+    int last = -1, i = 0;
+    for (int s = h; s < NT; s += H, ++i) {
+        last = s;
+        const int64_t c0 = (int64_t)s * kDT;
+        const int nc = (int)imin64(kDT, a.n - c0);
+        double *r = rptr(i, s);
+        const int ld = rstride(i);
+        for (int o = t; o < kDT * k; o += kTrsvThreads) {
+            const int cc = o / k, e = o % k;
+            const double v = cc < nc ? a.V[(c0 + cc) + (int64_t)e * a.n] : 0.0;
+            r[cc * ld + e] = v;
+            if (s - kLookC <= 0) a.rchain[c0 * k + o] = v;
+            const int s64 = s / 2;
+            if (s64 >= 1 && cc < nc)
+                a.chk[((int64_t)chk_count_before(s64, a.CI)) * kD * k + ((s % 2) * kDT + cc) * k + e] = v;
+        }
+        if (s - kLookC <= 0) cta_publish(a.rflag + s, a.epoch);
+    }
+    __syncthreads();
+    constexpr int NL = (kDT * kDT) / kTrsvThreads;
+    double pre[NL];
+    auto prefetch = [&](int tb, int s) {  // static operand: issue before waiting on the chain
+        const int64_t c0 = (int64_t)s * kDT;
+        const int nc = (int)imin64(kDT, a.n - c0);
+#pragma unroll
+        for (int q = 0; q < NL; ++q) {
+            const int idx = t + q * kTrsvThreads, cc = idx / kDT, m = idx % kDT;
+            pre[q] = cc < nc ? a.L[((int64_t)tb * kDT + m) + (c0 + cc) * a.ldl] : 0.0;
+        }
+    };
+    __shared__ int avail_s;
+    int done = 0;  // blocks of P already applied to the owned strips
+    while (done < last) {
+        // wait until every chain has published beyond `done`; take all available blocks
+        if (t < 32) {
+            unsigned m;
+            for (;;) {
+                unsigned cnt = 0xffffffffu;
+                if (t < a.NC) {
+                    const unsigned long long v = ld_acquire64(a.prog + t);
+                    cnt = (unsigned)(v >> 32) == a.epoch ? (unsigned)v : 0u;
+                }
+                m = __reduce_min_sync(kFull, cnt);
+                if ((int)m > done) break;
+                __nanosleep(64);
+            }
+            if (t == 0) avail_s = (int)m;
+        }
+        __syncthreads();
+        const int avail = min(avail_s, last);
+        for (int tb = done; tb < avail; ++tb) {
+            int sfirst = h;
+            while (sfirst <= tb) sfirst += H;
+            prefetch(tb, sfirst);
+            for (int o = t; o < kDT * KB; o += kTrsvThreads) {
+                const int m = o / KB, e = o % KB;
+                Pt[o] = (e < k && (int64_t)tb * kDT + m < a.n) ? __ldcg(a.P + ((int64_t)tb * kDT + m) * k + e) : 0.0;
+            }
+            int ii = 0;
+            for (int s = h; s < NT; s += H, ++ii) {
+                if (s <= tb) continue;
+                if (s != sfirst) prefetch(tb, s);
+#pragma unroll
+                for (int q = 0; q < NL; ++q) {
+                    const int idx = t + q * kTrsvThreads, cc = idx / kDT, m = idx % kDT;
+                    Lb[cc * kLdT + m] = pre[q];
+                }
+                __syncthreads();
+                const int64_t c0 = (int64_t)s * kDT;
+                const int nc = (int)imin64(kDT, a.n - c0);
+                double *r = rptr(ii, s);
+                const int ld = rstride(ii);
+                double racc[NQ];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int o = t + q * kTrsvThreads;
+                    const int cc = o / KB, e = o % KB;
+                    double s0 = 0.0, s1 = 0.0;
+                    if (o < kDT * KB && cc < nc && e < k) {
+                        s0 = r[cc * ld + e];
+                        const double *Lc = Lb + cc * kLdT;
+#pragma unroll 8
+                        for (int m = 0; m < kDT; m += 2) {
+                            s0 = fma(-Lc[m], Pt[m * KB + e], s0);
+                            s1 = fma(-Lc[m + 1], Pt[(m + 1) * KB + e], s1);
+                        }
+                    }
+                    racc[q] = s0 + s1;
+                }
+                const bool chain_handoff = (tb + 1 == s - kLookC);
+                const int b64 = (tb + 1) / 2, s64 = s / 2;
+                const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 % a.CI == 0);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int o = t + q * kTrsvThreads;
+                    const int cc = o / KB, e = o % KB;
+                    if (o < kDT * KB && cc < nc && e < k) {
+                        const double v = racc[q];
+                        r[cc * ld + e] = v;
+                        if (chain_handoff) a.rchain[c0 * k + (int64_t)cc * k + e] = v;
+                        if (checkpoint)
+                            a.chk[(chk_count_before(s64, a.CI) + b64 / a.CI) * kD * k + ((s % 2) * kDT + cc) * k + e] =
+                                v;
+                    }
+                }
+                if (chain_handoff) cta_publish(a.rflag + s, a.epoch);
+                __syncthreads();  // Lb reuse
+            }
+        }
+        done = avail;
+    }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(TrsvArgs a) {
+    extern __shared__ double smem_trsv[];
+    if ((int)blockIdx.x < a.NC)
+        trsv_chain(a, smem_trsv, blockIdx.x);
+    else
+        trsv_helper<KB>(a, smem_trsv, blockIdx.x - a.NC, gridDim.x - a.NC);
+}
+
+// Q_b = P_b^T P_b over the 64 rows of block b.
+__global__ void gram_kernel(const double *__restrict__ P, int64_t n, int k, double *__restrict__ Q) {
+    const int b = blockIdx.x;
+    const int64_t r0 = (int64_t)b * kD;
+    const int nr = (int)imin64(kD, n - r0);
+    for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
+        const int e1 = o / k, e2 = o % k;
+        double s0 = 0.0, s1 = 0.0;
+        int m = 0;
+        for (; m + 1 < nr; m += 2) {
+            s0 = fma(P[(r0 + m) * k + e1], P[(r0 + m) * k + e2], s0);
+            s1 = fma(P[(r0 + m + 1) * k + e1], P[(r0 + m + 1) * k + e2], s1);
+        }
+        if (m < nr) s0 = fma(P[(r0 + m) * k + e1], P[(r0 + m) * k + e2], s0);
+        Q[(int64_t)b * k * k + o] = s0 + s1;
+    }
+}
+
+// G[b] = sum_{b' < b} Q[b']  (exclusive prefix over row blocks).
+__global__ void gscan_kernel(const double *__restrict__ Q, double *__restrict__ G, int NB, int k) {
+    for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
+        double run = 0.0;
+#pragma unroll 8
+        for (int b = 0; b < NB; ++b) {
+            const double q = __ldg(Q + (int64_t)b * k * k + o);
+            G[(int64_t)b * k * k + o] = run;
+            run += q;
+        }
+    }
+}
+
+// One CTA per 64-row diagonal block, all blocks in parallel.
+template <int KB>
+__global__ void __launch_bounds__(kD) bdiag_kernel(double *__restrict__ L, int64_t n, int64_t ldl,
+                                                   double *__restrict__ V, int k, int sigma,
+                                                   const double *__restrict__ P, const double *__restrict__ Q,
+                                                   double *__restrict__ Uout, double *__restrict__ panels,
+                                                   unsigned long long *key, int64_t ebase) {
+    extern __shared__ double smem_bdiag[];
+    double(*Ls)[kD + 1] = reinterpret_cast<double(*)[kD + 1]>(smem_bdiag);               // [kD][kD+1]
+    double(*Ps)[KB + 1] = reinterpret_cast<double(*)[KB + 1]>(smem_bdiag + kD * (kD + 1)); // [kD][KB+1]
+    double(*M)[KB + 1] = reinterpret_cast<double(*)[KB + 1]>(smem_bdiag + kD * (kD + 1) + kD * (KB + 1));
+    __shared__ double vrow[KB], IM[KB], rho_s;
+    __shared__ double2 cs[KB];
+    const int t = threadIdx.x;
+    const int b = blockIdx.x;
+    const int64_t r0 = (int64_t)b * kD;
+    const int Db = (int)imin64(kD, n - r0);
+
+    // G_b (prefix-summed by gscan_kernel)  ->  M = I + sigma G_b
+    for (int o = t; o < k * k; o += kD) {
+        const double g = Q[(int64_t)b * k * k + o];
+        const int e1 = o / k, e2 = o % k;
+        M[e1][e2] = (e1 == e2 ? 1.0 : 0.0) + (sigma > 0 ? g : -g);
+    }
+    for (int idx = t; idx < kD * kD; idx += kD) {
+        const int m = idx / kD, j = idx % kD;
+        if (m < Db && j <= m) Ls[m][j] = L[(r0 + j) + (r0 + m) * ldl];
+    }
+    for (int o = t; o < kD * k; o += kD) {
+        const int m = o / k, e = o % k;
+        Ps[m][e] = m < Db ? P[(r0 + m) * k + e] : 0.0;
+    }
+    __syncthreads();
+    // U = chol_lower(M) in place (lower triangle), one warp, lane = row
+    if (t < 32) {
+        const int i = t;
+        for (int c = 0; c < k; ++c) {
+            if (i == c) M[c][c] = sqrt(M[c][c]);
+            __syncwarp();
+            if (i > c && i < k) M[i][c] = M[i][c] / M[c][c];
+            __syncwarp();
+            if (i > c && i < k)
+                for (int j = c + 1; j <= i; ++j) M[i][j] = fma(-M[i][c], M[j][c], M[i][j]);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int o = t; o < k * k; o += kD) {
+        const int e1 = o / k, e2 = o % k;
+        Uout[(int64_t)b * k * k + o] = e2 <= e1 ? M[e1][e2] : 0.0;
+    }
+    // V-state of column r0+t: y = U^{-1} (L_bb^T P_b)[t]
+    double v[KB];
+#pragma unroll
+    for (int e = 0; e < KB; ++e) v[e] = 0.0;
+    if (t < Db) {
+        for (int j = 0; j <= t; ++j) {
+            const double l = Ls[t][j];
+#pragma unroll
+            for (int e = 0; e < KB; ++e) v[e] = fma(l, Ps[j][e], v[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            if (e < k) {
+                double s = v[e];
+#pragma unroll
+                for (int ep = 0; ep < e; ++ep) s = fma(-M[e][ep], v[ep], s);
+                v[e] = s / M[e][e];
+            } else {
+                v[e] = 0.0;
+            }
+        }
+    }
+    __syncthreads();
+    double *panel = panels + (int64_t)b * panel_doubles(k);
+    block_sweep<KB, kD + 1>(Ls, v, Db, k, sigma, r0, panel, V + r0, n, key, ebase, vrow, IM, cs, &rho_s);
+    for (int idx = t; idx < kD * kD; idx += kD) {
+        const int m = idx / kD, j = idx % kD;
+        if (m < Db && j <= m) L[(r0 + j) + (r0 + m) * ldl] = Ls[m][j];
+    }
+}
+
+// One CTA per (checkpoint segment g, 64-column strip s): tiles b in
+// [g*CI, min(g*CI+CI, s)).  Thread = column; the tile streams through shared
+// memory in kRC-row chunks (cp.async, double-buffered, coalesced both ways);
+// the V state stays in registers, the coefficient panel in shared memory.
+constexpr int kRC = 16;
+constexpr int kLdC = kRC + 1;
+
+template <int KB>
+__global__ void __launch_bounds__(kApplyT) bapply_kernel(double *__restrict__ L, int64_t n, int64_t ldl, int k,
+                                                         const double *__restrict__ chk, int CI,
+                                                         const double *__restrict__ U,
+                                                         const double *__restrict__ panels) {
+    const int s = blockIdx.x + 1;
+    const int g = blockIdx.y;
+    const int b0 = g * CI;
+    if (b0 >= s) return;
+    const int b1 = min(b0 + CI, s);
+    extern __shared__ double2 smem_bapply[];
+    double2 *cs = smem_bapply;                              // [kD * k]
+    double *rho = reinterpret_cast<double *>(cs + kD * k);  // [kD]
+    double *nu = rho + kD;                                  // [KB]
+    double *Us = nu + KB;                                   // [KB * KB]
+    double *buf = Us + KB * KB;                             // [2][kD cols][kLdC]
+    const int t = threadIdx.x;
+    const int64_t c0 = (int64_t)s * kD;
+    const int nc = (int)imin64(kD, n - c0);
+    double v[KB];
+    constexpr int NCH = kD / kRC;
+
+    auto issue = [&](int b, int ch) {
+        double *bb = buf + (ch & 1) * kD * kLdC;
+        for (int idx = t; idx < kD * kRC; idx += kApplyT) {
+            const int c = idx / kRC, j = idx % kRC;
+            if (c < nc) cp_async8(bb + c * kLdC + j, L + ((int64_t)b * kD + ch * kRC + j) + (c0 + c) * ldl);
+        }
+        cp_async_commit();
+    };
+    for (int b = b0; b < b1; ++b) {
+        issue(b, 0);
+        const double *panel = panels + (int64_t)b * panel_doubles(k);
+        for (int i = t; i < kD * k; i += kApplyT) cs[i] = make_double2(panel[2 * i], panel[2 * i + 1]);
+        for (int i = t; i < kD; i += kApplyT) rho[i] = panel[2ll * kD * k + i];
+        for (int i = t; i < k; i += kApplyT) nu[i] = panel[2ll * kD * k + kD + i];
+        if (b == b0)
+            for (int i = t; i < k * k; i += kApplyT) Us[i] = U[(int64_t)b * k * k + i];
+        __syncthreads();
+        if (b == b0 && t < nc) {  // V-state = U_b^{-1} r  (forward substitution, k x k lower)
+            const double *r = chk + (chk_count_before(s, CI) + g) * kD * k + (int64_t)t * k;
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {
+                if (e < k) {
+                    double acc = r[e];
+#pragma unroll
+                    for (int ep = 0; ep < e; ++ep) acc = fma(-Us[e * k + ep], v[ep], acc);
+                    v[e] = acc / Us[e * k + e];
+                } else {
+                    v[e] = 0.0;
+                }
+            }
+        }
+        for (int ch = 0; ch < NCH; ++ch) {
+            if (ch + 1 < NCH) {
+                issue(b, ch + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                cp_async_wait_all();
+            }
+            __syncthreads();
+            double *bb = buf + (ch & 1) * kD * kLdC;
+            if (t < nc) {
+                double *col = bb + t * kLdC;
+#pragma unroll 4
+                for (int j = 0; j < kRC; ++j)
+                    col[j] = apply_row<KB>(col[j], v, cs + (ch * kRC + j) * k, rho[ch * kRC + j], k);
+            }
+            __syncthreads();
+            for (int idx = t; idx < kD * kRC; idx += kApplyT) {
+                const int c = idx / kRC, j = idx % kRC;
+                if (c < nc) L[((int64_t)b * kD + ch * kRC + j) + (c0 + c) * ldl] = bb[c * kLdC + j];
+            }
+        }
+        if (t < nc) {
+#pragma unroll
+            for (int e = 0; e < KB; ++e)
+                if (e < k) v[e] *= nu[e];
+        }
+        __syncthreads();
+    }
+}
+
+template <int KB>
+gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, int sigma, unsigned long long *key,
+                          int64_t ebase, char *wsbase, const Layout &lay, unsigned epoch, cudaStream_t stream) {
+    TrsvArgs a;
+    a.L = L;
+    a.n = n;
+    a.ldl = ldl;
+    a.V = V;
+    a.k = k;
+    a.P = reinterpret_cast<double *>(wsbase + lay.P);
+    a.rcur = reinterpret_cast<double *>(wsbase + lay.rcur);
+    a.rchain = reinterpret_cast<double *>(wsbase + lay.rchain);
+    a.MX = reinterpret_cast<double *>(wsbase + lay.MX);
+    a.bulk_ok = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0);
+    a.chk = reinterpret_cast<double *>(wsbase + lay.chk);
+    a.CI = lay.CI;
+    unsigned *flags = reinterpret_cast<unsigned *>(wsbase + lay.flags);
+    a.prog = reinterpret_cast<unsigned long long *>(flags);
+    a.rflag = flags + 2 * 16;
+    a.lflag = a.rflag + lay.NT;
+    a.epoch = epoch;
+
+    a.NC = (k + kRPC - 1) / kRPC;
+    int dev = 0, nsm = 0;
+    gcm_status_t st = check_cuda(cudaGetDevice(&dev));
+    if (st == GCM_OK) st = check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (st != GCM_OK) return st;
+    const size_t smem_chain = (size_t)ChainSmem::total * sizeof(double);
+    const size_t smem_help =
+        (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + kHelpMaxOwn * kDT * KB) * sizeof(double);
+    const size_t smem = std::max(smem_chain, smem_help);
+    st = check_cuda(cudaFuncSetAttribute(trsv_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (st != GCM_OK) return st;
+    int per_sm = 0;
+    st = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trsv_kernel<KB>, kTrsvThreads, smem));
+    if (st != GCM_OK) return st;
+    if (per_sm < 1) return GCM_ECUDA;
+    const int grid = (int)std::min<int64_t>((int64_t)nsm * per_sm, a.NC + lay.NT);
+    if (grid <= a.NC) return GCM_ECUDA;
+    void *args[] = {&a};
+    st = check_cuda(cudaLaunchCooperativeKernel((const void *)trsv_kernel<KB>, dim3(grid), dim3(kTrsvThreads), args,
+                                                smem, stream));
+    if (st != GCM_OK) return st;
+
+    double *Q = reinterpret_cast<double *>(wsbase + lay.Q);
+    double *U = reinterpret_cast<double *>(wsbase + lay.U);
+    double *panels = reinterpret_cast<double *>(wsbase + lay.panels);
+    gram_kernel<<<lay.NB, 256, 0, stream>>>(a.P, n, k, Q);
+    double *G = reinterpret_cast<double *>(wsbase + lay.G);
+    gscan_kernel<<<1, 1024, 0, stream>>>(Q, G, lay.NB, k);
+    const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1)) * sizeof(double);
+    st = check_cuda(cudaFuncSetAttribute(bdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_diag));
+    if (st != GCM_OK) return st;
+    bdiag_kernel<KB><<<lay.NB, kD, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, G, U, panels, key, ebase);
+    if (lay.NB > 1) {
+        const size_t smem_apply = (size_t)(2 * kD * k + kD + KB + KB * KB + 2 * kD * kLdC) * sizeof(double);
+        st = check_cuda(
+            cudaFuncSetAttribute(bapply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_apply));
+        if (st != GCM_OK) return st;
+        const dim3 grid2(lay.NB - 1, (lay.NB - 1 + lay.CI - 1) / lay.CI);
+        bapply_kernel<KB><<<grid2, kApplyT, smem_apply, stream>>>(L, n, ldl, k, a.chk, lay.CI, U, panels);
+    }
+    return check_cuda(cudaGetLastError());
+}
+
+}  // namespace
+
+#ifdef GCM_TRACE
+extern "C" int gcm_debug_trace(long long *host, int count) {
+    return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * count);
+}
+#endif
+
+size_t blocked_workspace_bytes(int64_t n, int64_t k) {
+    const int kc = (int)std::min<int64_t>(k, kBKMax);
+    return make_layout(n, kc, kChkBudget).total;
+}
+
+gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
+                            unsigned long long *key, cudaStream_t stream) {
+    Workspace *ws = nullptr;
+    const int kc0 = (int)std::min<int64_t>(k, kBKMax);
+    const Layout lay0 = make_layout(n, kc0, kChkBudget);
+    gcm_status_t st = get_workspace(stream, lay0.total, 1, &ws);
+    if (st != GCM_OK) return st;
+    char *base = reinterpret_cast<char *>(ws->panels);
+    for (int64_t e0 = 0; e0 < k; e0 += kBKMax) {
+        const int kc = (int)std::min<int64_t>(kBKMax, k - e0);
+        const Layout lay = make_layout(n, kc, kChkBudget);
+        const unsigned epoch = ++ws->epoch;
+        double *Vc = V + e0 * n;
+        if (kc <= 4) st = blocked_pass<4>(L, n, ldl, Vc, kc, sigma, key, e0, base, lay, epoch, stream);
+        else if (kc <= 8) st = blocked_pass<8>(L, n, ldl, Vc, kc, sigma, key, e0, base, lay, epoch, stream);
+        else if (kc <= 16) st = blocked_pass<16>(L, n, ldl, Vc, kc, sigma, key, e0, base, lay, epoch, stream);
+        else st = blocked_pass<32>(L, n, ldl, Vc, kc, sigma, key, e0, base, lay, epoch, stream);
+        if (st != GCM_OK) return st;
+    }
+    return GCM_OK;
+}
+
 }  // namespace gcm

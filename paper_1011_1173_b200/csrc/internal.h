@@ -34,6 +34,7 @@ struct Workspace {
     unsigned long long *key = nullptr; // failure key (batched: one per factor)
     void *extra = nullptr;             // algorithm-specific scratch
     size_t bytes = 0;
+    unsigned epoch = 0;                // device-flag epoch of the last call (flags start zeroed)
 };
 
 // Returns a workspace of at least `bytes` bytes (+ key) for (current device, stream).

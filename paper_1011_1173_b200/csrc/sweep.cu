@@ -32,7 +32,6 @@ __global__ void __launch_bounds__(kD) diag_chain_kernel(double *__restrict__ L, 
     __shared__ double rho_s;
 
     const int t = threadIdx.x;
-    const int lane = t & 31;
     const int Db = (int)(n - r0 < kD ? n - r0 : kD);
 
     // load the block's upper triangle (coalesced: consecutive threads -> consecutive rows)
@@ -43,34 +42,9 @@ __global__ void __launch_bounds__(kD) diag_chain_kernel(double *__restrict__ L, 
     double v[KMAX];
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) v[e] = (t < Db && e < k) ? V[(r0 + t) + (int64_t)e * n] : 0.0;
-    for (int e = t; e < k; e += kD) IM[e] = 1.0;
     __syncthreads();
 
-    double *gpanel = panel;
-    double *rho_g = panel + 2ll * kD * k;
-    for (int j = 0; j < Db; ++j) {
-        if (t == j) {
-#pragma unroll
-            for (int e = 0; e < KMAX; ++e)
-                if (e < k) vrow[e] = v[e];
-        }
-        __syncthreads();
-        if (t < 32) {
-            const double w = compute_row_warp(lane, Ls[j][j], vrow, IM, cs, gpanel + 2ll * j * k,
-                                              V + (r0 + j), n, k, sigma, r0 + j, ebase, key);
-            if (lane == 0) {
-                const double rho = Ls[j][j] / w;
-                rho_s = rho;
-                rho_g[j] = rho;
-                Ls[j][j] = w;
-            }
-        }
-        __syncthreads();
-        if (t > j && t < Db) Ls[t][j] = apply_row<KMAX>(Ls[t][j], v, cs, rho_s, k);
-    }
-    __syncthreads();
-    double *nu_g = panel + 2ll * kD * k + kD;
-    for (int e = t; e < k; e += kD) nu_g[e] = sqrt(IM[e]);
+    block_sweep<KMAX, kD + 1>(Ls, v, Db, k, sigma, r0, panel, V + r0, n, key, ebase, vrow, IM, cs, &rho_s);
     for (int idx = t; idx < kD * kD; idx += kD) {
         const int m = idx / kD, j = idx % kD;
         if (m < Db && j <= m) L[(r0 + j) + (r0 + m) * ldl] = Ls[m][j];

@@ -59,7 +59,10 @@ SIZES = [1, 2, 3, 31, 63, 64, 65, 127, 128, 129, 200]
 RANKS = [1, 2, 3, 8, 15, 16, 17, 33, 64, 65]
 
 
-@pytest.mark.parametrize("algo", ["sweep", "auto"])
+ALGOS = ["sweep", "blocked", "auto"]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("sigma", [1, -1])
 @pytest.mark.parametrize("n", SIZES)
 def test_parity_grid_sizes(gcm, n, sigma, algo):
@@ -67,17 +70,19 @@ def test_parity_grid_sizes(gcm, n, sigma, algo):
         check(*run_both(gcm, n, k, sigma, seed=n * 7 + k, algo=algo), n)
 
 
+@pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("sigma", [1, -1])
 @pytest.mark.parametrize("k", RANKS)
-def test_parity_grid_ranks(gcm, k, sigma):
-    check(*run_both(gcm, 150, k, sigma, seed=100 + k), 150)
+def test_parity_grid_ranks(gcm, k, sigma, algo):
+    check(*run_both(gcm, 150, k, sigma, seed=100 + k, algo=algo), 150)
 
 
+@pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("ldl_pad", [3, 64])
-def test_parity_leading_dimension(gcm, ldl_pad):
+def test_parity_leading_dimension(gcm, ldl_pad, algo):
     for sigma in (1, -1):
         n = 190
-        check(*run_both(gcm, n, 7, sigma, ldl=n + ldl_pad, seed=ldl_pad), n)
+        check(*run_both(gcm, n, 7, sigma, ldl=n + ldl_pad, seed=ldl_pad, algo=algo), n)
 
 
 def test_parity_direct_instance(gcm):
@@ -99,9 +104,11 @@ def test_parity_direct_instance(gcm):
         L = torch.from_numpy(Lo.copy()).to(dev)
 
 
-def test_parity_moderate(gcm):
+@pytest.mark.parametrize("algo", ALGOS)
+def test_parity_moderate(gcm, algo):
     for sigma in (1, -1):
-        check(*run_both(gcm, 1000, 16, sigma, seed=12), 1000)
+        check(*run_both(gcm, 1000, 16, sigma, seed=12, algo=algo), 1000)
+        check(*run_both(gcm, 2113, 32, sigma, seed=13, algo=algo), 2113)
 
 
 def test_zero_update_identity(gcm):
@@ -125,7 +132,8 @@ def test_empty_is_noop(gcm):
     gcm.modify(L0, torch.ones(3, 0, dtype=torch.float64, device="cuda"), -1)
 
 
-def test_indefinite_downdate_reported(gcm):
+@pytest.mark.parametrize("algo", ALGOS)
+def test_indefinite_downdate_reported(gcm, algo):
     n, m = 150, 97
     Lbuf, _, _ = synth.paper_instance(n, 1, 1, seed=4)
     v = 1.01 * upper(Lbuf)[m, :]
@@ -133,18 +141,19 @@ def test_indefinite_downdate_reported(gcm):
     L = torch.from_numpy(Lbuf).cuda()
     Vt = torch.from_numpy(V).cuda()
     info = gcm.new_info("cuda")
-    gcm.modify(L, Vt, -1, info=info)
+    gcm.modify(L, Vt, -1, info=info, algo=algo)
     Lo, Vo = Lbuf.copy(), V.copy()
     _, _, oi = oracle.modify_a(Lo, Vo, -1)
     assert (oi.code, oi.col, oi.row) == (1, 1, m)
     assert gcm.read_info(info)[0] == (1, 1, m)
 
 
-def test_non_positive_pivot_reported(gcm):
+@pytest.mark.parametrize("algo", ALGOS)
+def test_non_positive_pivot_reported(gcm, algo):
     Lbuf, Vbuf, _ = synth.paper_instance(80, 2, 1, seed=8)
     Lbuf[70, 70] = 0.0
     info = gcm.new_info("cuda")
-    gcm.modify(torch.from_numpy(Lbuf).cuda(), torch.from_numpy(Vbuf).cuda(), 1, info=info)
+    gcm.modify(torch.from_numpy(Lbuf).cuda(), torch.from_numpy(Vbuf).cuda(), 1, info=info, algo=algo)
     assert gcm.read_info(info)[0] == (2, 0, 70)
 
 
@@ -153,12 +162,12 @@ def test_repeated_calls_and_streams(gcm):
     n, k = 300, 8
     Lbuf, Vbuf, _ = synth.paper_instance(n, k, 1, seed=10)
     outs = []
-    for s in (None, torch.cuda.Stream(), torch.cuda.Stream()):
-        L = torch.from_numpy(Lbuf).cuda()
-        V = torch.from_numpy(Vbuf).cuda()
-        torch.cuda.synchronize()
-        for _ in range(3):
-            gcm.modify(L, V.clone(), 1, stream=s)
+    for s in (torch.cuda.current_stream(), torch.cuda.Stream(), torch.cuda.Stream()):
+        with torch.cuda.stream(s):  # clones and calls ordered on the same stream
+            L = torch.from_numpy(Lbuf).cuda()
+            V = torch.from_numpy(Vbuf).cuda()
+            for _ in range(3):
+                gcm.modify(L, V.clone(), 1)
         torch.cuda.synchronize()
         outs.append(L.cpu().numpy())
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])

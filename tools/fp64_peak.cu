@@ -1,0 +1,88 @@
+// FP64 microbenchmarks for the roofline denominators (MEASURED_PEAKS.json has no fp64 entry):
+//  (1) DFMA throughput: all SMs, 8 independent chains per thread
+//  (2) DFMA dependent latency: one warp, one chain
+//  (3) chain link cost of the paper's Compute (sqrt + div) and of rcp, one warp
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void dfma_tput(double *out, int iters, double a, double b) {
+    double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+__global__ void dfma_lat(double *out, long long *cyc, int iters, double a, double b) {
+    double x = threadIdx.x;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x = fma(x, a, b);
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = x;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+__global__ void link_lat(double *out, long long *cyc, int iters, int mode) {
+    double d = 3.0 + threadIdx.x * 1e-3, v = 0.5;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        if (mode == 0) {  // paper Compute: w = sqrt(d^2 + v^2); c = w/d; next d = w*c*1e-1... keep dependent
+            double w = sqrt(d * d + v * v);
+            double c = w / d;
+            d = c * 2.5;
+        } else if (mode == 1) {  // reciprocal only
+            d = 1.0 / (d + 1.0);
+        } else {  // rsqrt via sqrt/div in one
+            d = rsqrt(d * d + v);
+        }
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = d;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+int main() {
+    int dev = 0, nsm = 0, clk = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+    double *out;
+    long long *cyc;
+    cudaMalloc(&out, sizeof(double) * 148 * 64 * 1024);
+    cudaMalloc(&cyc, sizeof(long long) * 4);
+    const int threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int bps = 1; bps <= 8; bps *= 2) {
+        const int grid = nsm * bps;
+        dfma_tput<<<grid, threads>>>(out, 16, 1.0000001, 1e-9);
+        cudaEventRecord(e0);
+        dfma_tput<<<grid, threads>>>(out, iters, 1.0000001, 1e-9);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double fmas = (double)grid * threads * iters * 16 * 8;
+        printf("dfma_tput grid=%d (%d CTA/SM x %d thr): %.3f ms  %.2f TFLOP/s (2 flop/FMA)  %.1f FMA/clk/SM at nominal %d MHz\n",
+               grid, bps, threads, ms, 2 * fmas / ms / 1e9, fmas / (ms * 1e-3) / nsm / (clk * 1e3), clk / 1000);
+    }
+    long long h;
+    dfma_lat<<<1, 32>>>(out, cyc, iters, 1.0000001, 1e-9);
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("dfma dependent latency: %.2f cycles\n", (double)h / (iters * 16));
+    const char *names[] = {"compute link (sqrt+div+mul)", "rcp link (add+div)", "rsqrt link (fma+rsqrt)"};
+    for (int m = 0; m < 3; ++m) {
+        link_lat<<<1, 32>>>(out, cyc, 1024, m);
+        cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("%s: %.1f cycles\n", names[m], (double)h / 1024);
+    }
+    return 0;
+}

@@ -1,0 +1,32 @@
+"""Per-step phase timing of the blocked TRSV chain CTA (needs a -DGCM_TRACE build via GCM_LIB_PATH)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1011_1173_b200 as gcm  # noqa: E402
+from paper_1011_1173_b200 import _native  # noqa: E402
+import synth  # noqa: E402
+
+n, k = int(sys.argv[1]), int(sys.argv[2])
+Lbuf, Vbuf, _ = synth.paper_instance(n, k, 1)
+L = torch.from_numpy(Lbuf).cuda()
+V = torch.from_numpy(Vbuf).cuda()
+for _ in range(3):
+    gcm.modify(L, V.clone(), 1, algo="blocked")
+torch.cuda.synchronize()
+lib = _native.lib()
+buf = (ctypes.c_longlong * (4096 * 8))()
+lib.gcm_debug_trace(buf, 4096 * 8)
+tr = np.frombuffer(buf, dtype=np.int64).reshape(4096, 8)
+NT = (n + 31) // 32
+t = tr[:NT].astype(np.float64)
+step = np.diff(t[:, 0])
+print(f"steps {NT}: chain step cycles median {np.median(step):.0f} mean {step.mean():.0f}")
+names = ["crit.start", "crit.p_done", "prep.start", "prep.mbar_ok", "prep.partials", "prep.rflag_ok", "prep.done", "svc.issued"]
+for s in range(1, 8):
+    d = t[1:-2, s] - t[1:-2, 0]
+    print(f"  {names[s]:22s} - crit.start: median {np.median(d):8.0f}  p10 {np.percentile(d,10):8.0f} p90 {np.percentile(d,90):8.0f}")
