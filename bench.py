@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the rank-k Cholesky up/down-date (arXiv 1011.1173) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
+
+Prints ONE JSON line (rank 0).  A "step" is one pass of the whole hot path:
+one in-place rank-k modification of the factor (SURVEY.md section 8(a) rows a0-a4,
+through gcm_modify_ex), alternating update (sigma=+1) and downdate (sigma=-1) by
+the same V so the factor stays bounded; V is restored from a pristine copy and
+L2 is flushed (256 MiB write) between steps, outside the timed events.
+
+Configs (BASELINE.json): "n5000_k16" (default, configs[1]: the metric's config),
+"n5000_k1" / "n5000_k4" / "n5000_k64" (configs[2] sweep), "batched" (configs[4]:
+4096 factors n=512, k=8; weak-sharded over ranks).
+
+--impl reference times the CPU oracle (oracle/, plain serial C) on the same
+workload as the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "rank-k modify ms & fp64 GFLOP/s (n=5000,k=16); % of HBM/FP64 roofline"
+# FP64 vector peak derived from the unit counts and clock (B200_PROFILING.md: 148 SMs,
+# 1965 MHz max; 64 FP64 FMA/clk/SM): 148*64*2*1.965e9.  tools/fp64_peak.cu measured
+# 34.2 TFLOP/s on this pool.
+FP64_PEAK_TFLOPS_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
+FP64_PEAK_TFLOPS_MEASURED = 34.2
+
+CONFIGS = {
+    "n5000_k16": dict(n=5000, k=16),
+    "n5000_k1": dict(n=5000, k=1),
+    "n5000_k4": dict(n=5000, k=4),
+    "n5000_k64": dict(n=5000, k=64),
+    "batched": dict(n=512, k=8, batch=4096),
+}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic(n, k, batch=1):
+    """Algorithmic units of one step: Apply count, flops, HBM bytes."""
+    applies = batch * k * n * (n - 1) // 2
+    flops = 6 * applies
+    bytes_ = batch * (8 * n * (n + 1) + 16 * n * k)  # upper triangle read+write, V read+write
+    return applies, flops, bytes_
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.05)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(ngpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_1011_1173_b200 as gcm
+    import synth
+
+    cfg = CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n, k = cfg["n"], cfg["k"]
+    batch = cfg.get("batch", 1)
+    stream = torch.cuda.current_stream(dev)
+
+    if batch == 1:
+        Lbuf, Vbuf, _ = synth.paper_instance(n, k, +1, seed=synth.SEED_ROOT + rank)
+        L = torch.from_numpy(Lbuf).to(dev)
+        V0 = torch.from_numpy(Vbuf).to(dev)
+    else:
+        per = batch // world  # weak sharding: each rank owns its slice of the factors
+        distinct = min(per, 32)  # distinct seeded factors, tiled to fill the slice
+        Ls, Vs, _ = synth.batched_instances(distinct, n, k, +1, first=rank * per)
+        reps = (per + distinct - 1) // distinct
+        L = torch.from_numpy(np.tile(Ls, (reps, 1, 1))[:per].copy()).to(dev)
+        V0 = torch.from_numpy(np.tile(Vs, (reps, 1, 1))[:per].copy()).to(dev)
+        batch = per
+    V = V0.clone()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def call(sigma):
+        if batch == 1:
+            gcm.modify(L, V, sigma, algo=args.algo)
+        else:
+            gcm.modify_batched(L, V, sigma)
+
+    # warm-up
+    for i in range(args.warmup):
+        V.copy_(V0)
+        call(+1 if i % 2 == 0 else -1)
+    torch.cuda.synchronize()
+    gcm.profile_read()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    gcm.profile_enable(True)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        V.copy_(V0)
+        flush.fill_(float(i))  # L2 flush: 256 MiB write, outside the step's events
+        ev[i][0].record(stream)
+        call(+1 if i % 2 == 0 else -1)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    wall = time.perf_counter() - t0
+    gcm.profile_enable(False)
+    prof = gcm.profile_read()
+    clk = clocks.stop()
+
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = max_over_ranks(sum(step_ms), world)
+    ms_per_step = total_ms / args.steps
+    applies, flops, bytes_ = algorithmic(n, k, batch)
+    value = world * flops / (ms_per_step * 1e-3) / 1e9  # GFLOP/s, whole job
+
+    # dominant kernel and its roofline (bytes/flops per launch from DESIGN.md "roofline")
+    hbm, hbm_src = measured_peaks()
+    launches = sum(c for c, _ in prof.values())
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 0.0))
+    dname, (dcount, dms) = dom
+    per_launch_ms = dms / max(dcount, 1)
+    kb = kernel_units(dname, n, k, batch)
+    if kb["bound"] == "hbm":
+        achieved = kb["bytes"] / (per_launch_ms * 1e-3) / 1e9
+        peak, unit = hbm, "GB/s"
+    else:
+        achieved = kb["flops"] / (per_launch_ms * 1e-3) / 1e12
+        peak, unit = FP64_PEAK_TFLOPS_DERIVED, "TFLOP/s"
+    roofline = {"kernel": dname, "bound": kb["bound"], "achieved": round(achieved, 3), "peak": peak,
+                "peak_source": hbm_src if kb["bound"] == "hbm" else "derived (148 SM x 64 FMA/clk x 2 x 1.965 GHz)",
+                "unit": unit, "frac": round(achieved / peak, 4), "traffic": kb.get("traffic"),
+                "algorithmic": kb["what"], "share_of_step": round(dms / max(sum(m for _, m in prof.values()), 1e-9), 3)}
+    # whole-path roofline: T_roof = max(flops/F64, bytes/HBM)
+    t_roof = max(flops / (FP64_PEAK_TFLOPS_DERIVED * 1e12), bytes_ / (hbm * 1e9))
+    roofline_path = {"t_roof_ms": round(t_roof * 1e3, 4), "t_step_ms": round(ms_per_step, 4),
+                     "frac": round(t_roof * 1e3 / ms_per_step, 4),
+                     "bound": "fp64" if flops / FP64_PEAK_TFLOPS_DERIVED / 1e12 > bytes_ / hbm / 1e9 else "hbm",
+                     "achieved_gbs": round(bytes_ / (ms_per_step * 1e-3) / 1e9, 1),
+                     "achieved_gflops": round(flops / (ms_per_step * 1e-3) / 1e9, 1)}
+
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.config, n, k, batch * world),
+                   "n": n, "k": k, "batch_per_gpu": batch, "algo": args.algo if batch == 1 else "batched",
+                   "sigma": "alternating +1/-1 by the same V", "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"replicas x{world}" if batch == 1 else f"factor-sharded x{world}",
+                   "instance": "paper construction (PAPER.md 111): B,V ~ U[0,1), A = B^T B + I, seed 10111173+rank"},
+        "roofline": roofline, "roofline_path": roofline_path, "gpu_launches": int(launches),
+        "kernels": {kname: {"launches": c, "ms_total": round(m, 4)} for kname, (c, m) in prof.items()},
+        "clocks": clk, "wall_s": round(wall, 4),
+    }
+    if rank == 0 and batch == 1 and not args.no_e2e:
+        out["e2e"] = run_e2e(gcm, torch, Lbuf, Vbuf, n, k, flops)
+    if rank == 0 and not args.no_cpu:
+        out["cpu_baseline"] = run_cpu_baseline(n, k)
+    return out
+
+
+def kernel_units(name, n, k, batch):
+    """Algorithmic work of ONE launch of each kernel family."""
+    tri = 8 * n * (n + 1) // 2  # bytes of the upper triangle
+    if name == "trsv":  # reads the triangle once for P = L^-T V (k FMA per element)
+        return {"bound": "hbm", "bytes": tri + 16 * n * k, "flops": n * n * k,
+                "what": "L triangle read once + V read + P write; n^2 k flops"}
+    if name == "bapply":  # off-diagonal tiles read+write once, 2k FMA per element
+        off = 2 * tri * (1 - 64.0 / n)
+        return {"bound": "hbm" if k < 16 else "alu", "bytes": off, "flops": 6 * k * n * (n - 1) / 2 * (1 - 64.0 / n),
+                "what": "off-diagonal triangle read+write; 6 flops per Apply"}
+    if name in ("bdiag", "diag_chain"):
+        return {"bound": "alu", "bytes": 16 * 64 * n, "flops": 6 * k * 64 * n / 2,
+                "what": "diagonal blocks (64 x 64 per block) Compute+Apply"}
+    if name == "panel_apply":
+        return {"bound": "hbm", "bytes": 2 * tri / max(1, (n + 63) // 64), "flops": 6 * k * n * 64 / 2,
+                "what": "one 64-row panel read+write (average)"}
+    if name == "batched":
+        return {"bound": "hbm", "bytes": batch * (2 * tri + 16 * n * k), "flops": batch * 6 * k * n * (n - 1) / 2,
+                "what": "every factor's triangle read+write once, V read+write"}
+    return {"bound": "hbm", "bytes": 0, "flops": 0, "what": "unmodelled"}
+
+
+def workload_name(cfg, n, k, total_batch):
+    if total_batch > 1:
+        return f"batched {total_batch} x (n={n}, k={k}) fp64 update/downdate"
+    return f"n={n}, k={k} fp64 rank-k update/downdate (BASELINE configs[1])" if (n, k) == (5000, 16) else \
+        f"n={n}, k={k} fp64 rank-k update/downdate"
+
+
+def run_e2e(gcm, torch, Lbuf, Vbuf, n, k, flops, steps=3):
+    """Same metric through the C-ABI with HOST buffers (gcm_modify_host): H2D + modify + D2H per step."""
+    Lh = torch.from_numpy(Lbuf.copy()).pin_memory()
+    Vh0 = torch.from_numpy(Vbuf.copy())
+    Vh = Vh0.clone().pin_memory()
+    ts = []
+    for i in range(steps + 1):
+        Vh.copy_(Vh0)
+        t0 = time.perf_counter()
+        gcm.modify_host(Lh, Vh, +1 if i % 2 == 0 else -1)
+        dt = time.perf_counter() - t0
+        if i > 0:
+            ts.append(dt)
+    t = statistics.median(ts)
+    nb = Lh.numel() * 8 + Vh.numel() * 8
+    return {"value": round(flops / t / 1e9, 2), "unit": "GFLOP/s", "ms_per_step": round(t * 1e3, 3),
+            "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "api": "gcm_modify_host (pinned host L, V)"}
+
+
+def run_cpu_baseline(n, k, budget_s=20.0):
+    """The oracle (plain serial C, oracle/) on this host: bounded sample of the same workload."""
+    import oracle
+    import synth
+    cores = 1  # the oracle is single-threaded by construction
+    Lbuf, Vbuf, _ = synth.paper_instance(n, k, +1, seed=synth.SEED_ROOT)
+    calls, t_tot = 0, 0.0
+    while t_tot < budget_s and calls < 4:
+        L = Lbuf.copy()
+        V = Vbuf.copy()
+        t0 = time.perf_counter()
+        oracle.modify_a(L, V, +1)
+        t_tot += time.perf_counter() - t0
+        calls += 1
+        if t_tot > budget_s / 4:
+            break
+    _, flops, _ = algorithmic(n, k)
+    return {"value": round(flops * calls / t_tot / 1e9, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"{calls} full oracle call(s) of n={n}, k={k} update ({t_tot:.2f} s)",
+            "ms_per_call": round(t_tot / calls * 1e3, 1)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, world, rank):
+    """Reference arm: the CPU oracle, as it stands, on the host cores (rank 0 only)."""
+    import oracle
+    import synth
+    cfg = CONFIGS[args.config]
+    n, k = cfg["n"], cfg["k"]
+    batch = cfg.get("batch", 1)
+    if batch > 1:
+        n_use, k_use, calls_per_step = n, k, 16  # bounded sample: 16 factors per step
+    else:
+        n_use, k_use, calls_per_step = n, k, 1
+    Lbuf, Vbuf, _ = synth.paper_instance(n_use, k_use, +1, seed=synth.SEED_ROOT)
+    L = Lbuf.copy()
+
+    def step(i):
+        for _ in range(calls_per_step):
+            V = Vbuf.copy()
+            oracle.modify_a(L, V, +1 if i % 2 == 0 else -1)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    t = time.perf_counter() - t0
+    _, flops, _ = algorithmic(n_use, k_use, calls_per_step)
+    value = flops * args.steps / t / 1e9
+    sample = (f"{calls_per_step} oracle call(s) of n={n_use}, k={k_use} per step"
+              + (f" (bounded sample of the {batch}-factor batch)" if batch > 1 else ""))
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config, n, k, batch), "n": n, "k": k},
+            "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="n5000_k16")
+    ap.add_argument("--algo", choices=["auto", "sweep", "blocked"], default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, world, rank)), flush=True)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    out = run_ours(args, world, rank, local)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

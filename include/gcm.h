@@ -127,6 +127,17 @@ gcm_status_t gcm_modify_dist(gcm_comm_t comm, double *L_local, int64_t n, int64_
                              int64_t ldl_local, double *V_local, int64_t k, int sigma,
                              gcm_info_t *d_info, gcm_stream_t stream);
 
+/* ---- measurement hooks (used by bench.py; off by default, no cost when off) ----
+ * When enabled, every kernel launch of the library on any stream is bracketed by
+ * a pair of CUDA events recorded on that stream.  gcm_profile_read synchronises
+ * the recorded events and returns, per kernel family (e.g. "trsv", "bapply"),
+ * the number of launches and the summed event time in milliseconds, then clears
+ * the record.  names: caller buffer of max_entries * 32 chars (NUL-terminated
+ * strings, 32 bytes each); counts/ms: arrays of max_entries.  Returns the number
+ * of entries written (or -1 on a CUDA error). */
+gcm_status_t gcm_profile_enable(int on);
+int gcm_profile_read(char *names, int64_t *counts, double *ms, int max_entries);
+
 /* Human-readable status. */
 const char *gcm_status_string(gcm_status_t s);
 

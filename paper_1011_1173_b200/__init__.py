@@ -108,5 +108,27 @@ def modify_batched(L, V, sigma: int, info=None, stream=None) -> None:
     _native.check("gcm_modify_batched", st)
 
 
+def profile_enable(on: bool = True) -> None:
+    """Bracket every library kernel launch with CUDA events (measurement hook)."""
+    _native.check("gcm_profile_enable", _native.lib().gcm_profile_enable(1 if on else 0))
+
+
+def profile_read(max_entries: int = 32):
+    """{kernel family: (launches, total ms)} since the last read (synchronises)."""
+    import numpy as np
+    names = ctypes.create_string_buffer(32 * max_entries)
+    counts = np.zeros(max_entries, dtype=np.int64)
+    ms = np.zeros(max_entries, dtype=np.float64)
+    n = _native.lib().gcm_profile_read(names, counts.ctypes.data_as(ctypes.c_void_p),
+                                       ms.ctypes.data_as(ctypes.c_void_p), max_entries)
+    if n < 0:
+        raise GcmError("gcm_profile_read", 2)
+    out = {}
+    for i in range(n):
+        nm = names.raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode()
+        out[nm] = (int(counts[i]), float(ms[i]))
+    return out
+
+
 def release_workspace() -> None:
     _native.check("gcm_release_workspace", _native.lib().gcm_release_workspace())

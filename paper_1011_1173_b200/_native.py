@@ -29,6 +29,8 @@ SIGNATURES = {
     "gcm_comm_destroy": (_int, [_vp]),
     "gcm_dist_local_cols": (_i64, [_i64, _i64, _int, _int]),
     "gcm_modify_dist": (_int, [_vp, _dp, _i64, _i64, _i64, _dp, _i64, _int, _vp, _vp]),
+    "gcm_profile_enable": (_int, [_int]),
+    "gcm_profile_read": (_int, [ctypes.c_char_p, _vp, _vp, _int]),
     "gcm_status_string": (ctypes.c_char_p, [_int]),
     "gcm_release_workspace": (_int, []),
     "gcm_version": (ctypes.c_char_p, []),

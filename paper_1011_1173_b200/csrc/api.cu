@@ -7,7 +7,9 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <string>
 #include <utility>
+#include <vector>
 
 #include "internal.h"
 
@@ -17,6 +19,50 @@ gcm_status_t check_cuda(cudaError_t e) {
     if (e == cudaSuccess) return GCM_OK;
     if (e == cudaErrorMemoryAllocation) return GCM_ENOMEM;
     return GCM_ECUDA;
+}
+
+bool g_profile_on = false;
+
+namespace {
+
+struct ProfRec {
+    std::string name;
+    cudaEvent_t b, e;
+};
+std::mutex g_prof_mutex;
+std::vector<ProfRec> g_prof_open, g_prof_done;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t prof_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t ev = g_event_pool.back();
+        g_event_pool.pop_back();
+        return ev;
+    }
+    cudaEvent_t ev = nullptr;
+    cudaEventCreate(&ev);
+    return ev;
+}
+
+}  // namespace
+
+void prof_record(const char *name, cudaStream_t stream, bool begin) {
+    std::lock_guard<std::mutex> lock(g_prof_mutex);
+    cudaEvent_t ev = prof_event();
+    cudaEventRecord(ev, stream);
+    if (begin) {
+        g_prof_open.push_back({name, ev, nullptr});
+    } else {
+        for (size_t i = g_prof_open.size(); i-- > 0;) {
+            if (g_prof_open[i].name == name) {
+                g_prof_open[i].e = ev;
+                g_prof_done.push_back(g_prof_open[i]);
+                g_prof_open.erase(g_prof_open.begin() + i);
+                return;
+            }
+        }
+        g_event_pool.push_back(ev);
+    }
 }
 
 namespace {
@@ -54,9 +100,10 @@ gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     const char *env = std::getenv("GCM_ALGO");
     if (env && std::strcmp(env, "sweep") == 0) return GCM_ALGO_SWEEP;
     if (env && std::strcmp(env, "blocked") == 0) return GCM_ALGO_BLOCKED;
-    (void)n;
     (void)k;
-    return GCM_ALGO_SWEEP;
+    // the chain-shortened path wins once there is more
+    // than a handful of row blocks; tiny factors keep the two-kernel sweep.
+    return n >= 256 ? GCM_ALGO_BLOCKED : GCM_ALGO_SWEEP;
 }
 
 }  // namespace
@@ -205,6 +252,39 @@ gcm_status_t gcm_modify_batched(double *L, int64_t n, int64_t ldl, int64_t strid
         return GCM_OK;
     }
     return modify_batched(L, n, ldl, strideL, V, strideV, k, sigma, batch, d_info, (cudaStream_t)stream);
+}
+
+gcm_status_t gcm_profile_enable(int on) {
+    g_profile_on = on != 0;
+    return GCM_OK;
+}
+
+int gcm_profile_read(char *names, int64_t *counts, double *ms, int max_entries) {
+    std::lock_guard<std::mutex> lock(g_prof_mutex);
+    std::vector<std::string> order;
+    std::map<std::string, std::pair<int64_t, double>> agg;
+    int err = 0;
+    for (auto &r : g_prof_done) {
+        float t = 0.f;
+        if (cudaEventSynchronize(r.e) != cudaSuccess || cudaEventElapsedTime(&t, r.b, r.e) != cudaSuccess) err = 1;
+        if (!agg.count(r.name)) order.push_back(r.name);
+        agg[r.name].first += 1;
+        agg[r.name].second += t;
+        g_event_pool.push_back(r.b);
+        g_event_pool.push_back(r.e);
+    }
+    g_prof_done.clear();
+    if (err) return -1;
+    int n = 0;
+    for (auto &nm : order) {
+        if (n >= max_entries) break;
+        std::strncpy(names + 32 * n, nm.c_str(), 31);
+        names[32 * n + 31] = 0;
+        counts[n] = agg[nm].first;
+        ms[n] = agg[nm].second;
+        ++n;
+    }
+    return n;
 }
 
 const char *gcm_status_string(gcm_status_t s) {

@@ -860,26 +860,39 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     const int grid = (int)std::min<int64_t>((int64_t)nsm * per_sm, a.NC + lay.NT);
     if (grid <= a.NC) return GCM_ECUDA;
     void *args[] = {&a};
-    st = check_cuda(cudaLaunchCooperativeKernel((const void *)trsv_kernel<KB>, dim3(grid), dim3(kTrsvThreads), args,
-                                                smem, stream));
+    {
+        ProfScope ps("trsv", stream);
+        st = check_cuda(cudaLaunchCooperativeKernel((const void *)trsv_kernel<KB>, dim3(grid), dim3(kTrsvThreads),
+                                                    args, smem, stream));
+    }
     if (st != GCM_OK) return st;
 
     double *Q = reinterpret_cast<double *>(wsbase + lay.Q);
     double *U = reinterpret_cast<double *>(wsbase + lay.U);
     double *panels = reinterpret_cast<double *>(wsbase + lay.panels);
-    gram_kernel<<<lay.NB, 256, 0, stream>>>(a.P, n, k, Q);
+    {
+        ProfScope ps("gram", stream);
+        gram_kernel<<<lay.NB, 256, 0, stream>>>(a.P, n, k, Q);
+    }
     double *G = reinterpret_cast<double *>(wsbase + lay.G);
-    gscan_kernel<<<1, 1024, 0, stream>>>(Q, G, lay.NB, k);
+    {
+        ProfScope ps("gscan", stream);
+        gscan_kernel<<<1, 1024, 0, stream>>>(Q, G, lay.NB, k);
+    }
     const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1)) * sizeof(double);
     st = check_cuda(cudaFuncSetAttribute(bdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_diag));
     if (st != GCM_OK) return st;
-    bdiag_kernel<KB><<<lay.NB, kD, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, G, U, panels, key, ebase);
+    {
+        ProfScope ps("bdiag", stream);
+        bdiag_kernel<KB><<<lay.NB, kD, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, G, U, panels, key, ebase);
+    }
     if (lay.NB > 1) {
         const size_t smem_apply = (size_t)(2 * kD * k + kD + KB + KB * KB + 2 * kD * kLdC) * sizeof(double);
         st = check_cuda(
             cudaFuncSetAttribute(bapply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_apply));
         if (st != GCM_OK) return st;
         const dim3 grid2(lay.NB - 1, (lay.NB - 1 + lay.CI - 1) / lay.CI);
+        ProfScope ps("bapply", stream);
         bapply_kernel<KB><<<grid2, kApplyT, smem_apply, stream>>>(L, n, ldl, k, a.chk, lay.CI, U, panels);
     }
     return check_cuda(cudaGetLastError());

@@ -42,6 +42,21 @@ gcm_status_t get_workspace(cudaStream_t stream, size_t bytes, size_t nkeys, Work
 
 gcm_status_t check_cuda(cudaError_t e);
 
+// Profiling hook (gcm_profile_enable): bracket a launch with events on `stream`.
+// Usage: { ProfScope ps("trsv", stream); kernel<<<..., stream>>>(...); }
+extern bool g_profile_on;
+void prof_record(const char *name, cudaStream_t stream, bool begin);
+struct ProfScope {
+    const char *name;
+    cudaStream_t stream;
+    ProfScope(const char *n, cudaStream_t s) : name(n), stream(s) {
+        if (g_profile_on) prof_record(name, stream, true);
+    }
+    ~ProfScope() {
+        if (g_profile_on) prof_record(name, stream, false);
+    }
+};
+
 // algorithms (enqueue only; arguments already validated, n > 0, k > 0)
 gcm_status_t modify_sweep(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
                           unsigned long long *key, double *panels, cudaStream_t stream);

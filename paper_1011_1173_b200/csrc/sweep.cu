@@ -93,10 +93,14 @@ gcm_status_t sweep_pass(double *L, int64_t n, int64_t ldl, double *V, int k, int
     for (int64_t b = 0; b < nb; ++b) {
         const int64_t r0 = b * kD;
         double *panel = panels + b * pstride;
-        diag_chain_kernel<KMAX><<<1, kD, 0, stream>>>(L, n, ldl, V, k, sigma, r0, panel, key, ebase);
+        {
+            ProfScope ps("diag_chain", stream);
+            diag_chain_kernel<KMAX><<<1, kD, 0, stream>>>(L, n, ldl, V, k, sigma, r0, panel, key, ebase);
+        }
         const int64_t c0 = r0 + kD;
         if (c0 < n) {
             const unsigned grid = (unsigned)((n - c0 + kApplyThreads - 1) / kApplyThreads);
+            ProfScope ps("panel_apply", stream);
             panel_apply_kernel<KMAX><<<grid, kApplyThreads, smem, stream>>>(L, n, ldl, V, k, r0, c0, panel);
         }
     }
