@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -17,6 +18,7 @@ namespace gcm {
 
 gcm_status_t check_cuda(cudaError_t e) {
     if (e == cudaSuccess) return GCM_OK;
+    if (std::getenv("GCM_DEBUG")) std::fprintf(stderr, "gcm: CUDA error %d: %s\n", (int)e, cudaGetErrorString(e));
     if (e == cudaErrorMemoryAllocation) return GCM_ENOMEM;
     return GCM_ECUDA;
 }
@@ -95,6 +97,8 @@ gcm_status_t validate(const double *L, int64_t n, int64_t ldl, const double *V, 
     return GCM_OK;
 }
 
+}  // namespace
+
 gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     if (algo != GCM_ALGO_AUTO) return algo;
     const char *env = std::getenv("GCM_ALGO");
@@ -105,8 +109,6 @@ gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     // than a handful of row blocks; tiny factors keep the two-kernel sweep.
     return n >= 256 ? GCM_ALGO_BLOCKED : GCM_ALGO_SWEEP;
 }
-
-}  // namespace
 
 gcm_status_t get_workspace(cudaStream_t stream, size_t bytes, size_t nkeys, Workspace **out) {
     int dev = 0;
@@ -149,6 +151,21 @@ gcm_status_t finalize_info(const unsigned long long *key, gcm_info_t *d_info, in
     return check_cuda(cudaGetLastError());
 }
 
+size_t single_workspace_bytes(int64_t n, int64_t k, gcm_algo_t algo) {
+    const int64_t nblk = (n + kD - 1) / kD;
+    size_t bytes = (size_t)nblk * panel_doubles((int)std::min<int64_t>(k, kKMax)) * sizeof(double);
+    if (algo == GCM_ALGO_BLOCKED) bytes = std::max(bytes, blocked_workspace_bytes(n, k));
+    return bytes;
+}
+
+gcm_status_t run_single(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma, gcm_algo_t algo,
+                        unsigned long long *key, Workspace *ws, cudaStream_t stream) {
+    gcm_status_t st = check_cuda(cudaMemsetAsync(key, 0xff, sizeof(unsigned long long), stream));
+    if (st != GCM_OK) return st;
+    if (algo == GCM_ALGO_BLOCKED) return modify_blocked(L, n, ldl, V, k, sigma, key, ws, stream);
+    return modify_sweep(L, n, ldl, V, k, sigma, key, ws->panels, stream);
+}
+
 static gcm_status_t modify_impl(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
                                 gcm_info_t *d_info, gcm_algo_t algo, cudaStream_t stream) {
     gcm_status_t st = validate(L, n, ldl, V, k, sigma);
@@ -158,18 +175,10 @@ static gcm_status_t modify_impl(double *L, int64_t n, int64_t ldl, double *V, in
         return GCM_OK;
     }
     algo = pick_algo(n, k, algo);
-    const int64_t nblk = (n + kD - 1) / kD;
-    size_t bytes = (size_t)nblk * panel_doubles((int)std::min<int64_t>(k, kKMax)) * sizeof(double);
-    if (algo == GCM_ALGO_BLOCKED) bytes = std::max(bytes, blocked_workspace_bytes(n, k));
     Workspace *ws = nullptr;
-    st = get_workspace(stream, bytes, 1, &ws);
+    st = get_workspace(stream, single_workspace_bytes(n, k, algo), 1, &ws);
     if (st != GCM_OK) return st;
-    st = check_cuda(cudaMemsetAsync(ws->key, 0xff, sizeof(unsigned long long), stream));
-    if (st != GCM_OK) return st;
-    if (algo == GCM_ALGO_BLOCKED)
-        st = modify_blocked(L, n, ldl, V, k, sigma, ws->key, stream);
-    else
-        st = modify_sweep(L, n, ldl, V, k, sigma, ws->key, ws->panels, stream);
+    st = run_single(L, n, ldl, V, k, sigma, algo, ws->key, ws, stream);
     if (st != GCM_OK) return st;
     return finalize_info(ws->key, d_info, 1, stream);
 }

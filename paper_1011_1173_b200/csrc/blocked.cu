@@ -912,12 +912,8 @@ size_t blocked_workspace_bytes(int64_t n, int64_t k) {
 }
 
 gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
-                            unsigned long long *key, cudaStream_t stream) {
-    Workspace *ws = nullptr;
-    const int kc0 = (int)std::min<int64_t>(k, kBKMax);
-    const Layout lay0 = make_layout(n, kc0, kChkBudget);
-    gcm_status_t st = get_workspace(stream, lay0.total, 1, &ws);
-    if (st != GCM_OK) return st;
+                            unsigned long long *key, Workspace *ws, cudaStream_t stream) {
+    gcm_status_t st = GCM_OK;
     char *base = reinterpret_cast<char *>(ws->panels);
     for (int64_t e0 = 0; e0 < k; e0 += kBKMax) {
         const int kc = (int)std::min<int64_t>(kBKMax, k - e0);

@@ -61,7 +61,13 @@ struct ProfScope {
 gcm_status_t modify_sweep(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
                           unsigned long long *key, double *panels, cudaStream_t stream);
 gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
-                            unsigned long long *key, cudaStream_t stream);
+                            unsigned long long *key, Workspace *ws, cudaStream_t stream);
+// Bytes of scratch one single-factor call needs (either algorithm), and the
+// dispatcher that runs it on an already-sized workspace (no allocation).
+size_t single_workspace_bytes(int64_t n, int64_t k, gcm_algo_t algo);
+gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo);
+gcm_status_t run_single(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma, gcm_algo_t algo,
+                        unsigned long long *key, Workspace *ws, cudaStream_t stream);
 size_t blocked_workspace_bytes(int64_t n, int64_t k);
 gcm_status_t modify_batched(double *L, int64_t n, int64_t ldl, int64_t strideL, double *V,
                             int64_t strideV, int64_t k, int sigma, int64_t batch,

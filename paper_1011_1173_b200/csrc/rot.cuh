@@ -107,28 +107,32 @@ __device__ __forceinline__ double apply_row(double l, double (&v)[KMAX], const d
 }
 
 // The in-block sweep of one D-row diagonal block (PAPER.md lines 24-30
-// restricted to rows/columns r0 .. r0+Db-1), run by a CTA of >= Db threads
-// (>= 32): thread m owns column r0+m with its V state v[] (TRUE values on
-// entry, i.e. mu = 1), Ls[m][j] = L(r0+j, r0+m) in shared memory.  Emits the
-// block's coefficient panel (gamma/delta, rho, nu; layout in internal.h),
-// V_exit rows r0.. (vexit + e*ldv), and leaves L~ in Ls.
+// restricted to rows/columns r0 .. r0+Db-1), run by a CTA whose threads
+// tbase .. tbase+Db-1 own the block's columns: thread tbase+m owns column r0+m
+// with its V state v[] (TRUE values on entry, i.e. mu = 1); Ls[m][j] =
+// L(r0+j, r0+m) in shared memory.  The warp starting at thread tbase (tbase a
+// multiple of 32, Db <= blockDim - tbase) computes the rows' coefficients.
+// Emits the block's coefficient panel (gamma/delta, rho, nu; layout in
+// internal.h, panel may be shared or global memory), V_exit rows r0..
+// (vexit + e*ldv), and leaves L~ in Ls.  Must be called by ALL threads of the CTA.
 template <int KMAX, int LD>
 __device__ __forceinline__ void block_sweep(double (*Ls)[LD], double (&v)[KMAX], int Db, int k, int sigma,
                                             int64_t r0, double *panel, double *vexit, int64_t ldv,
                                             unsigned long long *key, int64_t ebase, double *vrow, double *IM,
-                                            double2 *cs, double *rho_s) {
+                                            double2 *cs, double *rho_s, int tbase = 0) {
     const int t = threadIdx.x;
+    const int m = t - tbase;  // own column within the block (valid if 0 <= m < Db)
     const int lane = t & 31;
     for (int e = t; e < k; e += blockDim.x) IM[e] = 1.0;
     double *rho_g = panel + 2ll * kD * k;
     for (int j = 0; j < Db; ++j) {
-        if (t == j) {
+        if (m == j) {
 #pragma unroll
             for (int e = 0; e < KMAX; ++e)
                 if (e < k) vrow[e] = v[e];
         }
         __syncthreads();
-        if (t < 32) {
+        if (m >= 0 && m < 32) {
             const double d0 = Ls[j][j];
             const double w = compute_row_warp(lane, d0, vrow, IM, cs, panel + 2ll * j * k, vexit + j, ldv, k,
                                               sigma, r0 + j, ebase, key);
@@ -140,7 +144,7 @@ __device__ __forceinline__ void block_sweep(double (*Ls)[LD], double (&v)[KMAX],
             }
         }
         __syncthreads();
-        if (t > j && t < Db) Ls[t][j] = apply_row<KMAX>(Ls[t][j], v, cs, *rho_s, k);
+        if (m > j && m < Db) Ls[m][j] = apply_row<KMAX>(Ls[m][j], v, cs, *rho_s, k);
     }
     __syncthreads();
     double *nu_g = panel + 2ll * kD * k + kD;
