@@ -22,6 +22,7 @@ namespace {
 constexpr int kBT = 256;          // threads per factor CTA
 constexpr int kMaxSlotsAll = 4;   // columns per thread -> n <= kBT * kMaxSlotsAll
 constexpr int kRows = 8;          // rows of a column loaded per register batch
+constexpr int kBatchNQ = 2;       // threads per column in the diagonal sweep (+ one coefficient warp)
 
 template <int KB, int kMaxSlots>
 __global__ void __launch_bounds__(kBT, 3) batched_kernel(double *__restrict__ Lall, int64_t n, int64_t ldl,
@@ -30,10 +31,11 @@ __global__ void __launch_bounds__(kBT, 3) batched_kernel(double *__restrict__ La
     extern __shared__ double smem_b[];
     double(*Ls)[kD + 1] = reinterpret_cast<double(*)[kD + 1]>(smem_b);  // [kD][kD+1]
     double *panel = smem_b + kD * (kD + 1);                              // panel_doubles(k)
-    double *vrow = panel + ((panel_doubles(k) + 1) & ~1ll);              // [KB] (16-byte aligned for cs)
-    double *IM = vrow + KB;                                              // [KB]
-    double2 *cs = reinterpret_cast<double2 *>(IM + KB);                  // [KB]
-    double *rho_s = reinterpret_cast<double *>(cs + KB);
+    double *vx = panel + wave_panel_doubles(KB) + 1;                     // [kD*KB] wave_sweep scratch
+    double *dinv = vx + kD * KB;                                         // [kD]
+    double *vt = dinv + kD;                                              // [kD*KB]
+    double *imx = vt + kD * KB;                                          // [kD*KB]
+    double *Vs = imx + kD * KB;                                          // [kD*KB]
 
     const int t = threadIdx.x;
     const int64_t f = blockIdx.x;
@@ -59,27 +61,30 @@ __global__ void __launch_bounds__(kBT, 3) batched_kernel(double *__restrict__ La
             const int m = idx / kD, j = idx % kD;
             if (m < Db && j <= m) Ls[m][j] = L[(r0 + j) + (r0 + m) * ldl];
         }
+        // owner threads hand their V state of the block's columns to the sweep
         const int slot_b = (int)(r0 / kBT);
         const int tbase = (int)(r0 % kBT);
-        double vd[KB];
+        if (t >= tbase && t < tbase + kD) {
 #pragma unroll
-        for (int e = 0; e < KB; ++e) {
-            double x = 0.0;
+            for (int e = 0; e < KB; ++e) {
+                double x = 0.0;
 #pragma unroll
-            for (int s = 0; s < kMaxSlots; ++s)
-                if (s == slot_b) x = v[s][e];
-            vd[e] = x;
+                for (int s = 0; s < kMaxSlots; ++s)
+                    if (s == slot_b) x = v[s][e];
+                Vs[(t - tbase) * KB + e] = x;
+            }
         }
         __syncthreads();
-        block_sweep<KB, kD + 1>(Ls, vd, Db, k, sigma, r0, panel, V + r0, n, key, 0, vrow, IM, cs, rho_s, tbase);
+        wave_sweep<KB, kBatchNQ, kD + 1>(Ls, Vs, Db, k, sigma, r0, panel, V + r0, n, key, 0, vx, dinv, vt, imx, 0,
+                                         kBatchNQ * kD / 32);
         for (int idx = t; idx < kD * kD; idx += kBT) {
             const int m = idx / kD, j = idx % kD;
             if (m < Db && j <= m) L[(r0 + j) + (r0 + m) * ldl] = Ls[m][j];
         }
         if (b + 1 == nb) break;
         // ---- Apply panel b to rows r0.. of every column to the right of the block
-        const double2 *pcs = reinterpret_cast<const double2 *>(panel);
-        const double *prho = panel + 2 * kD * k;
+        const double2 *pcs = reinterpret_cast<const double2 *>(panel);  // stride KB (padded rank)
+        const double *prho = panel + 2 * kD * KB;
         const double *pnu = prho + kD;
 #pragma unroll
         for (int s = 0; s < kMaxSlots; ++s) {
@@ -97,7 +102,7 @@ __global__ void __launch_bounds__(kBT, 3) batched_kernel(double *__restrict__ La
                 }
 #pragma unroll
                 for (int q = 0; q < kRows; ++q)
-                    col[j0 + q] = apply_row<KB>(buf[q], v[s], pcs + (j0 + q) * k, prho[j0 + q], k);
+                    col[j0 + q] = apply_row<KB>(buf[q], v[s], pcs + (j0 + q) * KB, prho[j0 + q], KB);
                 if (j0 + kRows < kD) {
 #pragma unroll
                     for (int q = 0; q < kRows; ++q) buf[q] = nxt[q];
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(kBT, 3) batched_kernel(double *__restrict__ La
 template <int KB, int SLOTS>
 gcm_status_t batched_launch_s(double *L, int64_t n, int64_t ldl, int64_t strideL, double *V, int64_t strideV, int k,
                               int sigma, int64_t batch, unsigned long long *keys, cudaStream_t stream) {
-    const size_t smem = (size_t)(kD * (kD + 1) + panel_doubles(k) + 1 + 4 * KB + 2) * sizeof(double);
+    const size_t smem = (size_t)(kD * (kD + 1) + wave_panel_doubles(KB) + 1 + 4 * kD * KB + kD) * sizeof(double);
     gcm_status_t st = check_cuda(
         cudaFuncSetAttribute(batched_kernel<KB, SLOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (st != GCM_OK) return st;

@@ -649,8 +649,11 @@ __global__ void gscan_kernel(const double *__restrict__ Q, double *__restrict__ 
 }
 
 // One CTA per 64-row diagonal block, all blocks in parallel.
+constexpr int kDiagNQ = 4;                        // threads per column in the diagonal sweep
+constexpr int kDiagThreads = kDiagNQ * kD + 32;  // column parts + the coefficient warp
+
 template <int KB>
-__global__ void __launch_bounds__(kD) bdiag_kernel(double *__restrict__ L, int64_t n, int64_t ldl,
+__global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict__ L, int64_t n, int64_t ldl,
                                                    double *__restrict__ V, int k, int sigma,
                                                    const double *__restrict__ P, const double *__restrict__ Q,
                                                    double *__restrict__ Uout, double *__restrict__ panels,
@@ -659,24 +662,29 @@ __global__ void __launch_bounds__(kD) bdiag_kernel(double *__restrict__ L, int64
     double(*Ls)[kD + 1] = reinterpret_cast<double(*)[kD + 1]>(smem_bdiag);               // [kD][kD+1]
     double(*Ps)[KB + 1] = reinterpret_cast<double(*)[KB + 1]>(smem_bdiag + kD * (kD + 1)); // [kD][KB+1]
     double(*M)[KB + 1] = reinterpret_cast<double(*)[KB + 1]>(smem_bdiag + kD * (kD + 1) + kD * (KB + 1));
-    __shared__ double vrow[KB], IM[KB], rho_s;
-    __shared__ double2 cs[KB];
+    double *pan = smem_bdiag + kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1);  // panel (16-byte aligned below)
+    pan += (reinterpret_cast<uintptr_t>(pan) & 15) ? 1 : 0;
+    double *vx = pan + wave_panel_doubles(KB) + 1;
+    double *dinv = vx + kD * KB;
+    double *vt = dinv + kD;
+    double *imx = vt + kD * KB;
+    double *Vs = imx + kD * KB;
     const int t = threadIdx.x;
     const int b = blockIdx.x;
     const int64_t r0 = (int64_t)b * kD;
     const int Db = (int)imin64(kD, n - r0);
 
     // G_b (prefix-summed by gscan_kernel)  ->  M = I + sigma G_b
-    for (int o = t; o < k * k; o += kD) {
+    for (int o = t; o < k * k; o += kDiagThreads) {
         const double g = Q[(int64_t)b * k * k + o];
         const int e1 = o / k, e2 = o % k;
         M[e1][e2] = (e1 == e2 ? 1.0 : 0.0) + (sigma > 0 ? g : -g);
     }
-    for (int idx = t; idx < kD * kD; idx += kD) {
+    for (int idx = t; idx < kD * kD; idx += kDiagThreads) {
         const int m = idx / kD, j = idx % kD;
         if (m < Db && j <= m) Ls[m][j] = L[(r0 + j) + (r0 + m) * ldl];
     }
-    for (int o = t; o < kD * k; o += kD) {
+    for (int o = t; o < kD * k; o += kDiagThreads) {
         const int m = o / k, e = o % k;
         Ps[m][e] = m < Db ? P[(r0 + m) * k + e] : 0.0;
     }
@@ -695,7 +703,7 @@ __global__ void __launch_bounds__(kD) bdiag_kernel(double *__restrict__ L, int64
         }
     }
     __syncthreads();
-    for (int o = t; o < k * k; o += kD) {
+    for (int o = t; o < k * k; o += kDiagThreads) {
         const int e1 = o / k, e2 = o % k;
         Uout[(int64_t)b * k * k + o] = e2 <= e1 ? M[e1][e2] : 0.0;
     }
@@ -722,9 +730,22 @@ __global__ void __launch_bounds__(kD) bdiag_kernel(double *__restrict__ L, int64
         }
     }
     __syncthreads();
+    if (t < kD)
+#pragma unroll
+        for (int e = 0; e < KB; ++e) Vs[t * KB + e] = (t < Db && e < k) ? v[e] : 0.0;
+    __syncthreads();  // wave_sweep reads Vs from other threads before its own first barrier
+    wave_sweep<KB, kDiagNQ, kD + 1>(Ls, Vs, Db, k, sigma, r0, pan, V + r0, n, key, ebase, vx, dinv, vt, imx, 0,
+                                    kDiagNQ * kD / 32);
+    // panel out, from stride KB (smem) to the global layout (stride k)
     double *panel = panels + (int64_t)b * panel_doubles(k);
-    block_sweep<KB, kD + 1>(Ls, v, Db, k, sigma, r0, panel, V + r0, n, key, ebase, vrow, IM, cs, &rho_s);
-    for (int idx = t; idx < kD * kD; idx += kD) {
+    for (int i = t; i < kD * k; i += kDiagThreads) {
+        const int j = i / k, e = i % k;
+        panel[2 * i] = pan[2 * (j * KB + e)];
+        panel[2 * i + 1] = pan[2 * (j * KB + e) + 1];
+    }
+    for (int i = t; i < kD; i += kDiagThreads) panel[2 * kD * k + i] = pan[2 * kD * KB + i];
+    for (int i = t; i < k; i += kDiagThreads) panel[2 * kD * k + kD + i] = pan[2 * kD * KB + kD + i];
+    for (int idx = t; idx < kD * kD; idx += kDiagThreads) {
         const int m = idx / kD, j = idx % kD;
         if (m < Db && j <= m) L[(r0 + j) + (r0 + m) * ldl] = Ls[m][j];
     }
@@ -879,12 +900,15 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
         ProfScope ps("gscan", stream);
         gscan_kernel<<<1, 1024, 0, stream>>>(Q, G, lay.NB, k);
     }
-    const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1)) * sizeof(double);
+    const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 +
+                                      4 * kD * KB + kD) *
+                             sizeof(double);
     st = check_cuda(cudaFuncSetAttribute(bdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_diag));
     if (st != GCM_OK) return st;
     {
         ProfScope ps("bdiag", stream);
-        bdiag_kernel<KB><<<lay.NB, kD, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, G, U, panels, key, ebase);
+        bdiag_kernel<KB><<<lay.NB, kDiagThreads, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, G, U, panels, key,
+                                                                      ebase);
     }
     if (lay.NB > 1) {
         const size_t smem_apply = (size_t)(2 * kD * k + kD + KB + KB * KB + 2 * kD * kLdC) * sizeof(double);

@@ -26,6 +26,26 @@ namespace gcm {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Reciprocal and reciprocal square root on the chain: the MUFU approximation
+// plus two Newton steps (quadratic convergence from ~2^-23: fully accurate to a
+// couple of ulp) instead of the IEEE division/sqrt sequences with their
+// slow-path branches (rounding-only difference).
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    return y * fma(-h * y, y, 1.5);
+}
+
 __device__ __forceinline__ void record_failure(unsigned long long *key, int64_t e, int64_t row, int code) {
     atomicMin(key, info_key(e, row, code));
 }
@@ -47,7 +67,7 @@ __device__ __forceinline__ double compute_row_warp(int lane, double d0, const do
         if (lane == 0) record_failure(key, ebase, grow, 2);
         d = __longlong_as_double(0x7ff8000000000000ll);
     }
-    const double invd = 1.0 / d;
+    const double invd = fast_rcp(d);
     double base = d * d;       // x_{j,-1}
     double rbase = invd * invd;
     for (int c0 = 0; c0 < k; c0 += 32) {
@@ -71,7 +91,7 @@ __device__ __forceinline__ double compute_row_warp(int lane, double d0, const do
             if (lane == first) record_failure(key, ebase + e, grow, 1);
             if (lane >= first) x = __longlong_as_double(0x7ff8000000000000ll);
         }
-        const double rx = 1.0 / x;
+        const double rx = fast_rcp(x);
         double rxp = __shfl_up_sync(kFull, rx, 1);
         if (lane == 0) rxp = rbase;
         if (valid) {
@@ -149,6 +169,139 @@ __device__ __forceinline__ void block_sweep(double (*Ls)[LD], double (&v)[KMAX],
     __syncthreads();
     double *nu_g = panel + 2ll * kD * k + kD;
     for (int e = t; e < k; e += blockDim.x) nu_g[e] = sqrt(IM[e]);
+}
+
+// Wavefront variant of block_sweep.  The Compute
+// of (row j, column e) needs only (j, e-1) [through x] and (j-1, e) [through
+// column j's V after row j-1's rotation e], so all (j, e) on an anti-diagonal
+// j + e = tau are independent: tick tau computes them in one dedicated warp
+// (lane = e) and, after one barrier, the column threads apply them.  The block
+// costs Db + KB - 1 ticks instead of Db full rows.  The running L of element
+// (j, m) lives in Ls[m][j] between ticks, so the KB rotations of a column can be
+// split over NQ threads (thread (m, q) owns update columns q*KB/NQ ..) at no cost.
+// The rank is padded to KB (update columns k..KB-1 have V = 0: identity
+// rotations, gamma = delta = 0), so all indices are compile-time.
+//   Vs[m*KB + e]   : column m's TRUE V state at block start (caller fills, smem, and
+//                    synchronises the CTA before the call)
+//   Ls[m][j]       : L(r0+j, r0+m) (smem), L~ on exit
+//   threads tbase + q*kD + m (q < NQ, m < Db) : column parts; warp cwarp: coefficients
+//   pan            : smem panel, (gamma, delta) at pan[2*(j*KB+e)], rho at 2*kD*KB, nu at +kD
+// Scratch (smem): vx[kD*KB], dinv[kD], vt[kD*KB], imx[kD*KB].  Called by ALL threads.
+#ifdef GCM_SWEEP_TRACE
+__device__ long long gcm_sweep_trace[4 * 256];
+#endif
+__host__ __device__ constexpr int wave_panel_doubles(int KB) { return 2 * kD * KB + kD + KB; }
+
+template <int KB, int NQ, int LD>
+__device__ __forceinline__ void wave_sweep(double (*Ls)[LD], const double *Vs, int Db, int k, int sigma, int64_t r0,
+                                           double *pan, double *vexit, int64_t ldv, unsigned long long *key,
+                                           int64_t ebase, double *vx, double *dinv, double *vt, double *imx,
+                                           int tbase, int cwarp) {
+    static_assert(KB <= 32 && KB % NQ == 0, "wave_sweep: KB <= 32 update columns, NQ | KB");
+    constexpr int EPT = KB / NQ;
+    const int t = threadIdx.x;
+    const int rel = t - tbase;
+    const int m = rel % kD, q = rel / kD;
+    const bool colthr = rel >= 0 && rel < NQ * kD && m < Db;
+    const bool cthr = (t >> 5) == cwarp;
+    const int lane = t & 31;
+    double *rho_g = pan + 2 * kD * KB;
+    double *nu_g = rho_g + kD;
+    const int e0 = q * EPT;
+    double v[EPT];
+    if (colthr) {
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) v[i] = Vs[m * KB + e0 + i];
+        if (m == 0)
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) vx[e0 + i] = v[i];  // row 0 computes on the initial V
+        if (q == 0) {
+            double d = Ls[m][m];
+            if (!(d > 0.0)) d = __longlong_as_double(0x7ff8000000000000ll);
+            dinv[m] = fast_rcp(d);
+        }
+    }
+    __syncthreads();
+    double im = 1.0;             // compute lane e: 1/mu^2 of its previous row
+    double xr = 0.0, rxr = 0.0;  // x_{j,e} and 1/x_{j,e} of the last tick (read by lane e+1)
+    const int ticks = Db + KB - 1;
+    for (int tau = 0; tau < ticks; ++tau) {
+#ifdef GCM_SWEEP_TRACE
+        if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[tau * 4 + 0] = clock64();
+#endif
+        if (cthr) {
+            const int e = lane;
+            const int j = tau - e;
+            const double xup = __shfl_up_sync(kFull, xr, 1);
+            const double rxup = __shfl_up_sync(kFull, rxr, 1);
+            if (e < KB && j >= 0 && j < Db) {
+                const double d = Ls[j][j];
+                const double id = dinv[j];
+                const double vv = vx[j * KB + e];
+                const double xp = e == 0 ? d * d : xup;
+                const double rxp = e == 0 ? id * id : rxup;
+                const double a = sigma > 0 ? vv * im : -(vv * im);
+                double x = fma(a, vv, xp);
+                const bool bad = !(x > 0.0) || !(d > 0.0);
+                if (bad) {
+                    if (e == 0 && !(d > 0.0)) record_failure(key, ebase, r0 + j, 2);
+                    else if (e < k) record_failure(key, ebase + e, r0 + j, 1);
+                    x = __longlong_as_double(0x7ff8000000000000ll);
+                }
+                const double rx = fast_rcp(x);
+                double2 gd;
+                gd.x = a * id;       // gamma
+                gd.y = vv * d * rx;  // delta
+                *reinterpret_cast<double2 *>(pan + 2 * (j * KB + e)) = gd;
+                vt[j * KB + e] = vv;
+                imx[j * KB + e] = im;
+                im = im * x * rxp;
+                if (e == KB - 1) rho_g[j] = d * fast_rsqrt(x);  // L_jj / L~_jj
+                if (j == Db - 1) nu_g[e] = sqrt(im);
+                xr = x;
+                rxr = rx;
+            }
+#ifdef GCM_SWEEP_TRACE
+            if (blockIdx.x == 0 && lane == 0) gcm_sweep_trace[tau * 4 + 1] = clock64();
+#endif
+        }
+        __syncthreads();
+        if (colthr) {
+            const double *lrow = &Ls[m][0];
+            double2 gd[EPT];
+            double lv[EPT];
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const int jc = min(max(tau - e0 - i, 0), Db - 1);
+                gd[i] = *reinterpret_cast<const double2 *>(pan + 2 * (jc * KB + e0 + i));
+                lv[i] = lrow[jc];
+            }
+            const int jlast = tau - (KB - 1);
+            const double rl = (q == NQ - 1 && jlast >= 0 && jlast < m) ? rho_g[jlast] : 1.0;
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const int j = tau - e0 - i;
+                const double l = fma(gd[i].x, v[i], lv[i]);
+                const double vn = fma(-gd[i].y, l, v[i]);
+                if (j >= 0 && j < m) {
+                    v[i] = vn;
+                    Ls[m][j] = (q == NQ - 1 && i == EPT - 1) ? l * rl : l;
+                    if (j == m - 1) vx[m * KB + e0 + i] = vn;  // column m after row m-1: row m may compute
+                }
+            }
+#ifdef GCM_SWEEP_TRACE
+            if (blockIdx.x == 0 && rel == 0) gcm_sweep_trace[tau * 4 + 3] = clock64();
+#endif
+        }
+        __syncthreads();
+    }
+    // epilogue: L~_jj and V_exit (true residual v = vt / mu = vt sqrt(IM_{j-1}))
+    for (int idx = t; idx < Db * k; idx += blockDim.x) {
+        const int j = idx / k, e = idx % k;
+        vexit[j + (int64_t)e * ldv] = vt[j * KB + e] * sqrt(imx[j * KB + e]);
+    }
+    if (colthr && q == 0) Ls[m][m] = Ls[m][m] / rho_g[m];  // w = L_jj / rho_j
+    __syncthreads();
 }
 
 }  // namespace gcm
