@@ -117,12 +117,20 @@ gcm_status_t gcm_modify_batched(double *L, int64_t n, int64_t ldl, int64_t strid
  * L_local is n x n_local column-major (ldl_local >= n), n_local = the number
  * of columns this rank owns; V_local holds the V rows of those columns
  * (n_local x k, ld n_local), overwritten with their V_exit rows.  Every rank
- * calls gcm_modify_dist with identical (n, nb, k, sigma); it is collective. */
+ * calls gcm_modify_dist with identical (n, nb, k, sigma); it is collective.
+ * nb must be a positive multiple of 64 (the panel height), else GCM_EINVAL.
+ * Per 64-row block the owner of its columns runs the diagonal Compute chain and
+ * one ncclBroadcast (root = owner) ships its coefficient panel; every rank then
+ * applies it to its own columns.  d_info (device, nullable) receives the global
+ * first failure on every rank.  Built without NCCL: GCM_ENOTSUP. */
 typedef struct gcm_comm *gcm_comm_t;
 gcm_status_t gcm_comm_unique_id(void *host_id_out /* 128 bytes */);
 gcm_status_t gcm_comm_init(gcm_comm_t *comm, const void *host_id, int nranks, int rank);
 gcm_status_t gcm_comm_destroy(gcm_comm_t comm);
+/* Number of columns rank `rank` owns (block-cyclic, width nb), or -1 on bad arguments. Host only. */
 int64_t gcm_dist_local_cols(int64_t n, int64_t nb, int nranks, int rank);
+/* Global column index of local column `local_col` of rank `rank`, or -1. Host only. */
+int64_t gcm_dist_global_col(int64_t nb, int nranks, int rank, int64_t local_col);
 gcm_status_t gcm_modify_dist(gcm_comm_t comm, double *L_local, int64_t n, int64_t nb,
                              int64_t ldl_local, double *V_local, int64_t k, int sigma,
                              gcm_info_t *d_info, gcm_stream_t stream);

@@ -28,6 +28,7 @@ SIGNATURES = {
     "gcm_comm_init": (_int, [ctypes.POINTER(_vp), _vp, _int, _int]),
     "gcm_comm_destroy": (_int, [_vp]),
     "gcm_dist_local_cols": (_i64, [_i64, _i64, _int, _int]),
+    "gcm_dist_global_col": (_i64, [_i64, _int, _int, _i64]),
     "gcm_modify_dist": (_int, [_vp, _dp, _i64, _i64, _i64, _dp, _i64, _int, _vp, _vp]),
     "gcm_profile_enable": (_int, [_int]),
     "gcm_profile_read": (_int, [ctypes.c_char_p, _vp, _vp, _int]),

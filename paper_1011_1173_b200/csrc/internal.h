@@ -58,6 +58,15 @@ struct ProfScope {
 };
 
 // algorithms (enqueue only; arguments already validated, n > 0, k > 0)
+// Sweep building blocks on arbitrary (local) column ranges, k <= kKMax:
+//  sweep_diag : the Compute chain of one diagonal block (Db rows/columns); Lb -> element
+//               (r0, first column), Vb -> V row of the first column (ld ldv); grow0 = r0
+//               (global row index, for failure reports); writes the coefficient panel.
+//  sweep_apply: that panel applied to ncols columns (Lr -> element (r0, first column)).
+gcm_status_t sweep_diag(double *Lb, int64_t ldl, int Db, double *Vb, int64_t ldv, int k, int sigma, int64_t grow0,
+                        double *panel, unsigned long long *key, int64_t ebase, cudaStream_t stream);
+gcm_status_t sweep_apply(double *Lr, int64_t ldl, int Db, int64_t ncols, double *Vc, int64_t ldv, int k,
+                         const double *panel, cudaStream_t stream);
 gcm_status_t modify_sweep(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
                           unsigned long long *key, double *panels, cudaStream_t stream);
 gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,

@@ -1,0 +1,86 @@
+"""Column-sharded multi-GPU binding (include/gcm.h: gcm_comm_*, gcm_modify_dist).
+
+One process per GPU.  torch.distributed is used only to share the 128-byte NCCL
+unique id; the data path is the library's own NCCL broadcasts of coefficient
+panels.  Argument marshalling only.
+
+Layout (block-cyclic columns, width nb, a multiple of 64): rank r owns global
+column blocks g = r, r + P, r + 2P, ...; ``L_local`` is a float64 CUDA tensor of
+shape (n_local, ldl) whose row c is the (global) column ``global_cols(...)[c]``
+of L (all n rows); ``V_local`` is (k, n_local): the V entries of those columns.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from ._native import GcmError
+
+
+def local_cols(n: int, nb: int, world: int, rank: int) -> int:
+    v = _native.lib().gcm_dist_local_cols(n, nb, world, rank)
+    if v < 0:
+        raise ValueError("invalid block-cyclic layout arguments")
+    return int(v)
+
+
+def global_cols(n: int, nb: int, world: int, rank: int) -> np.ndarray:
+    """Global column index of every local column of `rank` (increasing)."""
+    nloc = local_cols(n, nb, world, rank)
+    lib = _native.lib()
+    return np.array([lib.gcm_dist_global_col(nb, world, rank, c) for c in range(nloc)], dtype=np.int64)
+
+
+class Comm:
+    """NCCL communicator of the library.  world == 1 needs no process group."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        lib = _native.lib()
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _native.check("gcm_comm_unique_id", lib.gcm_comm_unique_id(uid))
+        if world > 1:
+            import torch.distributed as dist
+            obj = [uid.raw if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+        self._h = ctypes.c_void_p()
+        _native.check("gcm_comm_init", lib.gcm_comm_init(ctypes.byref(self._h), uid, world, rank))
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self._h:
+            _native.check("gcm_comm_destroy", _native.lib().gcm_comm_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def modify_dist(comm: Comm, L_local, V_local, n: int, nb: int, sigma: int, info=None, stream=None) -> None:
+    """Collective in-place modification of the sharded factor (every rank calls it)."""
+    import torch
+    if L_local.dtype != torch.float64 or V_local.dtype != torch.float64 or not (L_local.is_cuda and V_local.is_cuda):
+        raise ValueError("L_local and V_local must be float64 CUDA tensors")
+    if not (L_local.is_contiguous() and V_local.is_contiguous()):
+        raise ValueError("L_local and V_local must be contiguous")
+    nloc = local_cols(n, nb, comm.world, comm.rank)
+    if L_local.shape[0] != nloc or (V_local.numel() and V_local.shape[1] != nloc):
+        raise ValueError(f"this rank owns {nloc} columns")
+    k = V_local.shape[0]
+    ldl = L_local.shape[1]
+    if stream is None:
+        stream = torch.cuda.current_stream(L_local.device)
+    ip = ctypes.c_void_p(info.data_ptr()) if info is not None else None
+    st = _native.lib().gcm_modify_dist(comm._h, ctypes.c_void_p(L_local.data_ptr()), n, nb, ldl,
+                                       ctypes.c_void_p(V_local.data_ptr()), k, int(sigma), ip,
+                                       ctypes.c_void_p(stream.cuda_stream))
+    _native.check("gcm_modify_dist", st)
+
+
+__all__ = ["Comm", "modify_dist", "local_cols", "global_cols", "GcmError"]
