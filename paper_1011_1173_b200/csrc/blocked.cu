@@ -95,10 +95,18 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 #ifdef GCM_TRACE
+__device__ __forceinline__ long long gtime() {
+    long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
+__device__ long long g_htrace[4096 * 8];  // hand-off timeline in globaltimer ns, indexed by strip s
+#define HTRACE(slot, s) (g_htrace[(s) * 8 + (slot)] = gtime())
 __device__ long long g_trace[4096 * 8];
 #define TRACE(slot, tb) (blockIdx.x == 0 ? (void)(g_trace[(tb) * 8 + (slot)] = clock64()) : (void)0)
 #else
 #define TRACE(slot, tb) ((void)0)
+#define HTRACE(slot, s) ((void)0)
 #endif
 
 constexpr size_t kChkBudget = 2ull << 30;  // bytes of Apply checkpoints before CI doubles
@@ -164,6 +172,8 @@ constexpr int kSeg = (kLookC - 1) * kDT;  // rows of the prepared part of a look
 constexpr int kLdS = kSeg + 2;            // smem stride of a segment column (even: 16-byte bulk copies)
 constexpr int kLdT = kDT + 1;
 constexpr int kHelpMaxOwn = 4;          // strips whose residual a helper keeps in shared memory
+constexpr int kHelpRing = 6;            // L tiles a helper keeps in flight (cp.async ring)
+constexpr int kHelpPRing = 8;           // P blocks a helper keeps resident (loaded in batches)
 static_assert((kSvcWarp + 2) * 32 <= kTrsvThreads, "chain CTA needs publisher and loader warps");
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -331,6 +341,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
             while (ld_acquire(a.rflag + tb) != a.epoch) {
             }
         if (pt == 0) TRACE(5, tb - 1);
+        if (pt == 0 && c == 0) HTRACE(3, tb);
         named_bar(2, kPrepThreads);
         if (pt < kDT * kRPC) {
             const int jj = pt / kRPC, w = pt % kRPC;
@@ -372,6 +383,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
                 }
                 __threadfence();
                 st_release64(a.prog + c, ((unsigned long long)a.epoch << 32) | (unsigned)(tb + 1));
+                if (c == 0 && tb + kLookC + 1 < NT) HTRACE(0, tb + kLookC + 1);
             }
             __syncwarp();
         }
@@ -514,98 +526,137 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         if (s - kLookC <= 0) cta_publish(a.rflag + s, a.epoch);
     }
     __syncthreads();
-    constexpr int NL = (kDT * kDT) / kTrsvThreads;
-    double pre[NL];
-    auto prefetch = [&](int tb, int s) {  // static operand: issue before waiting on the chain
-        const int64_t c0 = (int64_t)s * kDT;
-        const int nc = (int)imin64(kDT, a.n - c0);
-#pragma unroll
-        for (int q = 0; q < NL; ++q) {
-            const int idx = t + q * kTrsvThreads, cc = idx / kDT, m = idx % kDT;
-            pre[q] = cc < nc ? a.L[((int64_t)tb * kDT + m) + (c0 + cc) * a.ldl] : 0.0;
+    // Tiles (tb, s), s owned and > tb, in tb-major order.  L tiles are static, so
+    // they stream through a kHelpRing-deep cp.async ring that runs ahead of the
+    // chain; only the small P block of each tb waits for the chains' progress.
+    int nown = 0;
+    for (int s = h; s < NT; s += H) ++nown;
+    struct It {
+        int tb, ii;
+    };
+    auto first_owned_after = [&](int tb) { return tb < h ? 0 : (tb - h) / H + 1; };
+    auto valid = [&](const It &x) { return x.tb < last && x.ii < nown; };
+    auto advance = [&](It &x) {
+        if (++x.ii >= nown) {
+            ++x.tb;
+            x.ii = first_owned_after(x.tb);
         }
     };
+    double *ring = rs + kHelpMaxOwn * kDT * KB;  // [kHelpRing][kDT * kLdT]
+    auto issue = [&](const It &x, int seq) {
+        if (valid(x)) {
+            const int s = h + x.ii * H;
+            double *stg = ring + (seq % kHelpRing) * (kDT * kLdT);
+            const int64_t c0 = (int64_t)s * kDT;
+            const int nc = (int)imin64(kDT, a.n - c0);
+            for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
+                const int cc = idx / kDT, m = idx % kDT;
+                if (cc < nc) cp_async8(stg + cc * kLdT + m, a.L + ((int64_t)x.tb * kDT + m) + (c0 + cc) * a.ldl);
+            }
+        }
+        cp_async_commit();  // possibly empty: keeps one group per task
+    };
     __shared__ int avail_s;
-    int done = 0;  // blocks of P already applied to the owned strips
-    while (done < last) {
-        // wait until every chain has published beyond `done`; take all available blocks
-        if (t < 32) {
-            unsigned m;
-            for (;;) {
-                unsigned cnt = 0xffffffffu;
-                if (t < a.NC) {
-                    const unsigned long long v = ld_acquire64(a.prog + t);
-                    cnt = (unsigned)(v >> 32) == a.epoch ? (unsigned)v : 0u;
-                }
-                m = __reduce_min_sync(kFull, cnt);
-                if ((int)m > done) break;
-                __nanosleep(64);
-            }
-            if (t == 0) avail_s = (int)m;
-        }
-        __syncthreads();
-        const int avail = min(avail_s, last);
-        for (int tb = done; tb < avail; ++tb) {
-            int sfirst = h;
-            while (sfirst <= tb) sfirst += H;
-            prefetch(tb, sfirst);
-            for (int o = t; o < kDT * KB; o += kTrsvThreads) {
-                const int m = o / KB, e = o % KB;
-                Pt[o] = (e < k && (int64_t)tb * kDT + m < a.n) ? __ldcg(a.P + ((int64_t)tb * kDT + m) * k + e) : 0.0;
-            }
-            int ii = 0;
-            for (int s = h; s < NT; s += H, ++ii) {
-                if (s <= tb) continue;
-                if (s != sfirst) prefetch(tb, s);
-#pragma unroll
-                for (int q = 0; q < NL; ++q) {
-                    const int idx = t + q * kTrsvThreads, cc = idx / kDT, m = idx % kDT;
-                    Lb[cc * kLdT + m] = pre[q];
-                }
-                __syncthreads();
-                const int64_t c0 = (int64_t)s * kDT;
-                const int nc = (int)imin64(kDT, a.n - c0);
-                double *r = rptr(ii, s);
-                const int ld = rstride(ii);
-                double racc[NQ];
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int o = t + q * kTrsvThreads;
-                    const int cc = o / KB, e = o % KB;
-                    double s0 = 0.0, s1 = 0.0;
-                    if (o < kDT * KB && cc < nc && e < k) {
-                        s0 = r[cc * ld + e];
-                        const double *Lc = Lb + cc * kLdT;
-#pragma unroll 8
-                        for (int m = 0; m < kDT; m += 2) {
-                            s0 = fma(-Lc[m], Pt[m * KB + e], s0);
-                            s1 = fma(-Lc[m + 1], Pt[(m + 1) * KB + e], s1);
-                        }
-                    }
-                    racc[q] = s0 + s1;
-                }
-                const bool chain_handoff = (tb + 1 == s - kLookC);
-                const int b64 = (tb + 1) / 2, s64 = s / 2;
-                const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 % a.CI == 0);
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int o = t + q * kTrsvThreads;
-                    const int cc = o / KB, e = o % KB;
-                    if (o < kDT * KB && cc < nc && e < k) {
-                        const double v = racc[q];
-                        r[cc * ld + e] = v;
-                        if (chain_handoff) a.rchain[c0 * k + (int64_t)cc * k + e] = v;
-                        if (checkpoint)
-                            a.chk[(chk_count_before(s64, a.CI) + b64 / a.CI) * kD * k + ((s % 2) * kDT + cc) * k + e] =
-                                v;
-                    }
-                }
-                if (chain_handoff) cta_publish(a.rflag + s, a.epoch);
-                __syncthreads();  // Lb reuse
-            }
-        }
-        done = avail;
+    double *pring = ring + kHelpRing * (kDT * kLdT);  // [kHelpPRing][kDT][KB]: P blocks by tb % kHelpPRing
+    int p_next = 0;                                   // first tb whose P block is not loaded yet
+    It pit{0, first_owned_after(0)}, iit = pit;
+    for (int q = 0; q < kHelpRing - 1; ++q) {
+        issue(iit, q);
+        advance(iit);
     }
+    int known = 0;
+    for (int seq = 0; valid(pit); ++seq) {
+        const int tb = pit.tb;
+        if (tb >= known) {  // wait until every chain has published block tb
+            if (t < 32) {
+                unsigned mm;
+                for (;;) {
+                    unsigned cnt = 0xffffffffu;
+                    if (t < a.NC) {
+                        const unsigned long long v = ld_acquire64(a.prog + t);
+                        cnt = (unsigned)(v >> 32) == a.epoch ? (unsigned)v : 0u;
+                    }
+                    mm = __reduce_min_sync(kFull, cnt);
+                    if ((int)mm > tb) break;
+                    __nanosleep(32);
+                }
+                if (t == 0) avail_s = (int)mm;
+            }
+            __syncthreads();
+            known = avail_s;
+        }
+        if (tb >= p_next) {  // load every published-but-not-loaded P block (one latency per batch)
+            const int p_end = min(min(known, last), tb + kHelpPRing);
+            for (int o = t; o < (p_end - tb) * kDT * KB; o += kTrsvThreads) {
+                const int bb = tb + o / (kDT * KB), w = o % (kDT * KB);
+                const int m = w / KB, e = w % KB;
+                pring[(bb % kHelpPRing) * kDT * KB + w] =
+                    (e < k && (int64_t)bb * kDT + m < a.n) ? __ldcg(a.P + ((int64_t)bb * kDT + m) * k + e) : 0.0;
+            }
+            p_next = p_end;
+        }
+        const double *Pt = pring + (tb % kHelpPRing) * kDT * KB;
+        issue(iit, seq + kHelpRing - 1);
+        advance(iit);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kHelpRing - 1) : "memory");
+        __syncthreads();
+        const int ii = pit.ii;
+        const int s = h + ii * H;
+        if (t == 0 && tb + 1 == s - kLookC) HTRACE(1, s);
+        const double *Lt = ring + (seq % kHelpRing) * (kDT * kLdT);
+        const int64_t c0 = (int64_t)s * kDT;
+        const int nc = (int)imin64(kDT, a.n - c0);
+        double *r = rptr(ii, s);
+        const int ld = rstride(ii);
+        // r[c][e] -= sum_m L(m, c) P[m][e]: thread = (column c, update-column pair eg);
+        // P pairs as 16-byte loads, 4 independent accumulators (tiles never straddle n)
+        constexpr int EG = KB / 2;                  // pairs per column
+        constexpr int CPP = kTrsvThreads / EG;      // columns per pass
+        const bool chain_handoff = (tb + 1 == s - kLookC);
+        const int b64 = (tb + 1) / 2, s64 = s / 2;
+        const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 % a.CI == 0);
+#pragma unroll
+        for (int pass = 0; pass < (kDT + CPP - 1) / CPP; ++pass) {
+            const int cc = pass * CPP + t / EG, eg = t % EG;
+            if (cc < kDT && cc < nc && 2 * eg < k) {
+                const double *Lc = Lt + cc * kLdT;
+                const double2 *Pp = reinterpret_cast<const double2 *>(Pt) + eg;
+                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+                for (int m = 0; m < kDT; m += 2) {
+                    const double l0 = Lc[m], l1 = Lc[m + 1];
+                    const double2 p0 = Pp[m * EG], p1 = Pp[(m + 1) * EG];
+                    a0 = fma(l0, p0.x, a0);
+                    a1 = fma(l0, p0.y, a1);
+                    b0 = fma(l1, p1.x, b0);
+                    b1 = fma(l1, p1.y, b1);
+                }
+                const int e = 2 * eg;
+                double *rr = r + cc * ld + e;
+                const double v0 = rr[0] - (a0 + b0);
+                rr[0] = v0;
+                double v1 = 0.0;
+                if (e + 1 < k) {
+                    v1 = rr[1] - (a1 + b1);
+                    rr[1] = v1;
+                }
+                if (chain_handoff) {
+                    a.rchain[c0 * k + (int64_t)cc * k + e] = v0;
+                    if (e + 1 < k) a.rchain[c0 * k + (int64_t)cc * k + e + 1] = v1;
+                }
+                if (checkpoint) {
+                    double *ck = a.chk + (chk_count_before(s64, a.CI) + b64 / a.CI) * kD * k + ((s % 2) * kDT + cc) * k + e;
+                    ck[0] = v0;
+                    if (e + 1 < k) ck[1] = v1;
+                }
+            }
+        }
+        if (chain_handoff) cta_publish(a.rflag + s, a.epoch);
+        if (chain_handoff && t == 0) HTRACE(2, s);
+        __syncthreads();  // ring stage, Pt and r reuse
+        advance(pit);
+    }
+    cp_async_wait_all();
 }
 
 template <int KB>
@@ -869,8 +920,9 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (st == GCM_OK) st = check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (st != GCM_OK) return st;
     const size_t smem_chain = (size_t)ChainSmem::total * sizeof(double);
-    const size_t smem_help =
-        (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + kHelpMaxOwn * kDT * KB) * sizeof(double);
+    const size_t smem_help = (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + kHelpMaxOwn * kDT * KB +
+                                      kHelpRing * kDT * kLdT + kHelpPRing * kDT * KB) *
+                             sizeof(double);
     const size_t smem = std::max(smem_chain, smem_help);
     st = check_cuda(cudaFuncSetAttribute(trsv_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (st != GCM_OK) return st;
@@ -927,6 +979,9 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
 #ifdef GCM_TRACE
 extern "C" int gcm_debug_trace(long long *host, int count) {
     return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * count);
+}
+extern "C" int gcm_debug_htrace(long long *host, int count) {
+    return (int)cudaMemcpyFromSymbol(host, g_htrace, sizeof(long long) * count);
 }
 #endif
 

@@ -30,3 +30,15 @@ names = ["crit.start", "crit.p_done", "prep.start", "prep.mbar_ok", "prep.partia
 for s in range(1, 8):
     d = t[1:-2, s] - t[1:-2, 0]
     print(f"  {names[s]:22s} - crit.start: median {np.median(d):8.0f}  p10 {np.percentile(d,10):8.0f} p90 {np.percentile(d,90):8.0f}")
+
+if hasattr(lib, "gcm_debug_htrace"):
+    hb = (ctypes.c_longlong * (4096 * 8))()
+    lib.gcm_debug_htrace(hb, 4096 * 8)
+    h = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8)[:NT].astype(np.float64)
+    ok = (h[:, 0] > 0) & (h[:, 1] > 0) & (h[:, 2] > 0) & (h[:, 3] > 0)
+    hh = h[ok]
+    print(f"hand-off timeline (ns, globaltimer) over {ok.sum()} strips:")
+    print(f"  chain publish P -> helper starts hand-off tile: median {np.median(hh[:,1]-hh[:,0]):.0f}")
+    print(f"  helper tile start -> rflag published:           median {np.median(hh[:,2]-hh[:,1]):.0f}")
+    print(f"  rflag published -> chain prep sees it:          median {np.median(hh[:,3]-hh[:,2]):.0f}")
+    print(f"  chain publish P -> chain sees hand-off:         median {np.median(hh[:,3]-hh[:,0]):.0f}")
