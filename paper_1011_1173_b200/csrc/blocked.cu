@@ -29,6 +29,7 @@
 //   bapply_kernel      per (tile segment, column strip): V-state from the
 //                      checkpoint, then the scaled 2-FMA Apply of the panels.
 #include <cooperative_groups.h>
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 
 #include <algorithm>
 
@@ -152,7 +153,8 @@ struct TrsvArgs {
     int k;
     double *P, *rcur, *rchain, *chk;
     double *MX;       // per 32-block: M^T (row-major) then X (row-major), X = L_bb^{-1}, M = X^T L_{b-1,b}^T
-    bool bulk_ok;     // L 16-byte aligned and ldl even: TMA bulk copies of column segments
+    bool bulk_ok;     // L 16-byte aligned and ldl even: TMA loads of the lookahead segments
+    CUtensorMap tmapL;  // 2-D tensor map over L (rows contiguous, ldl stride), box kSeg rows x 32 columns
     int CI;
     int NC;           // chain CTAs (each solves kRPC right-hand sides)
     unsigned long long *prog;  // [NC] chain progress: (epoch << 32) | blocks published
@@ -169,7 +171,7 @@ constexpr int kPrepWarps = 4;           // chain CTA warps: 0..kRPC-1 critical, 
 constexpr int kPrepThreads = kPrepWarps * 32;
 constexpr int kSvcWarp = kRPC + kPrepWarps;  // publisher warp; kSvcWarp + 1 = loader warp
 constexpr int kSeg = (kLookC - 1) * kDT;  // rows of the prepared part of a lookahead segment
-constexpr int kLdS = kSeg + 2;            // smem stride of a segment column (even: 16-byte bulk copies)
+constexpr int kLdS = kSeg;                // smem stride of a segment column (dense: the TMA box layout)
 constexpr int kLdT = kDT + 1;
 constexpr int kHelpMaxOwn = 4;          // strips whose residual a helper keeps in shared memory
 constexpr int kHelpRing = 6;            // L tiles a helper keeps in flight (cp.async ring)
@@ -267,12 +269,14 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         if (bulk) {
             if (lane == 0) {
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // helpers' generic stores -> TMA reads
-                const unsigned segb = (unsigned)(kSeg - skip) * 8u;
-                const unsigned bytes = (unsigned)nc * segb + 2u * kDT * kDT * 8u;
+                const unsigned bytes = (unsigned)(kSeg * kDT) * 8u + 2u * kDT * kDT * 8u;
                 mbar_arrive_expect_tx(bar, bytes);
-                if (segb)
-                    for (int j = 0; j < nc; ++j)
-                        bulk_g2s(st + j * kLdS + skip, a.L + (rs + skip) + (c0 + j) * a.ldl, segb, bar);
+                // one 2-D TMA box: rows rs .. rs+kSeg-1 (negative rows are zero-filled), columns c0..c0+31
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                    "[%4];" ::"r"(smem_u32(st)),
+                    "l"(reinterpret_cast<uint64_t>(&a.tmapL)), "r"((int)rs), "r"((int)c0), "r"(smem_u32(bar))
+                    : "memory");
                 bulk_g2s(st + S::seg, a.MX + (int64_t)tb * 2 * kDT * kDT, 2u * kDT * kDT * 8u, bar);
             }
         } else {
@@ -660,8 +664,8 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
 }
 
 template <int KB>
-__global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(TrsvArgs a) {
-    extern __shared__ double smem_trsv[];
+__global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_constant__ TrsvArgs a) {
+    extern __shared__ __align__(128) double smem_trsv[];
     if ((int)blockIdx.x < a.NC)
         trsv_chain(a, smem_trsv, blockIdx.x);
     else
@@ -892,6 +896,30 @@ __global__ void __launch_bounds__(kApplyT) bapply_kernel(double *__restrict__ L,
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool encode_tmap_L(CUtensorMap *m, const double *L, int64_t n, int64_t ldl) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            return false;
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldl * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)kSeg, (cuuint32_t)kDT};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(L), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int KB>
 gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, int sigma, unsigned long long *key,
                           int64_t ebase, char *wsbase, const Layout &lay, unsigned epoch, cudaStream_t stream) {
@@ -905,7 +933,8 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.rcur = reinterpret_cast<double *>(wsbase + lay.rcur);
     a.rchain = reinterpret_cast<double *>(wsbase + lay.rchain);
     a.MX = reinterpret_cast<double *>(wsbase + lay.MX);
-    a.bulk_ok = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0);
+    a.bulk_ok = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0) && n <= 0x7fffffff &&
+                encode_tmap_L(&a.tmapL, L, n, ldl);
     a.chk = reinterpret_cast<double *>(wsbase + lay.chk);
     a.CI = lay.CI;
     unsigned *flags = reinterpret_cast<unsigned *>(wsbase + lay.flags);
