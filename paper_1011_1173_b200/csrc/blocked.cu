@@ -41,7 +41,8 @@ namespace gcm {
 namespace {
 
 constexpr int kDT = 32;            // rows per triangular-solve block
-constexpr int kTrsvThreads = 256;
+constexpr int kTrsvThreads = 288;  // chain CTA: 2 critical + 5 prep + publisher + loader warps;
+                                   // helper CTA: 8 compute warps + 1 feeder warp
 constexpr int kBKMax = 32;         // update columns per pass
 constexpr int kApplyT = 64;        // threads per apply CTA (= kD columns)
 
@@ -167,15 +168,15 @@ constexpr int kRPC = 2;                 // right-hand sides per chain CTA
 #define GCM_LOOKC 4
 #endif
 constexpr int kLookC = GCM_LOOKC;       // blocks of lookahead the chain absorbs
-constexpr int kPrepWarps = 4;           // chain CTA warps: 0..kRPC-1 critical, then prep, publisher, loader
+constexpr int kPrepWarps = 5;           // chain CTA warps: 0..kRPC-1 critical, then prep, publisher, loader
 constexpr int kPrepThreads = kPrepWarps * 32;
 constexpr int kSvcWarp = kRPC + kPrepWarps;  // publisher warp; kSvcWarp + 1 = loader warp
 constexpr int kSeg = (kLookC - 1) * kDT;  // rows of the prepared part of a lookahead segment
 constexpr int kLdS = kSeg;                // smem stride of a segment column (dense: the TMA box layout)
 constexpr int kLdT = kDT + 1;
 constexpr int kHelpMaxOwn = 4;          // strips whose residual a helper keeps in shared memory
-constexpr int kHelpRing = 6;            // L tiles a helper keeps in flight (cp.async ring)
-constexpr int kHelpPRing = 8;           // P blocks a helper keeps resident (loaded in batches)
+constexpr int kHelpRing = 6;            // tiles (L tile + P block) a helper's feeder keeps in flight
+constexpr int kHelpCompute = 256;       // helper compute threads (warps 0..7); warp 8 feeds
 static_assert((kSvcWarp + 2) * 32 <= kTrsvThreads, "chain CTA needs publisher and loader warps");
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -530,9 +531,12 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         if (s - kLookC <= 0) cta_publish(a.rflag + s, a.epoch);
     }
     __syncthreads();
-    // Tiles (tb, s), s owned and > tb, in tb-major order.  L tiles are static, so
-    // they stream through a kHelpRing-deep cp.async ring that runs ahead of the
-    // chain; only the small P block of each tb waits for the chains' progress.
+    // Tiles (tb, s), s owned and > tb, in tb-major order, flow through a ring of
+    // kHelpRing shared-memory slots (L tile + P block).  Warp 8 (the feeder) runs
+    // ahead: it issues the static L tile as soon as a slot is free, waits until
+    // every chain has published P_tb, copies P_tb, and the slot's mbarrier completes
+    // when both cp.async batches land.  Warps 0..7 only compute, so a helper's
+    // tile throughput is its GEMM, not its memory and polling latency.
     int nown = 0;
     for (int s = h; s < NT; s += H) ++nown;
     struct It {
@@ -546,121 +550,139 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             x.ii = first_owned_after(x.tb);
         }
     };
-    double *ring = rs + kHelpMaxOwn * kDT * KB;  // [kHelpRing][kDT * kLdT]
-    auto issue = [&](const It &x, int seq) {
-        if (valid(x)) {
-            const int s = h + x.ii * H;
-            double *stg = ring + (seq % kHelpRing) * (kDT * kLdT);
+    constexpr int kPLd = KB + 1;  // odd row stride of the P block in a slot (bank spread for the mma B loads)
+    constexpr int kSlot = kDT * kLdT + kDT * kPLd;
+    double *ring = rs + kHelpMaxOwn * kDT * KB;  // [kHelpRing][kSlot]
+    unsigned long long *full = reinterpret_cast<unsigned long long *>(ring + kHelpRing * kSlot);
+    unsigned long long *empty = full + kHelpRing;
+    if (t == 0) {
+        for (int i = 0; i < kHelpRing; ++i) {
+            mbar_init(full + i, 64u);  // 2 noinc arrivals per feeder lane (L batch, P batch)
+            mbar_init(empty + i, kHelpCompute / 32);
+        }
+    }
+    __syncthreads();
+    const int warp = t >> 5, lane = t & 31;
+    if (warp == kHelpCompute / 32) {
+        // ------------------------------------------------------------ feeder
+        int known = 0;
+        int seq = 0;
+        for (It it{0, first_owned_after(0)}; valid(it); advance(it), ++seq) {
+            const int slot = seq % kHelpRing, use = seq / kHelpRing;
+            if (use > 0) mbar_wait(empty + slot, (unsigned)((use - 1) & 1));
+            double *stg = ring + slot * kSlot;
+            const int s = h + it.ii * H;
             const int64_t c0 = (int64_t)s * kDT;
             const int nc = (int)imin64(kDT, a.n - c0);
-            for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
-                const int cc = idx / kDT, m = idx % kDT;
-                if (cc < nc) cp_async8(stg + cc * kLdT + m, a.L + ((int64_t)x.tb * kDT + m) + (c0 + cc) * a.ldl);
-            }
-        }
-        cp_async_commit();  // possibly empty: keeps one group per task
-    };
-    __shared__ int avail_s;
-    double *pring = ring + kHelpRing * (kDT * kLdT);  // [kHelpPRing][kDT][KB]: P blocks by tb % kHelpPRing
-    int p_next = 0;                                   // first tb whose P block is not loaded yet
-    It pit{0, first_owned_after(0)}, iit = pit;
-    for (int q = 0; q < kHelpRing - 1; ++q) {
-        issue(iit, q);
-        advance(iit);
-    }
-    int known = 0;
-    for (int seq = 0; valid(pit); ++seq) {
-        const int tb = pit.tb;
-        if (tb >= known) {  // wait until every chain has published block tb
-            if (t < 32) {
+            for (int cc = 0; cc < nc; ++cc)  // lane = row: coalesced 256-byte column segments
+                cp_async8(stg + cc * kLdT + lane, a.L + ((int64_t)it.tb * kDT + lane) + (c0 + cc) * a.ldl);
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
+            if (it.tb >= known) {  // wait until every chain has published block tb
                 unsigned mm;
                 for (;;) {
                     unsigned cnt = 0xffffffffu;
-                    if (t < a.NC) {
-                        const unsigned long long v = ld_acquire64(a.prog + t);
+                    if (lane < a.NC) {
+                        const unsigned long long v = ld_acquire64(a.prog + lane);
                         cnt = (unsigned)(v >> 32) == a.epoch ? (unsigned)v : 0u;
                     }
                     mm = __reduce_min_sync(kFull, cnt);
-                    if ((int)mm > tb) break;
-                    __nanosleep(32);
+                    if ((int)mm > it.tb) break;
+                    __nanosleep(20);
                 }
-                if (t == 0) avail_s = (int)mm;
+                known = (int)mm;
             }
-            __syncthreads();
-            known = avail_s;
-        }
-        if (tb >= p_next) {  // load every published-but-not-loaded P block (one latency per batch)
-            const int p_end = min(min(known, last), tb + kHelpPRing);
-            for (int o = t; o < (p_end - tb) * kDT * KB; o += kTrsvThreads) {
-                const int bb = tb + o / (kDT * KB), w = o % (kDT * KB);
-                const int m = w / KB, e = w % KB;
-                pring[(bb % kHelpPRing) * kDT * KB + w] =
-                    (e < k && (int64_t)bb * kDT + m < a.n) ? __ldcg(a.P + ((int64_t)bb * kDT + m) * k + e) : 0.0;
+            __syncwarp();
+            if (lane == 0 && it.tb + 1 == s - kLookC) HTRACE(6, s);
+            double *pb = stg + kDT * kLdT;
+            for (int o = lane; o < kDT * k; o += 32) {
+                const int m = o / k, e = o % k;
+                if ((int64_t)it.tb * kDT + m < a.n)
+                    cp_async8(pb + m * kPLd + e, a.P + ((int64_t)it.tb * kDT + m) * k + e);
             }
-            p_next = p_end;
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
         }
-        const double *Pt = pring + (tb % kHelpPRing) * kDT * KB;
-        issue(iit, seq + kHelpRing - 1);
-        advance(iit);
-        asm volatile("cp.async.wait_group %0;" ::"n"(kHelpRing - 1) : "memory");
-        __syncthreads();
+        cp_async_wait_all();
+        return;
+    }
+    // ---------------------------------------------------------------- compute warps
+    int seq = 0;
+    for (It pit{0, first_owned_after(0)}; valid(pit); advance(pit), ++seq) {
+        const int tb = pit.tb;
+        const int slot = seq % kHelpRing;
+        mbar_wait(full + slot, (unsigned)((seq / kHelpRing) & 1));
         const int ii = pit.ii;
         const int s = h + ii * H;
         if (t == 0 && tb + 1 == s - kLookC) HTRACE(1, s);
-        const double *Lt = ring + (seq % kHelpRing) * (kDT * kLdT);
+        const double *Lt = ring + slot * kSlot;
+        const double *Pt = Lt + kDT * kLdT;
         const int64_t c0 = (int64_t)s * kDT;
         const int nc = (int)imin64(kDT, a.n - c0);
         double *r = rptr(ii, s);
         const int ld = rstride(ii);
-        // r[c][e] -= sum_m L(m, c) P[m][e]: thread = (column c, update-column pair eg);
-        // P pairs as 16-byte loads, 4 independent accumulators (tiles never straddle n)
-        constexpr int EG = KB / 2;                  // pairs per column
-        constexpr int CPP = kTrsvThreads / EG;      // columns per pass
+        // r[c][e] -= sum_m L(m, c) P[m][e] on the FP64 tensor cores: mma.sync m8n8k4
+        // (A = L^T 8 x 4 from the slot's L tile, B = P 4 x 8), one 8 x 8 output tile
+        // (8 columns x 8 update columns) per warp iteration, r in shared memory.
         const bool chain_handoff = (tb + 1 == s - kLookC);
         const int b64 = (tb + 1) / 2, s64 = s / 2;
         const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 % a.CI == 0);
+        constexpr int ET = (KB + 7) / 8;          // 8-wide update-column tiles
+        constexpr int NTILE = (kDT / 8) * ET;     // output tiles of the 32 x KB result
+        const int g = lane >> 2, t4 = lane & 3;
+        double vout[(NTILE + kHelpCompute / 32 - 1) / (kHelpCompute / 32)][2];
+        int tcount = 0;
+        for (int tile = warp; tile < NTILE; tile += kHelpCompute / 32, ++tcount) {
+            const int ct = tile / ET, et = tile % ET;
+            double acc0 = 0.0, acc1 = 0.0;
+            const double *Arow = Lt + (ct * 8 + g) * kLdT + t4;   // A[c][m] = L(m, c)
+            const int eb = et * 8 + g;                            // B column of this lane
 #pragma unroll
-        for (int pass = 0; pass < (kDT + CPP - 1) / CPP; ++pass) {
-            const int cc = pass * CPP + t / EG, eg = t % EG;
-            if (cc < kDT && cc < nc && 2 * eg < k) {
-                const double *Lc = Lt + cc * kLdT;
-                const double2 *Pp = reinterpret_cast<const double2 *>(Pt) + eg;
-                double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-#pragma unroll
-                for (int m = 0; m < kDT; m += 2) {
-                    const double l0 = Lc[m], l1 = Lc[m + 1];
-                    const double2 p0 = Pp[m * EG], p1 = Pp[(m + 1) * EG];
-                    a0 = fma(l0, p0.x, a0);
-                    a1 = fma(l0, p0.y, a1);
-                    b0 = fma(l1, p1.x, b0);
-                    b1 = fma(l1, p1.y, b1);
-                }
-                const int e = 2 * eg;
+            for (int k0 = 0; k0 < kDT; k0 += 4) {
+                const double av = Arow[k0];
+                const double bv = eb < k ? Pt[(k0 + t4) * kPLd + eb] : 0.0;
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(acc0), "+d"(acc1)
+                             : "d"(av), "d"(bv));
+            }
+            const int cc = ct * 8 + g, e = et * 8 + 2 * t4;
+            double v0 = 0.0, v1 = 0.0;
+            if (cc < nc) {
                 double *rr = r + cc * ld + e;
-                const double v0 = rr[0] - (a0 + b0);
-                rr[0] = v0;
-                double v1 = 0.0;
-                if (e + 1 < k) {
-                    v1 = rr[1] - (a1 + b1);
-                    rr[1] = v1;
-                }
+                if (e < k) rr[0] = v0 = rr[0] - acc0;
+                if (e + 1 < k) rr[1] = v1 = rr[1] - acc1;
                 if (chain_handoff) {
-                    a.rchain[c0 * k + (int64_t)cc * k + e] = v0;
+                    if (e < k) a.rchain[c0 * k + (int64_t)cc * k + e] = v0;
                     if (e + 1 < k) a.rchain[c0 * k + (int64_t)cc * k + e + 1] = v1;
                 }
-                if (checkpoint) {
-                    double *ck = a.chk + (chk_count_before(s64, a.CI) + b64 / a.CI) * kD * k + ((s % 2) * kDT + cc) * k + e;
-                    ck[0] = v0;
-                    if (e + 1 < k) ck[1] = v1;
+            }
+            vout[tcount][0] = v0;
+            vout[tcount][1] = v1;
+        }
+        if (chain_handoff && t == 0) HTRACE(4, s);
+        if (chain_handoff) {
+            named_bar(1, kHelpCompute);
+            if (t == 0) HTRACE(5, s);
+            if (t == 0) {
+                __threadfence();
+                st_release(a.rflag + s, a.epoch);
+                HTRACE(2, s);
+            }
+        }
+        if (checkpoint) {  // after the hand-off release: the chain does not wait for these
+            tcount = 0;
+            for (int tile = warp; tile < NTILE; tile += kHelpCompute / 32, ++tcount) {
+                const int ct = tile / ET, et = tile % ET;
+                const int cc = ct * 8 + g, e = et * 8 + 2 * t4;
+                if (cc < nc) {
+                    double *ck =
+                        a.chk + (chk_count_before(s64, a.CI) + b64 / a.CI) * kD * k + ((s % 2) * kDT + cc) * k + e;
+                    if (e < k) ck[0] = vout[tcount][0];
+                    if (e + 1 < k) ck[1] = vout[tcount][1];
                 }
             }
         }
-        if (chain_handoff) cta_publish(a.rflag + s, a.epoch);
-        if (chain_handoff && t == 0) HTRACE(2, s);
-        __syncthreads();  // ring stage, Pt and r reuse
-        advance(pit);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
     }
-    cp_async_wait_all();
 }
 
 template <int KB>
@@ -950,7 +972,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (st != GCM_OK) return st;
     const size_t smem_chain = (size_t)ChainSmem::total * sizeof(double);
     const size_t smem_help = (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + kHelpMaxOwn * kDT * KB +
-                                      kHelpRing * kDT * kLdT + kHelpPRing * kDT * KB) *
+                                      kHelpRing * (kDT * kLdT + kDT * (KB + 1)) + 2 * kHelpRing) *
                              sizeof(double);
     const size_t smem = std::max(smem_chain, smem_help);
     st = check_cuda(cudaFuncSetAttribute(trsv_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -42,3 +42,7 @@ if hasattr(lib, "gcm_debug_htrace"):
     print(f"  helper tile start -> rflag published:           median {np.median(hh[:,2]-hh[:,1]):.0f}")
     print(f"  rflag published -> chain prep sees it:          median {np.median(hh[:,3]-hh[:,2]):.0f}")
     print(f"  chain publish P -> chain sees hand-off:         median {np.median(hh[:,3]-hh[:,0]):.0f}")
+    ok2 = ok & (h[:, 4] > 0) & (h[:, 5] > 0) & (h[:, 6] > 0)
+    h2 = h[ok2]
+    print(f"  publish -> feeder sees progress: {np.median(h2[:,6]-h2[:,0]):.0f}; feeder -> data landed (tile start): {np.median(h2[:,1]-h2[:,6]):.0f}")
+    print(f"  tile start -> thread0 GEMM done: {np.median(h2[:,4]-h2[:,1]):.0f}; -> all compute done: {np.median(h2[:,5]-h2[:,1]):.0f}; -> rflag: {np.median(h2[:,2]-h2[:,1]):.0f}")
