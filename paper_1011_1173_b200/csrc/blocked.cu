@@ -918,6 +918,91 @@ __global__ void __launch_bounds__(kApplyT) bapply_kernel(double *__restrict__ L,
     }
 }
 
+// CI == 1 (every tile has its own checkpoint): one CTA per (row block b, group of
+// kStripsPerCta strips right of it).  The coefficient panel of block b is loaded
+// once per CTA; thread (q, c) owns column c of strip q: its V state starts at
+// U_b^{-1} r (the checkpointed residual), and the tile streams through shared
+// memory in kRC-row chunks (cp.async double buffer, coalesced loads and stores).
+constexpr int kStripsPerCta = 4;
+constexpr int kTileThreads = kStripsPerCta * kD;
+
+template <int KB>
+__global__ void __launch_bounds__(kTileThreads, 2) btile_kernel(double *__restrict__ L, int64_t n, int64_t ldl, int k,
+                                                                const double *__restrict__ chk,
+                                                                const double *__restrict__ U,
+                                                                const double *__restrict__ panels, int NB) {
+    const int b = blockIdx.x;
+    const int s0 = b + 1 + kStripsPerCta * blockIdx.y;  // first strip of this CTA
+    if (s0 >= NB) return;
+    extern __shared__ double2 smem_btile[];
+    double2 *cs = smem_btile;                                // [kD * k]
+    double *rho = reinterpret_cast<double *>(cs + kD * k);  // [kD]
+    double *nu = rho + kD;                                  // [KB]
+    double *Us = nu + KB;                                   // [KB * KB]
+    double *buf = Us + KB * KB;                             // [2][kStripsPerCta * kD][kLdC]
+    const int t = threadIdx.x;
+    const int q = t / kD, c = t % kD;
+    const int s = s0 + q;
+    const int64_t c0 = (int64_t)s * kD;
+    const int nstr = min(kStripsPerCta, NB - s0);  // strips in this CTA
+    const int64_t ncols_cta = imin64((int64_t)nstr * kD, n - (int64_t)s0 * kD);
+    constexpr int NCH = kD / kRC;
+    const int64_t rb = (int64_t)b * kD;
+    auto issue = [&](int ch) {
+        double *bb = buf + (ch & 1) * kStripsPerCta * kD * kLdC;
+        for (int idx = t; idx < kStripsPerCta * kD * kRC; idx += kTileThreads) {
+            const int col = idx / kRC, j = idx % kRC;
+            if (col < ncols_cta)
+                cp_async8(bb + col * kLdC + j, L + (rb + ch * kRC + j) + ((int64_t)s0 * kD + col) * ldl);
+        }
+        cp_async_commit();
+    };
+    issue(0);
+    const double *panel = panels + (int64_t)b * panel_doubles(k);
+    for (int i = t; i < kD * k; i += kTileThreads) cs[i] = make_double2(panel[2 * i], panel[2 * i + 1]);
+    for (int i = t; i < kD; i += kTileThreads) rho[i] = panel[2ll * kD * k + i];
+    for (int i = t; i < k; i += kTileThreads) nu[i] = panel[2ll * kD * k + kD + i];
+    for (int i = t; i < k * k; i += kTileThreads) Us[i] = U[(int64_t)b * k * k + i];
+    __syncthreads();
+    const bool act = q < nstr && c0 + c < n;
+    double v[KB];
+    if (act) {  // V-state = U_b^{-1} r  (forward substitution, k x k lower)
+        const double *r = chk + (chk_count_before(s, 1) + b) * kD * k + (int64_t)c * k;
+#pragma unroll
+        for (int e = 0; e < KB; ++e) {
+            if (e < k) {
+                double acc = r[e];
+#pragma unroll
+                for (int ep = 0; ep < e; ++ep) acc = fma(-Us[e * k + ep], v[ep], acc);
+                v[e] = acc / Us[e * k + e];
+            } else {
+                v[e] = 0.0;
+            }
+        }
+    }
+    for (int ch = 0; ch < NCH; ++ch) {
+        if (ch + 1 < NCH) {
+            issue(ch + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            cp_async_wait_all();
+        }
+        __syncthreads();
+        double *bb = buf + (ch & 1) * kStripsPerCta * kD * kLdC;
+        if (act) {
+            double *col = bb + t * kLdC;
+#pragma unroll 4
+            for (int j = 0; j < kRC; ++j)
+                col[j] = apply_row<KB>(col[j], v, cs + (ch * kRC + j) * k, rho[ch * kRC + j], k);
+        }
+        __syncthreads();
+        for (int idx = t; idx < kStripsPerCta * kD * kRC; idx += kTileThreads) {
+            const int col = idx / kRC, j = idx % kRC;
+            if (col < ncols_cta) L[(rb + ch * kRC + j) + ((int64_t)s0 * kD + col) * ldl] = bb[col * kLdC + j];
+        }
+    }
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -1018,6 +1103,17 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
         st = check_cuda(
             cudaFuncSetAttribute(bapply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_apply));
         if (st != GCM_OK) return st;
+        if (lay.CI == 1) {
+            const size_t smem_tile =
+                (size_t)(2 * kD * k + kD + KB + KB * KB + 2 * kStripsPerCta * kD * kLdC) * sizeof(double);
+            st = check_cuda(
+                cudaFuncSetAttribute(btile_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tile));
+            if (st != GCM_OK) return st;
+            const dim3 gridt(lay.NB - 1, (lay.NB - 1 + kStripsPerCta - 1) / kStripsPerCta);
+            ProfScope ps("bapply", stream);
+            btile_kernel<KB><<<gridt, kTileThreads, smem_tile, stream>>>(L, n, ldl, k, a.chk, U, panels, lay.NB);
+            return check_cuda(cudaGetLastError());
+        }
         const dim3 grid2(lay.NB - 1, (lay.NB - 1 + lay.CI - 1) / lay.CI);
         ProfScope ps("bapply", stream);
         bapply_kernel<KB><<<grid2, kApplyT, smem_apply, stream>>>(L, n, ldl, k, a.chk, lay.CI, U, panels);
