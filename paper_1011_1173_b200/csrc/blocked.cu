@@ -46,6 +46,19 @@ constexpr int kTrsvThreads = 288;  // chain CTA: 2 critical + 5 prep + publisher
 constexpr int kBKMax = 32;         // update columns per pass
 constexpr int kApplyT = 64;        // threads per apply CTA (= kD columns)
 
+#ifndef GCM_PROG_STRIDE
+#define GCM_PROG_STRIDE 16
+#endif
+#ifndef GCM_POLL_RELAXED
+#define GCM_POLL_RELAXED 1
+#endif
+#ifndef GCM_POLL_NS
+#define GCM_POLL_NS 20
+#endif
+// Each chain's progress word sits in its own 128-byte line: 140 helper feeders
+// poll them, and one shared line would serialise those polls on one L2 slice.
+constexpr int kProgStride = GCM_PROG_STRIDE;
+
 struct Layout {
     int64_t n;
     int k;
@@ -80,7 +93,7 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
         o += ((doubles * sizeof(double) + 255) / 256) * 256;
         return at;
     };
-    l.P = take((size_t)n * k);
+    l.P = take((size_t)l.NT * kDT * k);  // padded to whole 32-row blocks (bulk copies)
     l.rcur = take((size_t)l.NT * kDT * k);
     l.rchain = take((size_t)l.NT * kDT * k);
     l.MX = take((size_t)l.NT * 2 * kDT * kDT);
@@ -89,7 +102,8 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
     l.G = take((size_t)l.NB * k * k);
     l.U = take((size_t)l.NB * k * k);
     l.panels = take((size_t)l.NB * panel_doubles(k));
-    l.flags = take((2ull * l.NT * sizeof(unsigned) + 16 * sizeof(unsigned long long) + 7) / 8);  // prog[16], rflag, lflag
+    l.flags = take((2ull * l.NT * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
+                   8);  // prog[16 * kProgStride], rflag, lflag
     l.total = o;
     return l;
 }
@@ -104,11 +118,13 @@ __device__ __forceinline__ long long gtime() {
 }
 __device__ long long g_htrace[4096 * 8];  // hand-off timeline in globaltimer ns, indexed by strip s
 #define HTRACE(slot, s) (g_htrace[(s) * 8 + (slot)] = gtime())
+#define CTRACE(slot, s) (g_trace[(s) * 8 + (slot)] = clock64())
 __device__ long long g_trace[4096 * 8];
 #define TRACE(slot, tb) (blockIdx.x == 0 ? (void)(g_trace[(tb) * 8 + (slot)] = clock64()) : (void)0)
 #else
 #define TRACE(slot, tb) ((void)0)
 #define HTRACE(slot, s) ((void)0)
+#define CTRACE(slot, s) ((void)0)
 #endif
 
 constexpr size_t kChkBudget = 2ull << 30;  // bytes of Apply checkpoints before CI doubles
@@ -121,6 +137,17 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
 __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// polling load: relaxed (no L1 invalidation per poll); the caller fences once it
+// has seen the value it waits for
+__device__ __forceinline__ unsigned long long ld_poll64(const unsigned long long *p) {
+    unsigned long long v;
+#if GCM_POLL_RELAXED
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+#else
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+#endif
     return v;
 }
 __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
@@ -387,8 +414,9 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
                 while (*pcount < (unsigned)(kRPC * (tb + 1))) {
                 }
                 __threadfence();
-                st_release64(a.prog + c, ((unsigned long long)a.epoch << 32) | (unsigned)(tb + 1));
+                st_release64(a.prog + c * kProgStride, ((unsigned long long)a.epoch << 32) | (unsigned)(tb + 1));
                 if (c == 0 && tb + kLookC + 1 < NT) HTRACE(0, tb + kLookC + 1);
+                if (c < 8 && tb + kLookC + 1 < NT) HTRACE(c, 2048 + tb + kLookC + 1);
             }
             __syncwarp();
         }
@@ -550,14 +578,13 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             x.ii = first_owned_after(x.tb);
         }
     };
-    constexpr int kPLd = KB + 1;  // odd row stride of the P block in a slot (bank spread for the mma B loads)
-    constexpr int kSlot = kDT * kLdT + kDT * kPLd;
+    constexpr int kSlot = kDT * kLdT + kDT * KB;  // L tile [32][kLdT] + P block [32][k] (dense, bulk copy)
     double *ring = rs + kHelpMaxOwn * kDT * KB;  // [kHelpRing][kSlot]
     unsigned long long *full = reinterpret_cast<unsigned long long *>(ring + kHelpRing * kSlot);
     unsigned long long *empty = full + kHelpRing;
     if (t == 0) {
         for (int i = 0; i < kHelpRing; ++i) {
-            mbar_init(full + i, 64u);  // 2 noinc arrivals per feeder lane (L batch, P batch)
+            mbar_init(full + i, 33u);  // 1 noinc arrival per feeder lane (L batch) + the P bulk copy's arrive
             mbar_init(empty + i, kHelpCompute / 32);
         }
     }
@@ -569,7 +596,9 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         int seq = 0;
         for (It it{0, first_owned_after(0)}; valid(it); advance(it), ++seq) {
             const int slot = seq % kHelpRing, use = seq / kHelpRing;
+            if (lane == 0 && h == 60 && seq < 1000) CTRACE(3, 3000 + seq);
             if (use > 0) mbar_wait(empty + slot, (unsigned)((use - 1) & 1));
+            if (lane == 0 && h == 60 && seq < 1000) CTRACE(4, 3000 + seq);
             double *stg = ring + slot * kSlot;
             const int s = h + it.ii * H;
             const int64_t c0 = (int64_t)s * kDT;
@@ -577,29 +606,36 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             for (int cc = 0; cc < nc; ++cc)  // lane = row: coalesced 256-byte column segments
                 cp_async8(stg + cc * kLdT + lane, a.L + ((int64_t)it.tb * kDT + lane) + (c0 + cc) * a.ldl);
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
+            if (lane == 0 && it.tb + 1 == s - kLookC) HTRACE(7, s);
             if (it.tb >= known) {  // wait until every chain has published block tb
                 unsigned mm;
                 for (;;) {
                     unsigned cnt = 0xffffffffu;
                     if (lane < a.NC) {
-                        const unsigned long long v = ld_acquire64(a.prog + lane);
+                        const unsigned long long v = ld_poll64(a.prog + lane * kProgStride);
                         cnt = (unsigned)(v >> 32) == a.epoch ? (unsigned)v : 0u;
                     }
                     mm = __reduce_min_sync(kFull, cnt);
-                    if ((int)mm > it.tb) break;
-                    __nanosleep(20);
+                    if ((int)mm > it.tb) {
+#if GCM_POLL_RELAXED
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+                        break;
+                    }
+                    __nanosleep(GCM_POLL_NS);
                 }
                 known = (int)mm;
             }
             __syncwarp();
             if (lane == 0 && it.tb + 1 == s - kLookC) HTRACE(6, s);
-            double *pb = stg + kDT * kLdT;
-            for (int o = lane; o < kDT * k; o += 32) {
-                const int m = o / k, e = o % k;
-                if ((int64_t)it.tb * kDT + m < a.n)
-                    cp_async8(pb + m * kPLd + e, a.P + ((int64_t)it.tb * kDT + m) * k + e);
+            if (lane == 0 && h == 60 && seq < 1000) CTRACE(5, 3000 + seq);
+            if (lane == 0) {  // P_tb (32 x k, contiguous) with one bulk copy
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // chains' generic stores -> bulk read
+                const unsigned bytes = (unsigned)(kDT * k) * 8u;
+                mbar_arrive_expect_tx(full + slot, bytes);
+                bulk_g2s(stg + kDT * kLdT, a.P + (int64_t)it.tb * kDT * k, bytes, full + slot);
             }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
+            if (lane == 0 && h == 60 && seq < 1000) CTRACE(6, 3000 + seq);
         }
         cp_async_wait_all();
         return;
@@ -610,6 +646,7 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         const int tb = pit.tb;
         const int slot = seq % kHelpRing;
         mbar_wait(full + slot, (unsigned)((seq / kHelpRing) & 1));
+        if (t == 0 && h == 60 && seq < 1000) CTRACE(0, 3000 + seq);
         const int ii = pit.ii;
         const int s = h + ii * H;
         if (t == 0 && tb + 1 == s - kLookC) HTRACE(1, s);
@@ -619,45 +656,47 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         const int nc = (int)imin64(kDT, a.n - c0);
         double *r = rptr(ii, s);
         const int ld = rstride(ii);
-        // r[c][e] -= sum_m L(m, c) P[m][e] on the FP64 tensor cores: mma.sync m8n8k4
-        // (A = L^T 8 x 4 from the slot's L tile, B = P 4 x 8), one 8 x 8 output tile
-        // (8 columns x 8 update columns) per warp iteration, r in shared memory.
+        // r[c][e] -= sum_m L(m, c) P[m][e]: thread (c = t / 8, g = t % 8) owns update
+        // columns e = g, g + 8, ..; each 32-long dot product runs as two independent
+        // FMA chains, so the tile's latency is ~16 dependent FMAs (this tile is on
+        // the hand-off's critical path; throughput is not the constraint)
         const bool chain_handoff = (tb + 1 == s - kLookC);
         const int b64 = (tb + 1) / 2, s64 = s / 2;
         const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 % a.CI == 0);
-        constexpr int ET = (KB + 7) / 8;          // 8-wide update-column tiles
-        constexpr int NTILE = (kDT / 8) * ET;     // output tiles of the 32 x KB result
-        const int g = lane >> 2, t4 = lane & 3;
-        double vout[(NTILE + kHelpCompute / 32 - 1) / (kHelpCompute / 32)][2];
-        int tcount = 0;
-        for (int tile = warp; tile < NTILE; tile += kHelpCompute / 32, ++tcount) {
-            const int ct = tile / ET, et = tile % ET;
-            double acc0 = 0.0, acc1 = 0.0;
-            const double *Arow = Lt + (ct * 8 + g) * kLdT + t4;   // A[c][m] = L(m, c)
-            const int eb = et * 8 + g;                            // B column of this lane
+        constexpr int NE = (KB + 7) / 8;
+        const int cc = t >> 3, g = t & 7;
+        double vout[NE];
+        {
+            double s0[NE], s1[NE];
 #pragma unroll
-            for (int k0 = 0; k0 < kDT; k0 += 4) {
-                const double av = Arow[k0];
-                const double bv = eb < k ? Pt[(k0 + t4) * kPLd + eb] : 0.0;
-                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                             : "+d"(acc0), "+d"(acc1)
-                             : "d"(av), "d"(bv));
-            }
-            const int cc = ct * 8 + g, e = et * 8 + 2 * t4;
-            double v0 = 0.0, v1 = 0.0;
-            if (cc < nc) {
-                double *rr = r + cc * ld + e;
-                if (e < k) rr[0] = v0 = rr[0] - acc0;
-                if (e + 1 < k) rr[1] = v1 = rr[1] - acc1;
-                if (chain_handoff) {
-                    if (e < k) a.rchain[c0 * k + (int64_t)cc * k + e] = v0;
-                    if (e + 1 < k) a.rchain[c0 * k + (int64_t)cc * k + e + 1] = v1;
+            for (int u = 0; u < NE; ++u) s0[u] = s1[u] = 0.0;
+            const double *Lc = Lt + cc * kLdT;
+#pragma unroll
+            for (int m = 0; m < kDT; m += 2) {
+                const double l0 = Lc[m], l1 = Lc[m + 1];
+#pragma unroll
+                for (int u = 0; u < NE; ++u) {
+                    const int e = g + 8 * u;
+                    if (e < k) {
+                        s0[u] = fma(l0, Pt[m * k + e], s0[u]);
+                        s1[u] = fma(l1, Pt[(m + 1) * k + e], s1[u]);
+                    }
                 }
             }
-            vout[tcount][0] = v0;
-            vout[tcount][1] = v1;
+#pragma unroll
+            for (int u = 0; u < NE; ++u) {
+                const int e = g + 8 * u;
+                double v = 0.0;
+                if (cc < nc && e < k) {
+                    double *rr = r + cc * ld + e;
+                    *rr = v = *rr - (s0[u] + s1[u]);
+                    if (chain_handoff) a.rchain[c0 * k + (int64_t)cc * k + e] = v;
+                }
+                vout[u] = v;
+            }
         }
         if (chain_handoff && t == 0) HTRACE(4, s);
+        if (t == 0 && h == 60 && seq < 1000) CTRACE(1, 3000 + seq);
         if (chain_handoff) {
             named_bar(1, kHelpCompute);
             if (t == 0) HTRACE(5, s);
@@ -667,20 +706,14 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                 HTRACE(2, s);
             }
         }
-        if (checkpoint) {  // after the hand-off release: the chain does not wait for these
-            tcount = 0;
-            for (int tile = warp; tile < NTILE; tile += kHelpCompute / 32, ++tcount) {
-                const int ct = tile / ET, et = tile % ET;
-                const int cc = ct * 8 + g, e = et * 8 + 2 * t4;
-                if (cc < nc) {
-                    double *ck =
-                        a.chk + (chk_count_before(s64, a.CI) + b64 / a.CI) * kD * k + ((s % 2) * kDT + cc) * k + e;
-                    if (e < k) ck[0] = vout[tcount][0];
-                    if (e + 1 < k) ck[1] = vout[tcount][1];
-                }
-            }
+        if (checkpoint && cc < nc) {  // after the hand-off release: the chain does not wait for these
+            double *ck = a.chk + (chk_count_before(s64, a.CI) + b64 / a.CI) * kD * k + ((s % 2) * kDT + cc) * k;
+#pragma unroll
+            for (int u = 0; u < NE; ++u)
+                if (g + 8 * u < k) ck[g + 8 * u] = vout[u];
         }
         __syncwarp();
+        if (t == 0 && h == 60 && seq < 1000) CTRACE(2, 3000 + seq);
         if (lane == 0) mbar_arrive(empty + slot);
     }
 }
@@ -927,7 +960,7 @@ constexpr int kStripsPerCta = 4;
 constexpr int kTileThreads = kStripsPerCta * kD;
 
 template <int KB>
-__global__ void __launch_bounds__(kTileThreads, 2) btile_kernel(double *__restrict__ L, int64_t n, int64_t ldl, int k,
+__global__ void __launch_bounds__(kTileThreads, KB >= 32 ? 1 : 2) btile_kernel(double *__restrict__ L, int64_t n, int64_t ldl, int k,
                                                                 const double *__restrict__ chk,
                                                                 const double *__restrict__ U,
                                                                 const double *__restrict__ panels, int NB) {
@@ -935,8 +968,8 @@ __global__ void __launch_bounds__(kTileThreads, 2) btile_kernel(double *__restri
     const int s0 = b + 1 + kStripsPerCta * blockIdx.y;  // first strip of this CTA
     if (s0 >= NB) return;
     extern __shared__ double2 smem_btile[];
-    double2 *cs = smem_btile;                                // [kD * k]
-    double *rho = reinterpret_cast<double *>(cs + kD * k);  // [kD]
+    double2 *cs = smem_btile;                                // [kD * KB]
+    double *rho = reinterpret_cast<double *>(cs + kD * KB);  // [kD]
     double *nu = rho + kD;                                  // [KB]
     double *Us = nu + KB;                                   // [KB * KB]
     double *buf = Us + KB * KB;                             // [2][kStripsPerCta * kD][kLdC]
@@ -959,7 +992,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) btile_kernel(double *__restri
     };
     issue(0);
     const double *panel = panels + (int64_t)b * panel_doubles(k);
-    for (int i = t; i < kD * k; i += kTileThreads) cs[i] = make_double2(panel[2 * i], panel[2 * i + 1]);
+    // coefficients padded to stride KB (identity rotations for e >= k: gamma = delta = 0)
+    for (int i = t; i < kD * KB; i += kTileThreads) {
+        const int j = i / KB, e = i % KB;
+        cs[i] = e < k ? make_double2(panel[2 * (j * k + e)], panel[2 * (j * k + e) + 1]) : make_double2(0.0, 0.0);
+    }
     for (int i = t; i < kD; i += kTileThreads) rho[i] = panel[2ll * kD * k + i];
     for (int i = t; i < k; i += kTileThreads) nu[i] = panel[2ll * kD * k + kD + i];
     for (int i = t; i < k * k; i += kTileThreads) Us[i] = U[(int64_t)b * k * k + i];
@@ -990,10 +1027,29 @@ __global__ void __launch_bounds__(kTileThreads, 2) btile_kernel(double *__restri
         __syncthreads();
         double *bb = buf + (ch & 1) * kStripsPerCta * kD * kLdC;
         if (act) {
+            // rows held in registers and the (row, e) loops fully unrolled: row j+1's
+            // rotation e only waits for row j's rotation e, so rows pipeline
+            // instead of serialising on the 2k-deep chain of one row
+            constexpr int RG = KB <= 8 ? kRC : kRC / 2;
             double *col = bb + t * kLdC;
-#pragma unroll 4
-            for (int j = 0; j < kRC; ++j)
-                col[j] = apply_row<KB>(col[j], v, cs + (ch * kRC + j) * k, rho[ch * kRC + j], k);
+#pragma unroll
+            for (int g = 0; g < kRC; g += RG) {
+                double l[RG];
+#pragma unroll
+                for (int j = 0; j < RG; ++j) l[j] = col[g + j];
+                const double2 *cc = cs + (ch * kRC + g) * KB;
+#pragma unroll
+                for (int j = 0; j < RG; ++j) {
+#pragma unroll
+                    for (int e = 0; e < KB; ++e) {
+                        const double2 gd = cc[j * KB + e];
+                        l[j] = fma(gd.x, v[e], l[j]);
+                        v[e] = fma(-gd.y, l[j], v[e]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < RG; ++j) col[g + j] = l[j] * rho[ch * kRC + g + j];
+            }
         }
         __syncthreads();
         for (int idx = t; idx < kStripsPerCta * kD * kRC; idx += kTileThreads) {
@@ -1046,7 +1102,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.CI = lay.CI;
     unsigned *flags = reinterpret_cast<unsigned *>(wsbase + lay.flags);
     a.prog = reinterpret_cast<unsigned long long *>(flags);
-    a.rflag = flags + 2 * 16;
+    a.rflag = flags + 2 * 16 * kProgStride;
     a.lflag = a.rflag + lay.NT;
     a.epoch = epoch;
 
@@ -1105,7 +1161,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
         if (st != GCM_OK) return st;
         if (lay.CI == 1) {
             const size_t smem_tile =
-                (size_t)(2 * kD * k + kD + KB + KB * KB + 2 * kStripsPerCta * kD * kLdC) * sizeof(double);
+                (size_t)(2 * kD * KB + kD + KB + KB * KB + 2 * kStripsPerCta * kD * kLdC) * sizeof(double);
             st = check_cuda(
                 cudaFuncSetAttribute(btile_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tile));
             if (st != GCM_OK) return st;

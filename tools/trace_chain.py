@@ -46,3 +46,24 @@ if hasattr(lib, "gcm_debug_htrace"):
     h2 = h[ok2]
     print(f"  publish -> feeder sees progress: {np.median(h2[:,6]-h2[:,0]):.0f}; feeder -> data landed (tile start): {np.median(h2[:,1]-h2[:,6]):.0f}")
     print(f"  tile start -> thread0 GEMM done: {np.median(h2[:,4]-h2[:,1]):.0f}; -> all compute done: {np.median(h2[:,5]-h2[:,1]):.0f}; -> rflag: {np.median(h2[:,2]-h2[:,1]):.0f}")
+    ok3 = ok2 & (h[:, 7] > 0)
+    h3 = h[ok3]
+    print(f"  feeder reaches hand-off tile - publish: median {np.median(h3[:,7]-h3[:,0]):.0f} p10 {np.percentile(h3[:,7]-h3[:,0],10):.0f} p90 {np.percentile(h3[:,7]-h3[:,0],90):.0f}")
+    print(f"  per-chain publish skew unknown; feeder poll time (seen - max(reach, publish)): {np.median(h3[:,6]-np.maximum(h3[:,7],h3[:,0])):.0f}")
+    hc = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8)[2048:2048 + NT].astype(np.float64)
+    okc = np.all(hc > 0, axis=1)
+    print("  per-chain publish time - chain0 (median over strips):", np.median(hc[okc] - hc[okc][:, :1], axis=0))
+    rows = np.nonzero(ok3 & okc)[0]
+    print("  feeder reach - last chain publish: median", np.median(h[rows, 7] - hc[rows].max(axis=1)))
+    hs = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8)[3000:3060].astype(np.float64)
+    pub = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8)[2048:2048+NT, 0].astype(np.float64)  # chain0 publish of tb = s-5 at row s
+    base = hs[0, 3]
+    print("helper 60, per tile seq (tb = seq): times rel. to feeder start (us): feeder[pre-empty, got-empty, got-P] compute[start, gemm, end]  P_tb published")
+    for q in range(0, 60, 3):
+        ptb = pub[q + 5] - base if q + 5 < NT and pub[q + 5] > 0 else float('nan')
+        print(q, np.round((hs[q, [3, 4, 5, 0, 1, 2]] - base) / 1000, 2), round(ptb / 1000, 2))
+    hs = tr[3000:3060].astype(np.float64)
+    base = hs[0, 3]
+    print("helper 60 clock64 (kcycles rel): feeder[reach, got-empty, got-P, P-issued] compute[start, gemm, end]")
+    for q in range(0, 60, 3):
+        print(q, np.round((hs[q, [3, 4, 5, 6, 0, 1, 2]] - base) / 1000, 2))
