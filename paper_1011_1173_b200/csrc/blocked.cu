@@ -50,7 +50,10 @@ constexpr int kApplyT = 64;        // threads per apply CTA (= kD columns)
 #define GCM_PROG_STRIDE 16
 #endif
 #ifndef GCM_POLL_RELAXED
-#define GCM_POLL_RELAXED 1
+#define GCM_POLL_RELAXED 0
+#endif
+#ifndef GCM_PUB_FENCE
+#define GCM_PUB_FENCE 1
 #endif
 #ifndef GCM_POLL_NS
 #define GCM_POLL_NS 20
@@ -64,7 +67,7 @@ struct Layout {
     int k;
     int NT, NB, CI;
     int64_t nchk;
-    size_t P, rcur, rchain, MX, chk, Q, G, U, panels, flags, total;
+    size_t P, rcur, rchain, pfast, MX, chk, Q, G, U, panels, flags, total;
 };
 
 __host__ __device__ inline int64_t chk_count_before(int64_t s, int CI) {
@@ -73,6 +76,14 @@ __host__ __device__ inline int64_t chk_count_before(int64_t s, int CI) {
     if (S <= 0) return 0;
     const int64_t q = S / CI, r = S % CI;
     return CI * q * (q + 1) / 2 + (q + 1) * r;
+}
+
+// chk_count_before for CI = 2^CIlog without a 64-bit division (device hot loop)
+__device__ __forceinline__ int64_t chk_count_before_pow2(int s, int CIlog) {
+    const int S = s - 1;
+    if (S <= 0) return 0;
+    const int64_t q = S >> CIlog, r = S & ((1 << CIlog) - 1);
+    return ((q * (q + 1) / 2) << CIlog) + (q + 1) * r;
 }
 
 Layout make_layout(int64_t n, int k, size_t chk_budget) {
@@ -96,14 +107,15 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
     l.P = take((size_t)l.NT * kDT * k);  // padded to whole 32-row blocks (bulk copies)
     l.rcur = take((size_t)l.NT * kDT * k);
     l.rchain = take((size_t)l.NT * kDT * k);
+    l.pfast = take((size_t)l.NT * kDT * k);  // must follow rchain (one memset arms both)
     l.MX = take((size_t)l.NT * 2 * kDT * kDT);
     l.chk = take((size_t)l.nchk * kD * k);
     l.Q = take((size_t)l.NB * k * k);
     l.G = take((size_t)l.NB * k * k);
     l.U = take((size_t)l.NB * k * k);
     l.panels = take((size_t)l.NB * panel_doubles(k));
-    l.flags = take((2ull * l.NT * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
-                   8);  // prog[16 * kProgStride], rflag, lflag
+    l.flags = take((1ull * l.NT * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
+                   8);  // prog[16 * kProgStride], lflag
     l.total = o;
     return l;
 }
@@ -150,6 +162,37 @@ __device__ __forceinline__ unsigned long long ld_poll64(const unsigned long long
 #endif
     return v;
 }
+// Hand-off values are self-validating: rchain starts all-ones (a NaN no
+// producer writes, see handoff_value) and each chain thread polls its own
+// 8-byte value, so the hand-off needs no flag, no fence and no second round trip.
+constexpr unsigned long long kEmpty = ~0ull;
+__device__ __forceinline__ double handoff_value(double v) {
+    return v == v ? v : __longlong_as_double(0x7ff8000000000000ll);  // NaNs canonicalised
+}
+__device__ __forceinline__ void st_handoff(double *p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(handoff_value(v)) : "memory");
+}
+__device__ __forceinline__ double ld_handoff(double *p) {
+    unsigned long long u;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(u) : "l"(p) : "memory");
+    } while (u == kEmpty);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(kEmpty) : "memory");  // re-arm for the next call
+    return __longlong_as_double((long long)u);
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double *p) {
+    unsigned long long u;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(u) : "l"(p) : "memory");
+    return u;
+}
+// same, for values several consumers read (no re-arm; the pass's memset arms them)
+__device__ __forceinline__ double ld_value(const double *p) {
+    unsigned long long u;
+    do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(u) : "l"(p) : "memory");
+    } while (u == kEmpty);
+    return __longlong_as_double((long long)u);
+}
 __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -179,14 +222,14 @@ struct TrsvArgs {
     int64_t n, ldl;
     const double *V;  // this pass's first column (ld n)
     int k;
-    double *P, *rcur, *rchain, *chk;
+    double *P, *rcur, *rchain, *pfast, *chk;  // pfast: self-validating copy of P for the hand-off tiles
     double *MX;       // per 32-block: M^T (row-major) then X (row-major), X = L_bb^{-1}, M = X^T L_{b-1,b}^T
     bool bulk_ok;     // L 16-byte aligned and ldl even: TMA loads of the lookahead segments
     CUtensorMap tmapL;  // 2-D tensor map over L (rows contiguous, ldl stride), box kSeg rows x 32 columns
-    int CI;
+    int CI, CIlog;  // checkpoint interval (a power of two) and its log2
     int NC;           // chain CTAs (each solves kRPC right-hand sides)
     unsigned long long *prog;  // [NC] chain progress: (epoch << 32) | blocks published
-    unsigned *rflag, *lflag;
+    unsigned *lflag;
     unsigned epoch;
 };
 
@@ -203,9 +246,19 @@ constexpr int kLdS = kSeg;                // smem stride of a segment column (de
 constexpr int kLdT = kDT + 1;
 constexpr int kHelpMaxOwn = 4;          // strips whose residual a helper keeps in shared memory
 constexpr int kHelpRing = 6;            // tiles (L tile + P block) a helper's feeder keeps in flight
+#ifndef GCM_FASTBACK
+#define GCM_FASTBACK 2
+#endif
+constexpr int kFastBack = GCM_FASTBACK;         // tiles before the hand-off tile that also read P from pfast
 constexpr int kHelpCompute = 256;       // helper compute threads (warps 0..7); warp 8 feeds
 static_assert((kSvcWarp + 2) * 32 <= kTrsvThreads, "chain CTA needs publisher and loader warps");
 
+// Tile (tb, s) takes P_tb from pfast (no progress word, no bulk copy) when it is
+// the strip's hand-off tile or one of the kFastBack before it: those sit on the
+// chain's critical loop, the earlier ones have slack for the published path.
+__device__ __forceinline__ bool fast_tile(int tb, int s) {
+    return tb + 1 <= s - kLookC && tb + 1 >= s - kLookC - kFastBack;
+}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -369,21 +422,19 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
 #pragma unroll
         for (int w = 0; w < kRPC; ++w) part[(pw * kDT + j) * kRPC + w] = acc[w];
         if (pt == 0) TRACE(4, tb - 1);
-        if (pt == 0)
-            while (ld_acquire(a.rflag + tb) != a.epoch) {
-            }
-        if (pt == 0) TRACE(5, tb - 1);
-        if (pt == 0 && c == 0) HTRACE(3, tb);
         named_bar(2, kPrepThreads);
         if (pt < kDT * kRPC) {
             const int jj = pt / kRPC, w = pt % kRPC;
             const int e = e0 + w;
             const int64_t row = (int64_t)tb * kDT + jj;
-            double acc = (e < k && row < a.n) ? __ldcg(a.rchain + (int64_t)tb * kDT * k + (int64_t)jj * k + e) : 0.0;
+            double acc = 0.0;
 #pragma unroll
             for (int q = 0; q < kPrepWarps; ++q) acc += part[(q * kDT + jj) * kRPC + w];
+            if (e < k && row < a.n) acc += ld_handoff(a.rchain + (int64_t)tb * kDT * k + (int64_t)jj * k + e);
             accs[jj * kRPC + w] = acc;
         }
+        if (pt == 0) TRACE(5, tb - 1);
+        if (pt == 0 && c == 0) HTRACE(3, tb);
         named_bar(2, kPrepThreads);
         if (pt < kDT * kRPC) {  // prepX[j][w] = sum_q X(q, j) acc[q][w]   (X row-major in the stage)
             const int jj = pt % kDT, w = pt / kDT;
@@ -413,9 +464,12 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
             if (lane == 0) {
                 while (*pcount < (unsigned)(kRPC * (tb + 1))) {
                 }
+#if GCM_PUB_FENCE
                 __threadfence();
+#endif
                 st_release64(a.prog + c * kProgStride, ((unsigned long long)a.epoch << 32) | (unsigned)(tb + 1));
                 if (c == 0 && tb + kLookC + 1 < NT) HTRACE(0, tb + kLookC + 1);
+                if (c == 0) CTRACE(0, 1024 + tb);
                 if (c < 8 && tb + kLookC + 1 < NT) HTRACE(c, 2048 + tb + kLookC + 1);
             }
             __syncwarp();
@@ -453,7 +507,10 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
             pwin[((tb % kLookC) * kDT + j) * kRPC + w] = p;
             const int e = e0 + w;
             const int64_t row = (int64_t)tb * kDT + j;
-            if (e < k && row < a.n) a.P[row * k + e] = p;
+            if (e < k && row < a.n) {
+                a.P[row * k + e] = p;
+                st_handoff(a.pfast + row * k + e, p);  // polled by the helpers of strips tb+kLookC+1..
+            }
             if (t == 0) TRACE(1, tb);
             __syncwarp();
             if (lane == 0) {
@@ -551,12 +608,11 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             const int cc = o / k, e = o % k;
             const double v = cc < nc ? a.V[(c0 + cc) + (int64_t)e * a.n] : 0.0;
             r[cc * ld + e] = v;
-            if (s - kLookC <= 0) a.rchain[c0 * k + o] = v;
+            if (s - kLookC <= 0 && cc < nc) st_handoff(a.rchain + c0 * k + o, v);
             const int s64 = s / 2;
             if (s64 >= 1 && cc < nc)
                 a.chk[((int64_t)chk_count_before(s64, a.CI)) * kD * k + ((s % 2) * kDT + cc) * k + e] = v;
         }
-        if (s - kLookC <= 0) cta_publish(a.rflag + s, a.epoch);
     }
     __syncthreads();
     // Tiles (tb, s), s owned and > tb, in tb-major order, flow through a ring of
@@ -567,6 +623,7 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
     // tile throughput is its GEMM, not its memory and polling latency.
     int nown = 0;
     for (int s = h; s < NT; s += H) ++nown;
+
     struct It {
         int tb, ii;
     };
@@ -607,6 +664,10 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                 cp_async8(stg + cc * kLdT + lane, a.L + ((int64_t)it.tb * kDT + lane) + (c0 + cc) * a.ldl);
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
             if (lane == 0 && it.tb + 1 == s - kLookC) HTRACE(7, s);
+            if (fast_tile(it.tb, s)) {  // tiles next to the hand-off: the compute warps poll pfast themselves
+                if (lane == 0) mbar_arrive(full + slot);
+                continue;
+            }
             if (it.tb >= known) {  // wait until every chain has published block tb
                 unsigned mm;
                 for (;;) {
@@ -656,62 +717,110 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         const int nc = (int)imin64(kDT, a.n - c0);
         double *r = rptr(ii, s);
         const int ld = rstride(ii);
-        // r[c][e] -= sum_m L(m, c) P[m][e]: thread (c = t / 8, g = t % 8) owns update
-        // columns e = g, g + 8, ..; each 32-long dot product runs as two independent
-        // FMA chains, so the tile's latency is ~16 dependent FMAs (this tile is on
-        // the hand-off's critical path; throughput is not the constraint)
+        // r[c][e] -= sum_m L(m, c) P[m][e], register-blocked 2 columns x 2 update
+        // columns per thread (EG = KB/2 e-pairs, 16 * EG threads): per row m one
+        // L pair and one P pair feed four FMAs, so the tile costs ~kDT*(3 LDS +
+        // 4 FMA) per thread -- this tile is on the hand-off's critical path and
+        // shared-memory wavefronts, not FMAs, set its latency.
         const bool chain_handoff = (tb + 1 == s - kLookC);
         const int b64 = (tb + 1) / 2, s64 = s / 2;
-        const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 % a.CI == 0);
-        constexpr int NE = (KB + 7) / 8;
-        const int cc = t >> 3, g = t & 7;
-        double vout[NE];
-        {
-            double s0[NE], s1[NE];
+        const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 & (a.CI - 1)) == 0;
+        if (t == 0 && h == 60 && seq < 400) CTRACE(1, 3500 + seq);
+        if (fast_tile(tb, s)) {  // P_tb straight from the chains' self-validating copy
+            double *Pw = const_cast<double *>(Pt);
+            const double *src = a.pfast + (int64_t)tb * kDT * k;
+            constexpr int kPer = (kDT * KB + kHelpCompute - 1) / kHelpCompute;
+            unsigned long long u[kPer];
 #pragma unroll
-            for (int u = 0; u < NE; ++u) s0[u] = s1[u] = 0.0;
-            const double *Lc = Lt + cc * kLdT;
+            for (int q = 0; q < kPer; ++q) {  // issue every load first: one round trip, not kPer
+                const int o = t + q * kHelpCompute;
+                u[q] = o < kDT * k ? ld_relaxed_u64(src + o) : 0ull;
+            }
 #pragma unroll
-            for (int m = 0; m < kDT; m += 2) {
-                const double l0 = Lc[m], l1 = Lc[m + 1];
+            for (int q = 0; q < kPer; ++q) {
+                const int o = t + q * kHelpCompute;
+                if (o < kDT * k) {
+                    if (u[q] == kEmpty) u[q] = __double_as_longlong(ld_value(src + o));
+                    Pw[o] = __longlong_as_double((long long)u[q]);
+                }
+            }
+            if (t == 0 && h == 60 && seq < 1000) CTRACE(7, 3000 + seq);
+            named_bar(1, kHelpCompute);
+        }
+        constexpr int EG = KB / 2;
+        constexpr int kGemmT = 16 * EG;
+        static_assert(kGemmT <= kHelpCompute, "helper GEMM threads");
+        if (t < kGemmT) {
+            const int cq = t / EG, eg = t % EG;
+            const int ca = 2 * cq, e = 2 * eg;
+            // four interleaved partial sums per output: FMA chains 8 deep, not 32
+            double acc[4][4];
 #pragma unroll
-                for (int u = 0; u < NE; ++u) {
-                    const int e = g + 8 * u;
-                    if (e < k) {
-                        s0[u] = fma(l0, Pt[m * k + e], s0[u]);
-                        s1[u] = fma(l1, Pt[(m + 1) * k + e], s1[u]);
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int o = 0; o < 4; ++o) acc[q][o] = 0.0;
+            if (e < k) {
+                const double *La = Lt + ca * kLdT, *Lb2 = La + kLdT;
+                if ((k & 1) == 0) {
+#pragma unroll
+                    for (int m = 0; m < kDT; ++m) {
+                        const double2 pv = *reinterpret_cast<const double2 *>(Pt + m * k + e);
+                        const double la = La[m], lb = Lb2[m];
+                        acc[m & 3][0] = fma(la, pv.x, acc[m & 3][0]);
+                        acc[m & 3][1] = fma(la, pv.y, acc[m & 3][1]);
+                        acc[m & 3][2] = fma(lb, pv.x, acc[m & 3][2]);
+                        acc[m & 3][3] = fma(lb, pv.y, acc[m & 3][3]);
+                    }
+                } else {
+                    const bool e1 = e + 1 < k;
+#pragma unroll
+                    for (int m = 0; m < kDT; ++m) {
+                        const double p0 = Pt[m * k + e], p1 = e1 ? Pt[m * k + e + 1] : 0.0;
+                        const double la = La[m], lb = Lb2[m];
+                        acc[m & 3][0] = fma(la, p0, acc[m & 3][0]);
+                        acc[m & 3][1] = fma(la, p1, acc[m & 3][1]);
+                        acc[m & 3][2] = fma(lb, p0, acc[m & 3][2]);
+                        acc[m & 3][3] = fma(lb, p1, acc[m & 3][3]);
                     }
                 }
             }
+            const double s00 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+            const double s01 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+            const double s10 = (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]);
+            const double s11 = (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]);
+            if (t == 0 && h == 60 && seq < 400) CTRACE(0, 3500 + seq);
+            if (t == 0 && h == 60 && seq < 400) CTRACE(3, 3500 + seq);
+            const double sv[2][2] = {{s00, s01}, {s10, s11}};
+            double vout[2][2];
 #pragma unroll
-            for (int u = 0; u < NE; ++u) {
-                const int e = g + 8 * u;
-                double v = 0.0;
-                if (cc < nc && e < k) {
-                    double *rr = r + cc * ld + e;
-                    *rr = v = *rr - (s0[u] + s1[u]);
-                    if (chain_handoff) a.rchain[c0 * k + (int64_t)cc * k + e] = v;
+            for (int i = 0; i < 2; ++i) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int c = ca + i, ee = e + j;
+                    double v = 0.0;
+                    if (c < nc && ee < k) {
+                        double *rr = r + c * ld + ee;
+                        *rr = v = *rr - sv[i][j];
+                        if (chain_handoff) st_handoff(a.rchain + c0 * k + (int64_t)c * k + ee, v);
+                    }
+                    vout[i][j] = v;
                 }
-                vout[u] = v;
             }
-        }
-        if (chain_handoff && t == 0) HTRACE(4, s);
-        if (t == 0 && h == 60 && seq < 1000) CTRACE(1, 3000 + seq);
-        if (chain_handoff) {
-            named_bar(1, kHelpCompute);
-            if (t == 0) HTRACE(5, s);
-            if (t == 0) {
-                __threadfence();
-                st_release(a.rflag + s, a.epoch);
-                HTRACE(2, s);
-            }
-        }
-        if (checkpoint && cc < nc) {  // after the hand-off release: the chain does not wait for these
-            double *ck = a.chk + (chk_count_before(s64, a.CI) + b64 / a.CI) * kD * k + ((s % 2) * kDT + cc) * k;
+            if (chain_handoff && t == 0) HTRACE(2, s);
+            if (t == 0 && h == 60 && seq < 400) CTRACE(2, 3500 + seq);
+            if (checkpoint) {  // the chain does not wait for these
 #pragma unroll
-            for (int u = 0; u < NE; ++u)
-                if (g + 8 * u < k) ck[g + 8 * u] = vout[u];
+                for (int i = 0; i < 2; ++i) {
+                    const int c = ca + i;
+                    double *ck = a.chk + (chk_count_before_pow2(s64, a.CIlog) + (b64 >> a.CIlog)) * kD * k +
+                                 ((s % 2) * kDT + c) * k;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        if (c < nc && e + j < k) ck[e + j] = vout[i][j];
+                }
+            }
         }
+        if (t == 0 && h == 60 && seq < 1000) CTRACE(1, 3000 + seq);
         __syncwarp();
         if (t == 0 && h == 60 && seq < 1000) CTRACE(2, 3000 + seq);
         if (lane == 0) mbar_arrive(empty + slot);
@@ -1095,15 +1204,17 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.P = reinterpret_cast<double *>(wsbase + lay.P);
     a.rcur = reinterpret_cast<double *>(wsbase + lay.rcur);
     a.rchain = reinterpret_cast<double *>(wsbase + lay.rchain);
+    a.pfast = reinterpret_cast<double *>(wsbase + lay.pfast);
     a.MX = reinterpret_cast<double *>(wsbase + lay.MX);
     a.bulk_ok = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0) && n <= 0x7fffffff &&
                 encode_tmap_L(&a.tmapL, L, n, ldl);
     a.chk = reinterpret_cast<double *>(wsbase + lay.chk);
     a.CI = lay.CI;
+    a.CIlog = 0;
+    while ((1 << a.CIlog) < lay.CI) ++a.CIlog;
     unsigned *flags = reinterpret_cast<unsigned *>(wsbase + lay.flags);
     a.prog = reinterpret_cast<unsigned long long *>(flags);
-    a.rflag = flags + 2 * 16 * kProgStride;
-    a.lflag = a.rflag + lay.NT;
+    a.lflag = flags + 2 * 16 * kProgStride;
     a.epoch = epoch;
 
     a.NC = (k + kRPC - 1) / kRPC;
@@ -1125,6 +1236,10 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     const int grid = (int)std::min<int64_t>((int64_t)nsm * per_sm, a.NC + lay.NT);
     if (grid <= a.NC) return GCM_ECUDA;
     void *args[] = {&a};
+    // hand-off slots start empty (all-ones); consumers re-arm what they read
+    st = check_cuda(cudaMemsetAsync(a.rchain, 0xff, lay.pfast - lay.rchain + (size_t)lay.NT * kDT * k * sizeof(double),
+                                    stream));
+    if (st != GCM_OK) return st;
     {
         ProfScope ps("trsv", stream);
         st = check_cuda(cudaLaunchCooperativeKernel((const void *)trsv_kernel<KB>, dim3(grid), dim3(kTrsvThreads),

@@ -26,6 +26,11 @@ NT = (n + 31) // 32
 t = tr[:NT].astype(np.float64)
 step = np.diff(t[:, 0])
 print(f"steps {NT}: chain step cycles median {np.median(step):.0f} mean {step.mean():.0f}")
+pubt = tr[1024:1024 + NT, 0].astype(np.float64)
+R = [t[tb - 1, 5] - pubt[tb - 5] for tb in range(10, NT - 2)]
+print(f"chain-local hand-off round trip (publish P_tb -> sees r for strip tb+5), cycles: median {np.median(R):.0f} p10 {np.percentile(R,10):.0f} p90 {np.percentile(R,90):.0f}")
+P2 = [pubt[tb] - t[tb, 1] for tb in range(10, NT - 2)]
+print(f"  p_done -> publish: median {np.median(P2):.0f}")
 names = ["crit.start", "crit.p_done", "prep.start", "prep.mbar_ok", "prep.partials", "prep.rflag_ok", "prep.done", "svc.issued"]
 for s in range(1, 8):
     d = t[1:-2, s] - t[1:-2, 0]
@@ -42,28 +47,24 @@ if hasattr(lib, "gcm_debug_htrace"):
     print(f"  helper tile start -> rflag published:           median {np.median(hh[:,2]-hh[:,1]):.0f}")
     print(f"  rflag published -> chain prep sees it:          median {np.median(hh[:,3]-hh[:,2]):.0f}")
     print(f"  chain publish P -> chain sees hand-off:         median {np.median(hh[:,3]-hh[:,0]):.0f}")
-    ok2 = ok & (h[:, 4] > 0) & (h[:, 5] > 0) & (h[:, 6] > 0)
-    h2 = h[ok2]
-    print(f"  publish -> feeder sees progress: {np.median(h2[:,6]-h2[:,0]):.0f}; feeder -> data landed (tile start): {np.median(h2[:,1]-h2[:,6]):.0f}")
-    print(f"  tile start -> thread0 GEMM done: {np.median(h2[:,4]-h2[:,1]):.0f}; -> all compute done: {np.median(h2[:,5]-h2[:,1]):.0f}; -> rflag: {np.median(h2[:,2]-h2[:,1]):.0f}")
-    ok3 = ok2 & (h[:, 7] > 0)
-    h3 = h[ok3]
-    print(f"  feeder reaches hand-off tile - publish: median {np.median(h3[:,7]-h3[:,0]):.0f} p10 {np.percentile(h3[:,7]-h3[:,0],10):.0f} p90 {np.percentile(h3[:,7]-h3[:,0],90):.0f}")
-    print(f"  per-chain publish skew unknown; feeder poll time (seen - max(reach, publish)): {np.median(h3[:,6]-np.maximum(h3[:,7],h3[:,0])):.0f}")
-    hc = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8)[2048:2048 + NT].astype(np.float64)
-    okc = np.all(hc > 0, axis=1)
-    print("  per-chain publish time - chain0 (median over strips):", np.median(hc[okc] - hc[okc][:, :1], axis=0))
-    rows = np.nonzero(ok3 & okc)[0]
-    print("  feeder reach - last chain publish: median", np.median(h[rows, 7] - hc[rows].max(axis=1)))
-    hs = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8)[3000:3060].astype(np.float64)
-    pub = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8)[2048:2048+NT, 0].astype(np.float64)  # chain0 publish of tb = s-5 at row s
-    base = hs[0, 3]
-    print("helper 60, per tile seq (tb = seq): times rel. to feeder start (us): feeder[pre-empty, got-empty, got-P] compute[start, gemm, end]  P_tb published")
-    for q in range(0, 60, 3):
-        ptb = pub[q + 5] - base if q + 5 < NT and pub[q + 5] > 0 else float('nan')
-        print(q, np.round((hs[q, [3, 4, 5, 0, 1, 2]] - base) / 1000, 2), round(ptb / 1000, 2))
     hs = tr[3000:3060].astype(np.float64)
     base = hs[0, 3]
     print("helper 60 clock64 (kcycles rel): feeder[reach, got-empty, got-P, P-issued] compute[start, gemm, end]")
     for q in range(0, 60, 3):
         print(q, np.round((hs[q, [3, 4, 5, 6, 0, 1, 2]] - base) / 1000, 2))
+print("helper 60 tiles 44..58 (kcycles rel. to tile 44 start): [full-wait done, pfast loaded (fast tiles), gemm done, end]")
+b0 = tr[3000 + 44, 0]
+for q in range(44, 59):
+    r = tr[3000 + q]
+    print(q, [round((r[i] - b0) / 1000, 2) if r[i] > 0 else None for i in (0, 7, 1, 2)])
+print("helper 60 tiles: [full-wait done, before fast, pfast loaded, fma loop done, all done]")
+for q in range(44, 59):
+    r = tr[3000 + q]; r2 = tr[3500 + q]
+    print(q, [round((x - b0) / 1000, 2) if x > 0 else None for x in (r[0], r2[1], r[7], r2[0], r[1])])
+print("helper 60 tiles: [full-wait done, before fast, pfast loaded, fma loop done, sums done, r updated, all done]")
+for q in range(44, 59):
+    r = tr[3000 + q]; r2 = tr[3500 + q]
+    print(q, [round((x - b0) / 1000, 2) if x > 0 else None for x in (r[0], r2[1], r[7], r2[0], r2[3], r2[2], r[1])])
+w = tr[2048:2048 + NT].astype(np.float64)
+print(f"hand-off not yet there at first poll: {int(w[10:NT-2,0].sum())} of {NT-12} steps; wait cycles median {np.median(w[10:NT-2,2]-w[10:NT-2,1]):.0f} p90 {np.percentile(w[10:NT-2,2]-w[10:NT-2,1],90):.0f}")
+print("first-poll time - crit.start (median):", np.median(w[10:NT-2,1] - t[10-1:NT-2-1,0]))
