@@ -430,11 +430,12 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
             double acc = 0.0;
 #pragma unroll
             for (int q = 0; q < kPrepWarps; ++q) acc += part[(q * kDT + jj) * kRPC + w];
+            if (pt == 0 && c == 0) HTRACE(0, 3500 + tb);
             if (e < k && row < a.n) acc += ld_handoff(a.rchain + (int64_t)tb * kDT * k + (int64_t)jj * k + e);
+            if (pt == 0 && c == 0) HTRACE(6, 3000 + tb);
             accs[jj * kRPC + w] = acc;
         }
         if (pt == 0) TRACE(5, tb - 1);
-        if (pt == 0 && c == 0) HTRACE(3, tb);
         named_bar(2, kPrepThreads);
         if (pt < kDT * kRPC) {  // prepX[j][w] = sum_q X(q, j) acc[q][w]   (X row-major in the stage)
             const int jj = pt % kDT, w = pt / kDT;
@@ -468,9 +469,6 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
                 __threadfence();
 #endif
                 st_release64(a.prog + c * kProgStride, ((unsigned long long)a.epoch << 32) | (unsigned)(tb + 1));
-                if (c == 0 && tb + kLookC + 1 < NT) HTRACE(0, tb + kLookC + 1);
-                if (c == 0) CTRACE(0, 1024 + tb);
-                if (c < 8 && tb + kLookC + 1 < NT) HTRACE(c, 2048 + tb + kLookC + 1);
             }
             __syncwarp();
         }
@@ -493,6 +491,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
             const int w = warp, j = lane;
             if (t == 0) TRACE(0, tb);
             double a0 = prepx[(tb & 1) * kDT * kRPC + j * kRPC + w], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (t == 0 && c == 0) HTRACE(7, 3000 + tb);
             if (tb > 0) {
                 const double *pprev = pwin + ((tb - 1) % kLookC) * kDT * kRPC + w;
 #pragma unroll
@@ -510,6 +509,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
             if (e < k && row < a.n) {
                 a.P[row * k + e] = p;
                 st_handoff(a.pfast + row * k + e, p);  // polled by the helpers of strips tb+kLookC+1..
+                if (t == 0 && c == 0) HTRACE(0, 3000 + tb + kLookC + 1);
             }
             if (t == 0) TRACE(1, tb);
             __syncwarp();
@@ -653,9 +653,7 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         int seq = 0;
         for (It it{0, first_owned_after(0)}; valid(it); advance(it), ++seq) {
             const int slot = seq % kHelpRing, use = seq / kHelpRing;
-            if (lane == 0 && h == 60 && seq < 1000) CTRACE(3, 3000 + seq);
             if (use > 0) mbar_wait(empty + slot, (unsigned)((use - 1) & 1));
-            if (lane == 0 && h == 60 && seq < 1000) CTRACE(4, 3000 + seq);
             double *stg = ring + slot * kSlot;
             const int s = h + it.ii * H;
             const int64_t c0 = (int64_t)s * kDT;
@@ -663,7 +661,6 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             for (int cc = 0; cc < nc; ++cc)  // lane = row: coalesced 256-byte column segments
                 cp_async8(stg + cc * kLdT + lane, a.L + ((int64_t)it.tb * kDT + lane) + (c0 + cc) * a.ldl);
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
-            if (lane == 0 && it.tb + 1 == s - kLookC) HTRACE(7, s);
             if (fast_tile(it.tb, s)) {  // tiles next to the hand-off: the compute warps poll pfast themselves
                 if (lane == 0) mbar_arrive(full + slot);
                 continue;
@@ -688,15 +685,12 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                 known = (int)mm;
             }
             __syncwarp();
-            if (lane == 0 && it.tb + 1 == s - kLookC) HTRACE(6, s);
-            if (lane == 0 && h == 60 && seq < 1000) CTRACE(5, 3000 + seq);
             if (lane == 0) {  // P_tb (32 x k, contiguous) with one bulk copy
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // chains' generic stores -> bulk read
                 const unsigned bytes = (unsigned)(kDT * k) * 8u;
                 mbar_arrive_expect_tx(full + slot, bytes);
                 bulk_g2s(stg + kDT * kLdT, a.P + (int64_t)it.tb * kDT * k, bytes, full + slot);
             }
-            if (lane == 0 && h == 60 && seq < 1000) CTRACE(6, 3000 + seq);
         }
         cp_async_wait_all();
         return;
@@ -707,10 +701,9 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         const int tb = pit.tb;
         const int slot = seq % kHelpRing;
         mbar_wait(full + slot, (unsigned)((seq / kHelpRing) & 1));
-        if (t == 0 && h == 60 && seq < 1000) CTRACE(0, 3000 + seq);
+        if (t == 0 && pit.tb + 1 == h + pit.ii * H - kLookC) HTRACE(1, 3000 + h + pit.ii * H);
         const int ii = pit.ii;
         const int s = h + ii * H;
-        if (t == 0 && tb + 1 == s - kLookC) HTRACE(1, s);
         const double *Lt = ring + slot * kSlot;
         const double *Pt = Lt + kDT * kLdT;
         const int64_t c0 = (int64_t)s * kDT;
@@ -725,7 +718,6 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         const bool chain_handoff = (tb + 1 == s - kLookC);
         const int b64 = (tb + 1) / 2, s64 = s / 2;
         const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 & (a.CI - 1)) == 0;
-        if (t == 0 && h == 60 && seq < 400) CTRACE(1, 3500 + seq);
         if (fast_tile(tb, s)) {  // P_tb straight from the chains' self-validating copy
             double *Pw = const_cast<double *>(Pt);
             const double *src = a.pfast + (int64_t)tb * kDT * k;
@@ -744,8 +736,9 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                     Pw[o] = __longlong_as_double((long long)u[q]);
                 }
             }
-            if (t == 0 && h == 60 && seq < 1000) CTRACE(7, 3000 + seq);
+            if (t == 0 && chain_handoff) HTRACE(2, 3000 + s);
             named_bar(1, kHelpCompute);
+            if (t == 0 && chain_handoff) HTRACE(3, 3000 + s);
         }
         constexpr int EG = KB / 2;
         constexpr int kGemmT = 16 * EG;
@@ -788,9 +781,8 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             const double s01 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
             const double s10 = (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]);
             const double s11 = (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]);
-            if (t == 0 && h == 60 && seq < 400) CTRACE(0, 3500 + seq);
-            if (t == 0 && h == 60 && seq < 400) CTRACE(3, 3500 + seq);
             const double sv[2][2] = {{s00, s01}, {s10, s11}};
+            if (t == 0 && chain_handoff) HTRACE(4, 3000 + s);
             double vout[2][2];
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
@@ -802,12 +794,11 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                         double *rr = r + c * ld + ee;
                         *rr = v = *rr - sv[i][j];
                         if (chain_handoff) st_handoff(a.rchain + c0 * k + (int64_t)c * k + ee, v);
+                        if (chain_handoff && t == 0 && i == 0 && j == 0) HTRACE(5, 3000 + s);
                     }
                     vout[i][j] = v;
                 }
             }
-            if (chain_handoff && t == 0) HTRACE(2, s);
-            if (t == 0 && h == 60 && seq < 400) CTRACE(2, 3500 + seq);
             if (checkpoint) {  // the chain does not wait for these
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
@@ -820,9 +811,7 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                 }
             }
         }
-        if (t == 0 && h == 60 && seq < 1000) CTRACE(1, 3000 + seq);
         __syncwarp();
-        if (t == 0 && h == 60 && seq < 1000) CTRACE(2, 3000 + seq);
         if (lane == 0) mbar_arrive(empty + slot);
     }
 }

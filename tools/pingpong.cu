@@ -50,6 +50,30 @@ __global__ void pingpong(unsigned long long *a, unsigned long long *b, int iters
     if (ping) out[0] = t1 - t0;
 }
 
+
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// one-way latency via globaltimer: ping records send time, pong records receive time
+__global__ void oneway(unsigned long long *a, long long *ts, int iters) {
+    if (threadIdx.x != 0) return;
+    for (int i = 1; i <= iters; ++i) {
+        if (blockIdx.x == 0) {
+            // wait for ack of previous
+            while (ld_relaxed(a + 64) != (unsigned long long)(i - 1)) {}
+            for (int d = 0; d < 2000; ++d) __nanosleep(1);  // random-ish gap
+            ts[2 * i] = gtimer();
+            st_relaxed(a, i);
+        } else {
+            while (ld_relaxed(a) != (unsigned long long)i) {}
+            ts[2 * i + 1] = gtimer();
+            st_relaxed(a + 64, i);
+        }
+    }
+}
+
 int main() {
     unsigned long long *a, *b;
     long long *out;
@@ -68,6 +92,14 @@ int main() {
             printf("%-16s round trip %.0f cycles (one-way %.0f)\n", names[mode], (double)h / iters, (double)h / iters / 2);
         }
     }
-    // contention: round trip while 140 other CTAs hammer loads on one line
+    long long *ts;
+    cudaMalloc(&ts, 8 * 2 * 1100);
+    cudaMemset(a, 0, 4096);
+    oneway<<<2, 32>>>(a, ts, 1000);
+    long long hts[2 * 1001];
+    cudaMemcpy(hts, ts, sizeof(hts), cudaMemcpyDeviceToHost);
+    double s = 0, mn = 1e18, mx = -1e18;
+    for (int i = 2; i <= 1000; ++i) { double d = (double)(hts[2 * i + 1] - hts[2 * i]); s += d; mn = d < mn ? d : mn; mx = d > mx ? d : mx; }
+    printf("globaltimer one-way: mean %.0f ns min %.0f max %.0f\n", s / 999, mn, mx);
     return 0;
 }

@@ -1,4 +1,11 @@
-"""Per-step phase timing of the blocked TRSV chain CTA (needs a -DGCM_TRACE build via GCM_LIB_PATH)."""
+"""Hand-off timeline of the blocked TRSV (needs a -DGCM_TRACE build, loaded via GCM_LIB_PATH).
+
+For every strip s (globaltimer ns, consistent across SMs to ~30 ns):
+  0 chain 0 stores P_{s-kLookC-1}      4 helper: contraction done
+  1 helper: hand-off tile's slot full  5 helper: hand-off values stored
+  2 helper: thread 0 has its P values  6 chain 0 has the hand-off value (prep of block s)
+  3 helper: all P values in smem       7 chain 0 starts the critical step of block s
+usage: trace_chain.py n k"""
 import ctypes
 import os
 import sys
@@ -19,52 +26,22 @@ for _ in range(3):
     gcm.modify(L, V.clone(), 1, algo="blocked")
 torch.cuda.synchronize()
 lib = _native.lib()
-buf = (ctypes.c_longlong * (4096 * 8))()
-lib.gcm_debug_trace(buf, 4096 * 8)
-tr = np.frombuffer(buf, dtype=np.int64).reshape(4096, 8)
+hb = (ctypes.c_longlong * (4096 * 8))()
+lib.gcm_debug_htrace(hb, 4096 * 8)
+hall = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8).astype(np.float64)
+h = hall[3000:]
+reach = hall[3500:3500 + 600, 0]
 NT = (n + 31) // 32
-t = tr[:NT].astype(np.float64)
-step = np.diff(t[:, 0])
-print(f"steps {NT}: chain step cycles median {np.median(step):.0f} mean {step.mean():.0f}")
-pubt = tr[1024:1024 + NT, 0].astype(np.float64)
-R = [t[tb - 1, 5] - pubt[tb - 5] for tb in range(10, NT - 2)]
-print(f"chain-local hand-off round trip (publish P_tb -> sees r for strip tb+5), cycles: median {np.median(R):.0f} p10 {np.percentile(R,10):.0f} p90 {np.percentile(R,90):.0f}")
-P2 = [pubt[tb] - t[tb, 1] for tb in range(10, NT - 2)]
-print(f"  p_done -> publish: median {np.median(P2):.0f}")
-names = ["crit.start", "crit.p_done", "prep.start", "prep.mbar_ok", "prep.partials", "prep.rflag_ok", "prep.done", "svc.issued"]
-for s in range(1, 8):
-    d = t[1:-2, s] - t[1:-2, 0]
-    print(f"  {names[s]:22s} - crit.start: median {np.median(d):8.0f}  p10 {np.percentile(d,10):8.0f} p90 {np.percentile(d,90):8.0f}")
-
-if hasattr(lib, "gcm_debug_htrace"):
-    hb = (ctypes.c_longlong * (4096 * 8))()
-    lib.gcm_debug_htrace(hb, 4096 * 8)
-    h = np.frombuffer(hb, dtype=np.int64).reshape(4096, 8)[:NT].astype(np.float64)
-    ok = (h[:, 0] > 0) & (h[:, 1] > 0) & (h[:, 2] > 0) & (h[:, 3] > 0)
-    hh = h[ok]
-    print(f"hand-off timeline (ns, globaltimer) over {ok.sum()} strips:")
-    print(f"  chain publish P -> helper starts hand-off tile: median {np.median(hh[:,1]-hh[:,0]):.0f}")
-    print(f"  helper tile start -> rflag published:           median {np.median(hh[:,2]-hh[:,1]):.0f}")
-    print(f"  rflag published -> chain prep sees it:          median {np.median(hh[:,3]-hh[:,2]):.0f}")
-    print(f"  chain publish P -> chain sees hand-off:         median {np.median(hh[:,3]-hh[:,0]):.0f}")
-    hs = tr[3000:3060].astype(np.float64)
-    base = hs[0, 3]
-    print("helper 60 clock64 (kcycles rel): feeder[reach, got-empty, got-P, P-issued] compute[start, gemm, end]")
-    for q in range(0, 60, 3):
-        print(q, np.round((hs[q, [3, 4, 5, 6, 0, 1, 2]] - base) / 1000, 2))
-print("helper 60 tiles 44..58 (kcycles rel. to tile 44 start): [full-wait done, pfast loaded (fast tiles), gemm done, end]")
-b0 = tr[3000 + 44, 0]
-for q in range(44, 59):
-    r = tr[3000 + q]
-    print(q, [round((r[i] - b0) / 1000, 2) if r[i] > 0 else None for i in (0, 7, 1, 2)])
-print("helper 60 tiles: [full-wait done, before fast, pfast loaded, fma loop done, all done]")
-for q in range(44, 59):
-    r = tr[3000 + q]; r2 = tr[3500 + q]
-    print(q, [round((x - b0) / 1000, 2) if x > 0 else None for x in (r[0], r2[1], r[7], r2[0], r[1])])
-print("helper 60 tiles: [full-wait done, before fast, pfast loaded, fma loop done, sums done, r updated, all done]")
-for q in range(44, 59):
-    r = tr[3000 + q]; r2 = tr[3500 + q]
-    print(q, [round((x - b0) / 1000, 2) if x > 0 else None for x in (r[0], r2[1], r[7], r2[0], r2[3], r2[2], r[1])])
-w = tr[2048:2048 + NT].astype(np.float64)
-print(f"hand-off not yet there at first poll: {int(w[10:NT-2,0].sum())} of {NT-12} steps; wait cycles median {np.median(w[10:NT-2,2]-w[10:NT-2,1]):.0f} p90 {np.percentile(w[10:NT-2,2]-w[10:NT-2,1],90):.0f}")
-print("first-poll time - crit.start (median):", np.median(w[10:NT-2,1] - t[10-1:NT-2-1,0]))
+rows = [s for s in range(12, NT - 2) if np.all(h[s, :] > 0)]
+d = h[rows] - h[rows, :1]
+names = ["P stored", "helper slot full", "helper t0 has P", "helper all P", "helper GEMM done", "hand-off stored",
+         "chain sees hand-off", "chain crit start"]
+print(f"{len(rows)} strips; ns after chain 0 stored P_(s-5) (median / p10 / p90):")
+for i in range(1, 8):
+    print(f"  {names[i]:22s} {np.median(d[:, i]):8.0f} {np.percentile(d[:, i], 10):8.0f} {np.percentile(d[:, i], 90):8.0f}")
+step = np.diff(h[12:NT - 2, 7])
+print(f"chain step (crit start to crit start): median {np.median(step):.0f} ns")
+print(f"  mean {step.mean():.0f} p90 {np.percentile(step, 90):.0f} max {step.max():.0f}; total chain span {h[NT-3,7]-h[12,7]:.0f} ns")
+wait = np.array([h[s, 6] - reach[s] for s in rows])
+print(f"chain waits for the hand-off (seen - reached poll): median {np.median(wait):.0f} p90 {np.percentile(wait,90):.0f} ns")
+print(f"hand-off stored - chain reached poll: median {np.median([h[s,5]-reach[s] for s in rows]):.0f} ns (negative = stored before needed)")
