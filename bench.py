@@ -66,48 +66,69 @@ def algorithmic(n, k, batch=1):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every 1 ms through NVML (the
+    library nvidia-smi reads) on a thread that runs DURING the timed region; the
+    region is only entered once the first sample has arrived.  Falls back to
+    `nvidia-smi -lms 200` when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
-    def __init__(self, index):
-        self.index = index
+    def __init__(self, device_index):
+        self.device_index = device_index
         self.rows = []
-        self.proc = None
+        self.stop_evt = threading.Event()
+        self.thread = None
+        self.handle = None
+        self.nvml = None
+        self.smax = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            handle = None
+            try:
+                import torch
+                pr = torch.cuda.get_device_properties(self.device_index)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                handle = pynvml.nvmlDeviceGetHandleByIndex(self.device_index)
+            self.nvml, self.handle = pynvml, handle
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(handle, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 2.0:
+                time.sleep(0.001)
         except Exception:
-            self.proc = None
+            self.nvml = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+    def _run(self):
+        nv, h = self.nvml, self.handle
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_evt.is_set():
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), int(get_reasons(h))))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        time.sleep(0.05)
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(self.rows)}
+    def mark(self):
+        """Index of the first sample taken after this call (start of the timed region)."""
+        return len(self.rows)
+
+    def stop(self, first=0):
+        if self.nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_evt.set()
+        self.thread.join(timeout=1)
+        rows = self.rows[first:] or self.rows[-1:]
+        sm = [r[0] for r in rows]
+        reasons = sorted({name for _, bits in rows for bit, name in self.REASONS.items() if bits & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax, "reasons": reasons,
+                "samples": len(rows), "source": "nvml, 1 ms period, timed region only"}
 
 
 def dist_setup(ngpus):
@@ -180,11 +201,12 @@ def run_ours(args, world, rank, local):
     gcm.profile_read()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     gcm.profile_enable(True)
     barrier(world)
     torch.cuda.synchronize()
+    first_sample = clocks.mark()
     t0 = time.perf_counter()
     for i in range(args.steps):
         V.copy_(V0)
@@ -197,7 +219,7 @@ def run_ours(args, world, rank, local):
     wall = time.perf_counter() - t0
     gcm.profile_enable(False)
     prof = gcm.profile_read()
-    clk = clocks.stop()
+    clk = clocks.stop(first_sample)
 
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = max_over_ranks(sum(step_ms), world)
@@ -220,7 +242,7 @@ def run_ours(args, world, rank, local):
         peak, unit = FP64_PEAK_TFLOPS_DERIVED, "TFLOP/s"
     roofline = {"kernel": dname, "bound": kb["bound"], "achieved": round(achieved, 3), "peak": peak,
                 "peak_source": hbm_src if kb["bound"] == "hbm" else "derived (148 SM x 64 FMA/clk x 2 x 1.965 GHz)",
-                "unit": unit, "frac": round(achieved / peak, 4), "traffic": kb.get("traffic"),
+                "unit": unit, "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, args.config),
                 "algorithmic": kb["what"], "share_of_step": round(dms / max(sum(m for _, m in prof.values()), 1e-9), 3)}
     # whole-path roofline: T_roof = max(flops/F64, bytes/HBM)
     t_roof = max(flops / (FP64_PEAK_TFLOPS_DERIVED * 1e12), bytes_ / (hbm * 1e9))
@@ -248,6 +270,23 @@ def run_ours(args, world, rank, local):
     if rank == 0 and not args.no_cpu:
         out["cpu_baseline"] = run_cpu_baseline(n, k)
     return out
+
+
+def ncu_traffic(kernel, config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the newest
+    committed `ncu --set full` summary (profiles/r*_ncu_summary.json, captured on the
+    default n5000_k16 workload), else None."""
+    if config != "n5000_k16":
+        return None
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_ncu_summary.json")))
+    if not files:
+        return None
+    try:
+        d = json.load(open(files[-1]))["kernels"].get(kernel)
+        return None if d is None else d["traffic_bytes"]
+    except Exception:
+        return None
 
 
 def kernel_units(name, n, k, batch):
