@@ -32,6 +32,7 @@
 #include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "rot.cuh"
@@ -86,6 +87,9 @@ __device__ __forceinline__ int64_t chk_count_before_pow2(int s, int CIlog) {
     return ((q * (q + 1) / 2) << CIlog) + (q + 1) * r;
 }
 
+// rank padding of a pass (the kernels' template KB)
+__host__ __device__ constexpr int kb_of(int k) { return k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32; }
+
 Layout make_layout(int64_t n, int k, size_t chk_budget) {
     Layout l{};
     l.n = n;
@@ -112,8 +116,8 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
     l.chk = take((size_t)l.nchk * kD * k);
     l.Q = take((size_t)l.NB * k * k);
     l.G = take((size_t)l.NB * k * k);
-    l.U = take((size_t)l.NB * k * k);
-    l.panels = take((size_t)l.NB * panel_doubles(k));
+    l.U = take((size_t)l.NB * kb_of(k) * kb_of(k));       // U_b^{-1}, KB x KB, zero padded
+    l.panels = take((size_t)l.NB * panel_doubles(kb_of(k)));  // coefficient panels, stride KB
     l.flags = take((1ull * l.NT * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
                    8);  // prog[16 * kProgStride], lflag
     l.total = o;
@@ -139,7 +143,12 @@ __device__ long long g_trace[4096 * 8];
 #define CTRACE(slot, s) ((void)0)
 #endif
 
-constexpr size_t kChkBudget = 2ull << 30;  // bytes of Apply checkpoints before CI doubles
+// Bytes of Apply checkpoints before the checkpoint interval CI doubles (2 GiB;
+// GCM_CHK_BUDGET overrides it per call -- the tests use it to exercise CI > 1).
+size_t chk_budget() {
+    const char *e = std::getenv("GCM_CHK_BUDGET");
+    return e ? (size_t)std::strtoull(e, nullptr, 10) : (size_t)(2ull << 30);
+}
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     unsigned v;
@@ -911,9 +920,25 @@ __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict_
         }
     }
     __syncthreads();
-    for (int o = t; o < k * k; o += kDiagThreads) {
-        const int e1 = o / k, e2 = o % k;
-        Uout[(int64_t)b * k * k + o] = e2 <= e1 ? M[e1][e2] : 0.0;
+    // U_b^{-1} (lower, KB x KB zero padded) for the off-diagonal tiles' V states:
+    // lane c solves U x = e_c by forward substitution
+    if (t < KB) {
+        const int c = t;
+        double x[KB];
+#pragma unroll
+        for (int i = 0; i < KB; ++i) {
+            if (i >= c && i < k) {
+                double acc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+                for (int j = 0; j < i; ++j)
+                    if (j >= c) acc = fma(-M[i][j], x[j], acc);
+                x[i] = acc / M[i][i];
+            } else {
+                x[i] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < KB; ++i) Uout[(int64_t)b * KB * KB + i * KB + c] = x[i];
     }
     // V-state of column r0+t: y = U^{-1} (L_bb^T P_b)[t]
     double v[KB];
@@ -944,15 +969,9 @@ __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict_
     __syncthreads();  // wave_sweep reads Vs from other threads before its own first barrier
     wave_sweep<KB, kDiagNQ, kD + 1>(Ls, Vs, Db, k, sigma, r0, pan, V + r0, n, key, ebase, vx, dinv, vt, imx, 0,
                                     kDiagNQ * kD / 32);
-    // panel out, from stride KB (smem) to the global layout (stride k)
-    double *panel = panels + (int64_t)b * panel_doubles(k);
-    for (int i = t; i < kD * k; i += kDiagThreads) {
-        const int j = i / k, e = i % k;
-        panel[2 * i] = pan[2 * (j * KB + e)];
-        panel[2 * i + 1] = pan[2 * (j * KB + e) + 1];
-    }
-    for (int i = t; i < kD; i += kDiagThreads) panel[2 * kD * k + i] = pan[2 * kD * KB + i];
-    for (int i = t; i < k; i += kDiagThreads) panel[2 * kD * k + kD + i] = pan[2 * kD * KB + kD + i];
+    // panel out in the blocked path's stride-KB layout (padding rotations are identities)
+    double *panel = panels + (int64_t)b * panel_doubles(KB);
+    for (int i = t; i < (int)panel_doubles(KB); i += kDiagThreads) panel[i] = pan[i];
     for (int idx = t; idx < kD * kD; idx += kDiagThreads) {
         const int m = idx / kD, j = idx % kD;
         if (m < Db && j <= m) L[(r0 + j) + (r0 + m) * ldl] = Ls[m][j];
@@ -977,8 +996,8 @@ __global__ void __launch_bounds__(kApplyT) bapply_kernel(double *__restrict__ L,
     if (b0 >= s) return;
     const int b1 = min(b0 + CI, s);
     extern __shared__ double2 smem_bapply[];
-    double2 *cs = smem_bapply;                              // [kD * k]
-    double *rho = reinterpret_cast<double *>(cs + kD * k);  // [kD]
+    double2 *cs = smem_bapply;                               // [kD * KB]
+    double *rho = reinterpret_cast<double *>(cs + kD * KB);  // [kD]
     double *nu = rho + kD;                                  // [KB]
     double *Us = nu + KB;                                   // [KB * KB]
     double *buf = Us + KB * KB;                             // [2][kD cols][kLdC]
@@ -998,25 +1017,24 @@ __global__ void __launch_bounds__(kApplyT) bapply_kernel(double *__restrict__ L,
     };
     for (int b = b0; b < b1; ++b) {
         issue(b, 0);
-        const double *panel = panels + (int64_t)b * panel_doubles(k);
-        for (int i = t; i < kD * k; i += kApplyT) cs[i] = make_double2(panel[2 * i], panel[2 * i + 1]);
-        for (int i = t; i < kD; i += kApplyT) rho[i] = panel[2ll * kD * k + i];
-        for (int i = t; i < k; i += kApplyT) nu[i] = panel[2ll * kD * k + kD + i];
+        const double *panel = panels + (int64_t)b * panel_doubles(KB);
+        for (int i = t; i < kD * KB; i += kApplyT) cs[i] = make_double2(panel[2 * i], panel[2 * i + 1]);
+        for (int i = t; i < kD; i += kApplyT) rho[i] = panel[2ll * kD * KB + i];
+        for (int i = t; i < KB; i += kApplyT) nu[i] = panel[2ll * kD * KB + kD + i];
         if (b == b0)
-            for (int i = t; i < k * k; i += kApplyT) Us[i] = U[(int64_t)b * k * k + i];
+            for (int i = t; i < KB * KB; i += kApplyT) Us[i] = U[(int64_t)b * KB * KB + i];
         __syncthreads();
-        if (b == b0 && t < nc) {  // V-state = U_b^{-1} r  (forward substitution, k x k lower)
+        if (b == b0 && t < nc) {  // V-state = U_b^{-1} r
             const double *r = chk + (chk_count_before(s, CI) + g) * kD * k + (int64_t)t * k;
+            double rr[KB];
+#pragma unroll
+            for (int e = 0; e < KB; ++e) rr[e] = e < k ? r[e] : 0.0;
 #pragma unroll
             for (int e = 0; e < KB; ++e) {
-                if (e < k) {
-                    double acc = r[e];
+                double acc = 0.0;
 #pragma unroll
-                    for (int ep = 0; ep < e; ++ep) acc = fma(-Us[e * k + ep], v[ep], acc);
-                    v[e] = acc / Us[e * k + e];
-                } else {
-                    v[e] = 0.0;
-                }
+                for (int ep = 0; ep <= e; ++ep) acc = fma(Us[e * KB + ep], rr[ep], acc);
+                v[e] = acc;
             }
         }
         for (int ch = 0; ch < NCH; ++ch) {
@@ -1032,7 +1050,7 @@ __global__ void __launch_bounds__(kApplyT) bapply_kernel(double *__restrict__ L,
                 double *col = bb + t * kLdC;
 #pragma unroll 4
                 for (int j = 0; j < kRC; ++j)
-                    col[j] = apply_row<KB>(col[j], v, cs + (ch * kRC + j) * k, rho[ch * kRC + j], k);
+                    col[j] = apply_row<KB>(col[j], v, cs + (ch * kRC + j) * KB, rho[ch * kRC + j], KB);
             }
             __syncthreads();
             for (int idx = t; idx < kD * kRC; idx += kApplyT) {
@@ -1042,8 +1060,7 @@ __global__ void __launch_bounds__(kApplyT) bapply_kernel(double *__restrict__ L,
         }
         if (t < nc) {
 #pragma unroll
-            for (int e = 0; e < KB; ++e)
-                if (e < k) v[e] *= nu[e];
+            for (int e = 0; e < KB; ++e) v[e] *= nu[e];
         }
         __syncthreads();
     }
@@ -1089,30 +1106,24 @@ __global__ void __launch_bounds__(kTileThreads, KB >= 32 ? 1 : 2) btile_kernel(d
         cp_async_commit();
     };
     issue(0);
-    const double *panel = panels + (int64_t)b * panel_doubles(k);
-    // coefficients padded to stride KB (identity rotations for e >= k: gamma = delta = 0)
-    for (int i = t; i < kD * KB; i += kTileThreads) {
-        const int j = i / KB, e = i % KB;
-        cs[i] = e < k ? make_double2(panel[2 * (j * k + e)], panel[2 * (j * k + e) + 1]) : make_double2(0.0, 0.0);
-    }
-    for (int i = t; i < kD; i += kTileThreads) rho[i] = panel[2ll * kD * k + i];
-    for (int i = t; i < k; i += kTileThreads) nu[i] = panel[2ll * kD * k + kD + i];
-    for (int i = t; i < k * k; i += kTileThreads) Us[i] = U[(int64_t)b * k * k + i];
+    const double *panel = panels + (int64_t)b * panel_doubles(KB);  // stride KB, padding = identities
+    for (int i = t; i < kD * KB; i += kTileThreads) cs[i] = make_double2(panel[2 * i], panel[2 * i + 1]);
+    for (int i = t; i < kD; i += kTileThreads) rho[i] = panel[2ll * kD * KB + i];
+    for (int i = t; i < KB * KB; i += kTileThreads) Us[i] = U[(int64_t)b * KB * KB + i];
     __syncthreads();
     const bool act = q < nstr && c0 + c < n;
     double v[KB];
-    if (act) {  // V-state = U_b^{-1} r  (forward substitution, k x k lower)
+    if (act) {  // V-state = U_b^{-1} r
         const double *r = chk + (chk_count_before(s, 1) + b) * kD * k + (int64_t)c * k;
+        double rr[KB];
+#pragma unroll
+        for (int e = 0; e < KB; ++e) rr[e] = e < k ? r[e] : 0.0;
 #pragma unroll
         for (int e = 0; e < KB; ++e) {
-            if (e < k) {
-                double acc = r[e];
+            double acc = 0.0;
 #pragma unroll
-                for (int ep = 0; ep < e; ++ep) acc = fma(-Us[e * k + ep], v[ep], acc);
-                v[e] = acc / Us[e * k + e];
-            } else {
-                v[e] = 0.0;
-            }
+            for (int ep = 0; ep <= e; ++ep) acc = fma(Us[e * KB + ep], rr[ep], acc);
+            v[e] = acc;
         }
     }
     for (int ch = 0; ch < NCH; ++ch) {
@@ -1157,12 +1168,186 @@ __global__ void __launch_bounds__(kTileThreads, KB >= 32 ? 1 : 2) btile_kernel(d
     }
 }
 
+// CI == 1 Apply through TMA (L 16-byte aligned, ldl even): one CTA of 128 threads per
+// (row block b, 2C column strips = 128*C columns); thread t owns columns t + 128q
+// (q < C, C = 4 for KB <= 16, else 2), so each broadcast (gamma, delta) load feeds 2C
+// FMAs and the shared-memory pipe stops being the limit.  The 64-row tile streams
+// through a 3-stage ring of 8-row chunks (one 8 x 256 TMA box per 256 columns, 64-byte
+// rows, 64B swizzle: a lane's row pair is one conflict-free 16-byte load), is rotated
+// in place and leaves by TMA stores; the panel and U_b^{-1} arrive by two bulk copies.
+// DRAM traffic is the tile read + write once; the V states start at U_b^{-1} r from
+// the checkpoints.
+#ifndef GCM_T2_STAGES
+#define GCM_T2_STAGES 4
+#endif
+constexpr int kT2Threads = 128;
+constexpr int kT2Box = 256;  // columns per TMA box
+constexpr int kT2Rows = 8;
+constexpr int kT2Stages = GCM_T2_STAGES;
+constexpr int kT2Chunks = kD / kT2Rows;
+constexpr unsigned kT2BoxBytes = kT2Rows * kT2Box * 8;
+
+#ifndef GCM_T2_C
+#define GCM_T2_C 2
+#endif
+#ifndef GCM_T2_UNROLL
+#define GCM_T2_UNROLL 4
+#endif
+constexpr int kT2Unroll = GCM_T2_UNROLL;
+__host__ __device__ constexpr int t2_cols_per_thread(int KB) { return KB <= 16 ? GCM_T2_C : 2; }
+__host__ __device__ constexpr int t2_strips(int KB) { return kT2Threads * t2_cols_per_thread(KB) / kD; }
+__host__ __device__ constexpr size_t t2_smem_bytes(int KB) {
+    return 1024 + (size_t)kT2Stages * kT2BoxBytes * (t2_cols_per_thread(KB) / 2) +
+           ((size_t)panel_doubles(KB) + KB * KB) * 8 + 8 * (2 * kT2Stages + 1);
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int c0, int c1,
+                                            unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, int c0, int c1, const void *src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(c0), "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kT2Threads, 2) btma_kernel(const __grid_constant__ CUtensorMap tm, int64_t n, int k,
+                                                              const double *__restrict__ chk,
+                                                              const double *__restrict__ Ui,
+                                                              const double *__restrict__ panels, int NB) {
+    constexpr int C = t2_cols_per_thread(KB);
+    constexpr int NBOX = C / 2;  // TMA boxes per chunk
+    constexpr unsigned kStage = kT2BoxBytes * NBOX;
+    const int b = blockIdx.x;
+    const int s0 = b + 1 + t2_strips(KB) * blockIdx.y;
+    if (s0 >= NB) return;
+    extern __shared__ __align__(16) unsigned char smem_t2[];
+    const unsigned sbase = smem_u32(smem_t2);
+    unsigned char *st = smem_t2 + (((sbase + 1023u) & ~1023u) - sbase);  // swizzled boxes: 1 KB aligned
+    double2 *cs = reinterpret_cast<double2 *>(st + kT2Stages * kStage);   // [kD][KB] (gamma, delta)
+    const double *rho = reinterpret_cast<const double *>(cs + kD * KB);    // [kD]
+    double *Us = reinterpret_cast<double *>(st + kT2Stages * kStage) + panel_doubles(KB);  // [KB][KB]
+    unsigned long long *bars = reinterpret_cast<unsigned long long *>(Us + KB * KB);     // full[stages], panel
+    const int t = threadIdx.x;
+    const int rb = b * kD, col0 = s0 * kD;
+    auto load_chunk = [&](int ch) {  // thread 0
+        const int sg = ch % kT2Stages;
+        mbar_arrive_expect_tx(bars + sg, kStage);
+#pragma unroll
+        for (int x = 0; x < NBOX; ++x)
+            tma_load_2d(st + sg * kStage + x * kT2BoxBytes, &tm, rb + ch * kT2Rows, col0 + x * kT2Box, bars + sg);
+    };
+    if (t == 0) {
+        for (int i = 0; i <= kT2Stages; ++i) mbar_init(bars + i, 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0) {
+        const unsigned pbytes = (unsigned)panel_doubles(KB) * 8u, ubytes = (unsigned)(KB * KB) * 8u;
+        mbar_arrive_expect_tx(bars + kT2Stages, pbytes + ubytes);
+        bulk_g2s(cs, panels + (int64_t)b * panel_doubles(KB), pbytes, bars + kT2Stages);
+        bulk_g2s(Us, Ui + (int64_t)b * KB * KB, ubytes, bars + kT2Stages);
+        for (int ch = 0; ch < kT2Stages; ++ch) load_chunk(ch);
+    }
+    // V states = U_b^{-1} r (checkpointed residuals), the C columns together so each
+    // U entry is loaded once and consumed at once
+    double v[C][KB];
+    const double *pr[C];
+    bool act[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        const int c = t + kT2Threads * q;
+        const int s = s0 + c / kD;
+        act[q] = s < NB && (int64_t)col0 + c < n;
+        pr[q] = chk + (chk_count_before(act[q] ? s : s0, 1) + b) * kD * k + (int64_t)(c % kD) * k;
+#pragma unroll
+        for (int e = 0; e < KB; ++e) v[q][e] = 0.0;
+    }
+    mbar_wait(bars + kT2Stages, 0u);
+#pragma unroll
+    for (int ep = 0; ep < KB; ++ep) {
+        double rv[C];
+#pragma unroll
+        for (int q = 0; q < C; ++q) rv[q] = (act[q] && ep < k) ? pr[q][ep] : 0.0;
+#pragma unroll
+        for (int e = ep; e < KB; ++e) {
+            const double u = Us[e * KB + ep];
+#pragma unroll
+            for (int q = 0; q < C; ++q) v[q][e] = fma(u, rv[q], v[q][e]);
+        }
+    }
+    for (int ch = 0; ch < kT2Chunks; ++ch) {
+        const int sg = ch % kT2Stages;
+        mbar_wait(bars + sg, (unsigned)((ch / kT2Stages) & 1));
+        unsigned char *buf = st + sg * kStage;
+#pragma unroll kT2Unroll
+        for (int jp = 0; jp < kT2Rows / 2; ++jp) {
+            double2 *p[C];
+            double2 x[C];
+#pragma unroll
+            for (int q = 0; q < C; ++q) {
+                const int c = t + kT2Threads * q, cc = c % kT2Box;
+                p[q] = reinterpret_cast<double2 *>(buf + (c / kT2Box) * kT2BoxBytes + cc * 64 +
+                                                   ((jp ^ ((cc >> 1) & 3)) << 4));
+                x[q] = *p[q];
+            }
+            const int j = ch * kT2Rows + 2 * jp;
+            const double2 *g0 = cs + j * KB, *g1 = g0 + KB;
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {  // row j
+                const double2 gd = g0[e];
+#pragma unroll
+                for (int q = 0; q < C; ++q) {
+                    x[q].x = fma(gd.x, v[q][e], x[q].x);
+                    v[q][e] = fma(-gd.y, x[q].x, v[q][e]);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < KB; ++e) {  // row j + 1
+                const double2 gd = g1[e];
+#pragma unroll
+                for (int q = 0; q < C; ++q) {
+                    x[q].y = fma(gd.x, v[q][e], x[q].y);
+                    v[q][e] = fma(-gd.y, x[q].y, v[q][e]);
+                }
+            }
+            const double ra = rho[j], rbb = rho[j + 1];
+#pragma unroll
+            for (int q = 0; q < C; ++q) {
+                x[q].x *= ra;
+                x[q].y *= rbb;
+                *p[q] = x[q];
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> TMA store
+        __syncthreads();
+        if (t == 0) {
+#pragma unroll
+            for (int x = 0; x < NBOX; ++x) tma_store_2d(&tm, rb + ch * kT2Rows, col0 + x * kT2Box, buf + x * kT2BoxBytes);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            const int nx = ch + kT2Stages - 1;  // refill the stage of chunk ch-1 once its store has read it
+            if (ch >= 1 && nx < kT2Chunks) {
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                load_chunk(nx);
+            }
+        }
+    }
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-bool encode_tmap_L(CUtensorMap *m, const double *L, int64_t n, int64_t ldl) {
+bool encode_tmap(CUtensorMap *m, const double *L, int64_t n, int64_t ldl, unsigned box_rows, unsigned box_cols,
+                 CUtensorMapSwizzle swz) {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -1174,11 +1359,14 @@ bool encode_tmap_L(CUtensorMap *m, const double *L, int64_t n, int64_t ldl) {
     }
     const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
     const cuuint64_t strides[1] = {(cuuint64_t)ldl * sizeof(double)};
-    const cuuint32_t box[2] = {(cuuint32_t)kSeg, (cuuint32_t)kDT};
+    const cuuint32_t box[2] = {box_rows, box_cols};
     const cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(L), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool encode_tmap_L(CUtensorMap *m, const double *L, int64_t n, int64_t ldl) {
+    return encode_tmap(m, L, n, ldl, (unsigned)kSeg, (unsigned)kDT, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 template <int KB>
@@ -1259,10 +1447,22 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
                                                                       ebase);
     }
     if (lay.NB > 1) {
-        const size_t smem_apply = (size_t)(2 * kD * k + kD + KB + KB * KB + 2 * kD * kLdC) * sizeof(double);
+        const size_t smem_apply = (size_t)(2 * kD * KB + kD + KB + KB * KB + 2 * kD * kLdC) * sizeof(double);
         st = check_cuda(
             cudaFuncSetAttribute(bapply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_apply));
         if (st != GCM_OK) return st;
+        CUtensorMap tm2;
+        if (lay.CI == 1 && a.bulk_ok &&
+            encode_tmap(&tm2, L, n, ldl, (unsigned)kT2Rows, (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B)) {
+            const size_t smem_t2 = t2_smem_bytes(KB);
+            st = check_cuda(cudaFuncSetAttribute(btma_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem_t2));
+            if (st != GCM_OK) return st;
+            const dim3 gridt(lay.NB - 1, (lay.NB - 1 + t2_strips(KB) - 1) / t2_strips(KB));
+            ProfScope ps("bapply", stream);
+            btma_kernel<KB><<<gridt, kT2Threads, smem_t2, stream>>>(tm2, n, k, a.chk, U, panels, lay.NB);
+            return check_cuda(cudaGetLastError());
+        }
         if (lay.CI == 1) {
             const size_t smem_tile =
                 (size_t)(2 * kD * KB + kD + KB + KB * KB + 2 * kStripsPerCta * kD * kLdC) * sizeof(double);
@@ -1294,7 +1494,7 @@ extern "C" int gcm_debug_htrace(long long *host, int count) {
 
 size_t blocked_workspace_bytes(int64_t n, int64_t k) {
     const int kc = (int)std::min<int64_t>(k, kBKMax);
-    return make_layout(n, kc, kChkBudget).total;
+    return make_layout(n, kc, chk_budget()).total;
 }
 
 gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
@@ -1303,7 +1503,7 @@ gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_
     char *base = reinterpret_cast<char *>(ws->panels);
     for (int64_t e0 = 0; e0 < k; e0 += kBKMax) {
         const int kc = (int)std::min<int64_t>(kBKMax, k - e0);
-        const Layout lay = make_layout(n, kc, kChkBudget);
+        const Layout lay = make_layout(n, kc, chk_budget());
         const unsigned epoch = ++ws->epoch;
         double *Vc = V + e0 * n;
         if (kc <= 4) st = blocked_pass<4>(L, n, ldl, Vc, kc, sigma, key, e0, base, lay, epoch, stream);

@@ -191,3 +191,12 @@ def test_parity_headline_config(gcm):
     """BASELINE configs[1]: n=5000, k=16, update and downdate, full-size element-wise parity."""
     for sigma in (1, -1):
         check(*run_both(gcm, 5000, 16, sigma, seed=synth.SEED_ROOT), 5000)
+
+
+@pytest.mark.parametrize("budget,n,k", [(1 << 18, 700, 16), (1 << 17, 1000, 5), (1 << 15, 1000, 5), (1 << 21, 1300, 32)])  # CI = 2, 4, 16, 2
+@pytest.mark.parametrize("sigma", [1, -1])
+def test_parity_checkpoint_interval(gcm, monkeypatch, budget, n, k, sigma):
+    """A small checkpoint budget forces CI > 1 (the very-large-n Apply walk, bapply_kernel),
+    which the default 2 GiB budget only reaches at n ~ 1e5."""
+    monkeypatch.setenv("GCM_CHK_BUDGET", str(budget))
+    check(*run_both(gcm, n, k, sigma, seed=n + k, algo="blocked"), n)
