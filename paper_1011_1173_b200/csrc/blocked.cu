@@ -68,7 +68,7 @@ struct Layout {
     int k;
     int NT, NB, CI;
     int64_t nchk;
-    size_t P, rcur, rchain, pfast, MX, chk, Q, G, U, panels, flags, total;
+    size_t P, rcur, rchain, pfast, MX, chk, G, Q, U, panels, flags, total;
 };
 
 __host__ __device__ inline int64_t chk_count_before(int64_t s, int CI) {
@@ -114,12 +114,12 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
     l.pfast = take((size_t)l.NT * kDT * k);  // must follow rchain (one memset arms both)
     l.MX = take((size_t)l.NT * 2 * kDT * kDT);
     l.chk = take((size_t)l.nchk * kD * k);
-    l.Q = take((size_t)l.NB * k * k);
-    l.G = take((size_t)l.NB * k * k);
+    l.G = take((size_t)l.NB * kb_of(k) * kb_of(k));     // Gram prefixes G_b (KB x KB)
+    l.Q = take((size_t)l.NT * kb_of(k) * kb_of(k));     // per 32-row block P_tb^T P_tb (helpers)
     l.U = take((size_t)l.NB * kb_of(k) * kb_of(k));       // U_b^{-1}, KB x KB, zero padded
     l.panels = take((size_t)l.NB * panel_doubles(kb_of(k)));  // coefficient panels, stride KB
-    l.flags = take((1ull * l.NT * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
-                   8);  // prog[16 * kProgStride], lflag
+    l.flags = take((2ull * l.NT * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
+                   8);  // prog[16 * kProgStride], lflag, qflag
     l.total = o;
     return l;
 }
@@ -240,6 +240,10 @@ struct TrsvArgs {
     unsigned long long *prog;  // [NC] chain progress: (epoch << 32) | blocks published
     unsigned *lflag;
     unsigned epoch;
+    double *G, *Ui;   // Gram prefixes G_b = P_{<b}^T P_{<b} and U_b^{-1} (U_b = chol_lower(I + sigma G_b))
+    double *Q;        // per 32-row block Q_tb = P_tb^T P_tb (KB x KB), by the helper of strip tb+1
+    unsigned *qflag;  // [NT] epoch when Q_tb is stored
+    int sigma;
 };
 
 constexpr int kRPC = 2;                 // right-hand sides per chain CTA
@@ -820,8 +824,134 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                 }
             }
         }
+        if (s == tb + 1) {  // this strip's last tile: the Gram contribution of P_tb for the Gram CTA
+            for (int o = t; o < KB * KB; o += kHelpCompute) {
+                const int e1 = o / KB, e2 = o % KB;
+                double acc0 = 0.0, acc1 = 0.0;
+                if (e1 < k && e2 < k) {
+#pragma unroll 8
+                    for (int m = 0; m < kDT; m += 2) {
+                        acc0 = fma(Pt[m * k + e1], Pt[m * k + e2], acc0);
+                        acc1 = fma(Pt[(m + 1) * k + e1], Pt[(m + 1) * k + e2], acc1);
+                    }
+                }
+                a.Q[(int64_t)tb * KB * KB + o] = acc0 + acc1;
+            }
+            named_bar(1, kHelpCompute);
+            if (t == 0) {
+                __threadfence();
+                st_release(a.qflag + tb, a.epoch);
+            }
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + slot);
+    }
+}
+
+// U^{-1} for U = chol_lower(A), A a KB x KB SPD matrix, in one warp: Gaussian elimination
+// on [A | I] with lane i holding row i (A part in a[], identity part in w[]); step c
+// broadcasts the pivot row by shuffles and every lower lane eliminates with one
+// multiply by the pivot's reciprocal, leaving A = D U'^T and w = U'^{-1} (U' unit
+// lower); then U^{-1} = D^{-1/2} U'^{-1}.  Writes U^{-1} row-major to out[KB*KB]
+// (lane i writes row i).  A non-positive pivot gives NaNs (the sweep reports it).
+template <int KB>
+__device__ __forceinline__ void warp_chol_inv(double (&a)[KB], double *out) {
+    const int i = threadIdx.x & 31;
+    double w[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) w[j] = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int c = 0; c < KB - 1; ++c) {
+        const double rp = 1.0 / __shfl_sync(kFull, a[c], c);
+        const double f = i > c ? a[c] * rp : 0.0;
+#pragma unroll
+        for (int j = c + 1; j < KB; ++j) a[j] = fma(-f, __shfl_sync(kFull, a[j], c), a[j]);
+#pragma unroll
+        for (int j = 0; j <= c; ++j) w[j] = fma(-f, __shfl_sync(kFull, w[j], c), w[j]);
+    }
+    double di = 0.0;
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+        if (j == i) di = a[j];
+    const double s = rsqrt(di);
+    if (i < KB)
+#pragma unroll
+        for (int j = 0; j < KB; ++j) out[i * KB + j] = w[j] * s;
+}
+
+// ---------------------------------------------------------------- Gram CTA
+// Accumulates G = P^T P block by block as the chains publish P (warps 0..3), stores the
+// prefix G_b at every 64-row boundary, and the other warps turn each G_b into
+// U_b^{-1} (chol_lower(I + sigma G_b), inverted) -- so the diagonal sweeps and the
+// Apply tiles find U_b^{-1} ready when the solve ends (no Gram/scan kernels).
+__host__ __device__ constexpr bool gram_chol_here(int KB) { return KB <= 16; }
+
+template <int KB>
+__device__ void trsv_gram(const TrsvArgs &a, double *smem) {
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int k = a.k;
+    const int NB = (int)((a.n + kD - 1) / kD);
+    constexpr int kAccT = 128;
+    volatile int *gready = reinterpret_cast<volatile int *>(smem);
+    if (t == 0) *gready = 0;
+    for (int o = t; o < KB * KB; o += blockDim.x) a.Ui[o] = (o / KB == o % KB) ? 1.0 : 0.0;  // U_0 = I
+    __syncthreads();
+    if (warp < kAccT / 32) {
+        // prefix sums of the helpers' per-block Grams Q_tb (thread t owns entries t + 128u)
+        constexpr int EPB = (KB * KB + kAccT - 1) / kAccT;
+        double g[EPB];
+#pragma unroll
+        for (int u = 0; u < EPB; ++u) g[u] = 0.0;
+        const int NT = (int)((a.n + kDT - 1) / kDT);
+        for (int tb = 0; tb + 1 < NT; ++tb) {  // Q of the last 32-row block never enters a G_b (b < NB)
+            if (t == 0)
+                while (ld_acquire(a.qflag + tb) != a.epoch) __nanosleep(GCM_POLL_NS);
+            named_bar(1, kAccT);
+            const double *Qt = a.Q + (int64_t)tb * KB * KB;
+#pragma unroll
+            for (int u = 0; u < EPB; ++u) {
+                const int o = t + kAccT * u;
+                if (o < KB * KB) g[u] += __ldcg(Qt + o);
+            }
+            const int bn = tb / 2 + 1;
+            if ((tb & 1) && bn < NB) {  // G_bn = P_{<bn}^T P_{<bn}
+#pragma unroll
+                for (int u = 0; u < EPB; ++u) {
+                    const int o = t + kAccT * u;
+                    if (o < KB * KB) a.G[(int64_t)bn * KB * KB + o] = g[u];
+                }
+                named_bar(1, kAccT);
+                if (t == 0) {
+                    __threadfence_block();
+                    *gready = bn;
+                }
+            }
+        }
+        return;
+    }
+    // U_b^{-1} warps: block bn by warp 4 + (bn - 1) % nw (for KB = 32 the inversion is too
+    // slow to keep pace with the chains; the diagonal kernel does it, see gram_chol_here)
+    if (!gram_chol_here(KB)) return;
+    const int nw = (int)(blockDim.x >> 5) - kAccT / 32, cw = warp - kAccT / 32;
+    const double sg = a.sigma > 0 ? 1.0 : -1.0;
+    for (int bn = 1 + cw; bn < NB; bn += nw) {
+        if (lane == 0)
+            while (*gready < bn) {
+            }
+        __syncwarp();
+        __threadfence_block();
+#ifdef GCM_SWEEP_TRACE
+        if (lane == 0 && bn < 500) gcm_sweep_trace[1536 + bn] = clock64();
+#endif
+        const double *Gb = a.G + (int64_t)bn * KB * KB;
+        double row[KB];
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+            row[j] = (lane < k && j < k) ? (lane == j ? 1.0 : 0.0) + sg * Gb[lane * KB + j] : (lane == j ? 1.0 : 0.0);
+        warp_chol_inv<KB>(row, a.Ui + (int64_t)bn * KB * KB);
+#ifdef GCM_SWEEP_TRACE
+        if (lane == 0 && bn < 500) gcm_sweep_trace[1024 + bn] = clock64();
+#endif
     }
 }
 
@@ -830,39 +960,13 @@ __global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_cons
     extern __shared__ __align__(128) double smem_trsv[];
     if ((int)blockIdx.x < a.NC)
         trsv_chain(a, smem_trsv, blockIdx.x);
+    else if ((int)blockIdx.x == a.NC) {
+#ifndef GCM_NO_GRAM
+        trsv_gram<KB>(a, smem_trsv);
+#endif
+    }
     else
-        trsv_helper<KB>(a, smem_trsv, blockIdx.x - a.NC, gridDim.x - a.NC);
-}
-
-// Q_b = P_b^T P_b over the 64 rows of block b.
-__global__ void gram_kernel(const double *__restrict__ P, int64_t n, int k, double *__restrict__ Q) {
-    const int b = blockIdx.x;
-    const int64_t r0 = (int64_t)b * kD;
-    const int nr = (int)imin64(kD, n - r0);
-    for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
-        const int e1 = o / k, e2 = o % k;
-        double s0 = 0.0, s1 = 0.0;
-        int m = 0;
-        for (; m + 1 < nr; m += 2) {
-            s0 = fma(P[(r0 + m) * k + e1], P[(r0 + m) * k + e2], s0);
-            s1 = fma(P[(r0 + m + 1) * k + e1], P[(r0 + m + 1) * k + e2], s1);
-        }
-        if (m < nr) s0 = fma(P[(r0 + m) * k + e1], P[(r0 + m) * k + e2], s0);
-        Q[(int64_t)b * k * k + o] = s0 + s1;
-    }
-}
-
-// G[b] = sum_{b' < b} Q[b']  (exclusive prefix over row blocks).
-__global__ void gscan_kernel(const double *__restrict__ Q, double *__restrict__ G, int NB, int k) {
-    for (int o = threadIdx.x; o < k * k; o += blockDim.x) {
-        double run = 0.0;
-#pragma unroll 8
-        for (int b = 0; b < NB; ++b) {
-            const double q = __ldg(Q + (int64_t)b * k * k + o);
-            G[(int64_t)b * k * k + o] = run;
-            run += q;
-        }
-    }
+        trsv_helper<KB>(a, smem_trsv, blockIdx.x - a.NC - 1, gridDim.x - a.NC - 1);
 }
 
 // One CTA per 64-row diagonal block, all blocks in parallel.
@@ -872,8 +976,8 @@ constexpr int kDiagThreads = kDiagNQ * kD + 32;  // column parts + the coefficie
 template <int KB>
 __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict__ L, int64_t n, int64_t ldl,
                                                    double *__restrict__ V, int k, int sigma,
-                                                   const double *__restrict__ P, const double *__restrict__ Q,
-                                                   double *__restrict__ Uout, double *__restrict__ panels,
+                                                   const double *__restrict__ P, double *__restrict__ Ui,
+                                                   const double *__restrict__ G, double *__restrict__ panels,
                                                    unsigned long long *key, int64_t ebase) {
     extern __shared__ double smem_bdiag[];
     double(*Ls)[kD + 1] = reinterpret_cast<double(*)[kD + 1]>(smem_bdiag);               // [kD][kD+1]
@@ -890,13 +994,15 @@ __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict_
     const int b = blockIdx.x;
     const int64_t r0 = (int64_t)b * kD;
     const int Db = (int)imin64(kD, n - r0);
+#ifdef GCM_SWEEP_TRACE
+    if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1000] = clock64();
+#endif
 
-    // G_b (prefix-summed by gscan_kernel)  ->  M = I + sigma G_b
-    for (int o = t; o < k * k; o += kDiagThreads) {
-        const double g = Q[(int64_t)b * k * k + o];
-        const int e1 = o / k, e2 = o % k;
-        M[e1][e2] = (e1 == e2 ? 1.0 : 0.0) + (sigma > 0 ? g : -g);
-    }
+    // U_b^{-1}: computed by the TRSV kernel's Gram CTA from G_b (KB <= 16), else here by
+    // the coefficient warp (idle until the sweep) while the column threads form w
+    double *Uis = reinterpret_cast<double *>(M);  // [KB][KB] in the (KB x KB+1) slot
+    if (gram_chol_here(KB))
+        for (int o = t; o < KB * KB; o += kDiagThreads) Uis[o] = Ui[(int64_t)b * KB * KB + o];
     for (int idx = t; idx < kD * kD; idx += kDiagThreads) {
         const int m = idx / kD, j = idx % kD;
         if (m < Db && j <= m) Ls[m][j] = L[(r0 + j) + (r0 + m) * ldl];
@@ -906,69 +1012,68 @@ __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict_
         Ps[m][e] = m < Db ? P[(r0 + m) * k + e] : 0.0;
     }
     __syncthreads();
-    // U = chol_lower(M) in place (lower triangle), one warp, lane = row
-    if (t < 32) {
-        const int i = t;
-        for (int c = 0; c < k; ++c) {
-            if (i == c) M[c][c] = sqrt(M[c][c]);
-            __syncwarp();
-            if (i > c && i < k) M[i][c] = M[i][c] / M[c][c];
-            __syncwarp();
-            if (i > c && i < k)
-                for (int j = c + 1; j <= i; ++j) M[i][j] = fma(-M[i][c], M[j][c], M[i][j]);
-            __syncwarp();
-        }
-    }
-    __syncthreads();
-    // U_b^{-1} (lower, KB x KB zero padded) for the off-diagonal tiles' V states:
-    // lane c solves U x = e_c by forward substitution
-    if (t < KB) {
-        const int c = t;
-        double x[KB];
+#ifdef GCM_SWEEP_TRACE
+    if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1003] = clock64();
+#endif
+    constexpr int EPT = KB / kDiagNQ;
+    if (t < kDiagNQ * kD) {
+        // column threads (m, q): w = (L_bb^T P_b)[m] for update columns q*EPT .. (into vt)
+        const int cm = t % kD, cq = t / kD;
+        double w[EPT];
 #pragma unroll
-        for (int i = 0; i < KB; ++i) {
-            if (i >= c && i < k) {
-                double acc = (i == c) ? 1.0 : 0.0;
+        for (int i = 0; i < EPT; ++i) w[i] = 0.0;
+        if (cm < Db) {
+            for (int j = 0; j <= cm; ++j) {
+                const double l = Ls[cm][j];
 #pragma unroll
-                for (int j = 0; j < i; ++j)
-                    if (j >= c) acc = fma(-M[i][j], x[j], acc);
-                x[i] = acc / M[i][i];
-            } else {
-                x[i] = 0.0;
+                for (int i = 0; i < EPT; ++i) w[i] = fma(l, Ps[j][cq * EPT + i], w[i]);
             }
         }
 #pragma unroll
-        for (int i = 0; i < KB; ++i) Uout[(int64_t)b * KB * KB + i * KB + c] = x[i];
-    }
-    // V-state of column r0+t: y = U^{-1} (L_bb^T P_b)[t]
-    double v[KB];
+        for (int i = 0; i < EPT; ++i) vt[cm * KB + cq * EPT + i] = w[i];
+#ifdef GCM_SWEEP_TRACE
+        if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1005] = clock64();
+#endif
+    } else if (!gram_chol_here(KB)) {
+
+        const int lane = t & 31;
+        if (b == 0) {
+            for (int o = lane; o < KB * KB; o += 32) Uis[o] = (o / KB == o % KB) ? 1.0 : 0.0;
+        } else {
+            const double *Gb = G + (int64_t)b * KB * KB;
+            double row[KB];
 #pragma unroll
-    for (int e = 0; e < KB; ++e) v[e] = 0.0;
-    if (t < Db) {
-        for (int j = 0; j <= t; ++j) {
-            const double l = Ls[t][j];
-#pragma unroll
-            for (int e = 0; e < KB; ++e) v[e] = fma(l, Ps[j][e], v[e]);
+            for (int j = 0; j < KB; ++j)
+                row[j] = (lane < k && j < k) ? (lane == j ? 1.0 : 0.0) + (sigma > 0 ? Gb[lane * KB + j] : -Gb[lane * KB + j])
+                                             : (lane == j ? 1.0 : 0.0);
+            warp_chol_inv<KB>(row, Uis);
         }
-#pragma unroll
-        for (int e = 0; e < KB; ++e) {
-            if (e < k) {
-                double s = v[e];
-#pragma unroll
-                for (int ep = 0; ep < e; ++ep) s = fma(-M[e][ep], v[ep], s);
-                v[e] = s / M[e][e];
-            } else {
-                v[e] = 0.0;
-            }
-        }
+        __syncwarp();
+        for (int o = lane; o < KB * KB; o += 32) Ui[(int64_t)b * KB * KB + o] = Uis[o];
     }
     __syncthreads();
-    if (t < kD)
+#ifdef GCM_SWEEP_TRACE
+    if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1006] = clock64();
+#endif
+    if (t < kDiagNQ * kD) {  // V state y = U^{-1} w
+        const int cm = t % kD, cq = t / kD;
 #pragma unroll
-        for (int e = 0; e < KB; ++e) Vs[t * KB + e] = (t < Db && e < k) ? v[e] : 0.0;
+        for (int i = 0; i < EPT; ++i) {
+            const int e = cq * EPT + i;
+            double acc = 0.0;
+            for (int ep = 0; ep <= e; ++ep) acc = fma(Uis[e * KB + ep], vt[cm * KB + ep], acc);
+            Vs[cm * KB + e] = (cm < Db && e < k) ? acc : 0.0;
+        }
+    }
     __syncthreads();  // wave_sweep reads Vs from other threads before its own first barrier
+#ifdef GCM_SWEEP_TRACE
+    if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1001] = clock64();
+#endif
     wave_sweep<KB, kDiagNQ, kD + 1>(Ls, Vs, Db, k, sigma, r0, pan, V + r0, n, key, ebase, vx, dinv, vt, imx, 0,
                                     kDiagNQ * kD / 32);
+#ifdef GCM_SWEEP_TRACE
+    if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1002] = clock64();
+#endif
     // panel out in the blocked path's stride-KB layout (padding rotations are identities)
     double *panel = panels + (int64_t)b * panel_doubles(KB);
     for (int i = t; i < (int)panel_doubles(KB); i += kDiagThreads) panel[i] = pan[i];
@@ -1392,9 +1497,14 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     unsigned *flags = reinterpret_cast<unsigned *>(wsbase + lay.flags);
     a.prog = reinterpret_cast<unsigned long long *>(flags);
     a.lflag = flags + 2 * 16 * kProgStride;
+    a.qflag = a.lflag + lay.NT;
+    a.Q = reinterpret_cast<double *>(wsbase + lay.Q);
     a.epoch = epoch;
 
     a.NC = (k + kRPC - 1) / kRPC;
+    a.G = reinterpret_cast<double *>(wsbase + lay.G);
+    a.Ui = reinterpret_cast<double *>(wsbase + lay.U);
+    a.sigma = sigma;
     int dev = 0, nsm = 0;
     gcm_status_t st = check_cuda(cudaGetDevice(&dev));
     if (st == GCM_OK) st = check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -1410,8 +1520,8 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     st = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trsv_kernel<KB>, kTrsvThreads, smem));
     if (st != GCM_OK) return st;
     if (per_sm < 1) return GCM_ECUDA;
-    const int grid = (int)std::min<int64_t>((int64_t)nsm * per_sm, a.NC + lay.NT);
-    if (grid <= a.NC) return GCM_ECUDA;
+    const int grid = (int)std::min<int64_t>((int64_t)nsm * per_sm, a.NC + 1 + lay.NT);
+    if (grid <= a.NC + 1) return GCM_ECUDA;
     void *args[] = {&a};
     // hand-off slots start empty (all-ones); consumers re-arm what they read
     st = check_cuda(cudaMemsetAsync(a.rchain, 0xff, lay.pfast - lay.rchain + (size_t)lay.NT * kDT * k * sizeof(double),
@@ -1424,18 +1534,8 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     }
     if (st != GCM_OK) return st;
 
-    double *Q = reinterpret_cast<double *>(wsbase + lay.Q);
     double *U = reinterpret_cast<double *>(wsbase + lay.U);
     double *panels = reinterpret_cast<double *>(wsbase + lay.panels);
-    {
-        ProfScope ps("gram", stream);
-        gram_kernel<<<lay.NB, 256, 0, stream>>>(a.P, n, k, Q);
-    }
-    double *G = reinterpret_cast<double *>(wsbase + lay.G);
-    {
-        ProfScope ps("gscan", stream);
-        gscan_kernel<<<1, 1024, 0, stream>>>(Q, G, lay.NB, k);
-    }
     const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 +
                                       4 * kD * KB + kD) *
                              sizeof(double);
@@ -1443,7 +1543,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (st != GCM_OK) return st;
     {
         ProfScope ps("bdiag", stream);
-        bdiag_kernel<KB><<<lay.NB, kDiagThreads, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, G, U, panels, key,
+        bdiag_kernel<KB><<<lay.NB, kDiagThreads, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, U, a.G, panels, key,
                                                                       ebase);
     }
     if (lay.NB > 1) {
@@ -1487,6 +1587,11 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
 extern "C" int gcm_debug_trace(long long *host, int count) {
     return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * count);
 }
+#ifdef GCM_SWEEP_TRACE
+extern "C" int gcm_debug_sweep_trace(long long *host, int count) {
+    return (int)cudaMemcpyFromSymbol(host, gcm::gcm_sweep_trace, sizeof(long long) * count);
+}
+#endif
 extern "C" int gcm_debug_htrace(long long *host, int count) {
     return (int)cudaMemcpyFromSymbol(host, g_htrace, sizeof(long long) * count);
 }

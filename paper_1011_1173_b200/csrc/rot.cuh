@@ -188,7 +188,7 @@ __device__ __forceinline__ void block_sweep(double (*Ls)[LD], double (&v)[KMAX],
 //   pan            : smem panel, (gamma, delta) at pan[2*(j*KB+e)], rho at 2*kD*KB, nu at +kD
 // Scratch (smem): vx[kD*KB], dinv[kD], vt[kD*KB], imx[kD*KB].  Called by ALL threads.
 #ifdef GCM_SWEEP_TRACE
-__device__ long long gcm_sweep_trace[4 * 256];
+__device__ long long gcm_sweep_trace[2048];
 #endif
 __host__ __device__ constexpr int wave_panel_doubles(int KB) { return 2 * kD * KB + kD + KB; }
 
