@@ -42,10 +42,24 @@ namespace gcm {
 namespace {
 
 constexpr int kDT = 32;            // rows per triangular-solve block
-constexpr int kTrsvThreads = 288;  // chain CTA: 2 critical + 5 prep + publisher + loader warps;
+constexpr int kTrsvThreads = 288;  // chain CTA: 2 critical + 6 prep + loader warps;
                                    // helper CTA: 8 compute warps + 1 feeder warp
 constexpr int kBKMax = 32;         // update columns per pass
 constexpr int kApplyT = 64;        // threads per apply CTA (= kD columns)
+constexpr int kLdT = kDT + 1;
+#ifndef GCM_LOOKC
+#define GCM_LOOKC 4
+#endif
+constexpr int kLookC = GCM_LOOKC;       // blocks of lookahead the chain absorbs
+constexpr int kSeg = (kLookC - 1) * kDT;  // rows of the prepared part of a lookahead segment (lags 2..kLookC)
+constexpr int kLdN = kSeg + 1;            // row stride of N (odd: lane = j reads are conflict-free)
+// Per 32-row block tb the helpers precompute (J1), contiguous so one bulk copy stages it:
+//   N   [kDT][kLdN]  N(j, R) = sum_q X(q, j) L(rs + R, tb*32 + q),  rs = (tb - kLookC) * 32
+//   M^T [kDT][kDT]   M = X^T L_{tb-1,tb}^T
+//   X   [kDT][kDT]   X = L_{tb,tb}^{-1} (row-major)
+// so the chain's prepared value is  prepX_tb = X^T r^{hand} - N p_seg  (no X matvec after the sums).
+constexpr int kMXN = kDT * kLdN;
+constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per block (16-byte multiple)
 
 #ifndef GCM_PROG_STRIDE
 #define GCM_PROG_STRIDE 16
@@ -55,6 +69,15 @@ constexpr int kApplyT = 64;        // threads per apply CTA (= kD columns)
 #endif
 #ifndef GCM_PUB_FENCE
 #define GCM_PUB_FENCE 1
+#endif
+#ifndef GCM_FEEDER_POLL
+#define GCM_FEEDER_POLL 1
+#endif
+#ifndef GCM_LATE_LOAD
+#define GCM_LATE_LOAD 0
+#endif
+#ifndef GCM_HPREFETCH
+#define GCM_HPREFETCH 1
 #endif
 #ifndef GCM_POLL_NS
 #define GCM_POLL_NS 20
@@ -111,15 +134,15 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
     l.P = take((size_t)l.NT * kDT * k);  // padded to whole 32-row blocks (bulk copies)
     l.rcur = take((size_t)l.NT * kDT * k);
     l.rchain = take((size_t)l.NT * kDT * k);
-    l.pfast = take((size_t)l.NT * kDT * k);  // must follow rchain (one memset arms both)
-    l.MX = take((size_t)l.NT * 2 * kDT * kDT);
+    l.pfast = take((size_t)l.NT * kDT * k + 2);  // must follow rchain (one memset arms both); + ticket counter
+    l.MX = take((size_t)l.NT * kMXStride);
     l.chk = take((size_t)l.nchk * kD * k);
     l.G = take((size_t)l.NB * kb_of(k) * kb_of(k));     // Gram prefixes G_b (KB x KB)
     l.Q = take((size_t)l.NT * kb_of(k) * kb_of(k));     // per 32-row block P_tb^T P_tb (helpers)
     l.U = take((size_t)l.NB * kb_of(k) * kb_of(k));       // U_b^{-1}, KB x KB, zero padded
     l.panels = take((size_t)l.NB * panel_doubles(kb_of(k)));  // coefficient panels, stride KB
-    l.flags = take((2ull * l.NT * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
-                   8);  // prog[16 * kProgStride], lflag, qflag
+    l.flags = take(((2ull * l.NT + l.NB) * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
+                   8);  // prog[16 * kProgStride], lflag, qflag, uflag
     l.total = o;
     return l;
 }
@@ -135,12 +158,15 @@ __device__ __forceinline__ long long gtime() {
 __device__ long long g_htrace[4096 * 8];  // hand-off timeline in globaltimer ns, indexed by strip s
 #define HTRACE(slot, s) (g_htrace[(s) * 8 + (slot)] = gtime())
 #define CTRACE(slot, s) (g_trace[(s) * 8 + (slot)] = clock64())
+// one helper's per-tile phases (clock64), rows = tile sequence number
+#define HPT(slot, val) ((h == 100 && t == 0 && seq < 2900) ? (void)(g_htrace[seq * 8 + (slot)] = (val)) : (void)0)
 __device__ long long g_trace[4096 * 8];
 #define TRACE(slot, tb) (blockIdx.x == 0 ? (void)(g_trace[(tb) * 8 + (slot)] = clock64()) : (void)0)
 #else
 #define TRACE(slot, tb) ((void)0)
 #define HTRACE(slot, s) ((void)0)
 #define CTRACE(slot, s) ((void)0)
+#define HPT(slot, val) ((void)0)
 #endif
 
 // Bytes of Apply checkpoints before the checkpoint interval CI doubles (2 GiB;
@@ -232,9 +258,8 @@ struct TrsvArgs {
     const double *V;  // this pass's first column (ld n)
     int k;
     double *P, *rcur, *rchain, *pfast, *chk;  // pfast: self-validating copy of P for the hand-off tiles
-    double *MX;       // per 32-block: M^T (row-major) then X (row-major), X = L_bb^{-1}, M = X^T L_{b-1,b}^T
-    bool bulk_ok;     // L 16-byte aligned and ldl even: TMA loads of the lookahead segments
-    CUtensorMap tmapL;  // 2-D tensor map over L (rows contiguous, ldl stride), box kSeg rows x 32 columns
+    double *MX;       // per 32-block (kMXStride doubles): N, M^T, X (see kMXN)
+    bool bulk_ok;     // L 16-byte aligned and ldl even (the Apply's TMA path)
     int CI, CIlog;  // checkpoint interval (a power of two) and its log2
     int NC;           // chain CTAs (each solves kRPC right-hand sides)
     unsigned long long *prog;  // [NC] chain progress: (epoch << 32) | blocks published
@@ -244,19 +269,22 @@ struct TrsvArgs {
     double *Q;        // per 32-row block Q_tb = P_tb^T P_tb (KB x KB), by the helper of strip tb+1
     unsigned *qflag;  // [NT] epoch when Q_tb is stored
     int sigma;
+    // fused diagonal sweeps: helpers whose strips are done run bdiag tasks (ticket order)
+    double *Vw;               // this pass's V (V_exit written by the sweeps)
+    double *panels;           // coefficient panels
+    unsigned long long *key;  // first-failure key
+    int64_t ebase;            // first update column of this pass
+    unsigned *uflag;          // [NB] epoch when what block b's sweep needs from the Gram CTA is stored
+    unsigned *taskctr;        // ticket counter (armed to all-ones by the pass's memset)
+    int fuse;                 // 1: the diagonal sweeps run here (else bdiag_kernel after this kernel)
 };
 
 constexpr int kRPC = 2;                 // right-hand sides per chain CTA
-#ifndef GCM_LOOKC
-#define GCM_LOOKC 4
-#endif
-constexpr int kLookC = GCM_LOOKC;       // blocks of lookahead the chain absorbs
-constexpr int kPrepWarps = 5;           // chain CTA warps: 0..kRPC-1 critical, then prep, publisher, loader
+constexpr int kPrepWarps = 6;           // chain CTA warps: 0..kRPC-1 critical, then prep, then the loader
 constexpr int kPrepThreads = kPrepWarps * 32;
-constexpr int kSvcWarp = kRPC + kPrepWarps;  // publisher warp; kSvcWarp + 1 = loader warp
-constexpr int kSeg = (kLookC - 1) * kDT;  // rows of the prepared part of a lookahead segment
-constexpr int kLdS = kSeg;                // smem stride of a segment column (dense: the TMA box layout)
-constexpr int kLdT = kDT + 1;
+constexpr int kSvcWarp = kRPC + kPrepWarps;  // loader warp
+constexpr int kWin = kLookC <= 4 ? 128 : kLookC <= 8 ? 256 : 512;  // rows of the chain's p window (pow2 >= kLookC*kDT)
+static_assert(kWin >= kLookC * kDT && kLookC <= 16, "p window indexed by row & (kWin - 1)");
 constexpr int kHelpMaxOwn = 4;          // strips whose residual a helper keeps in shared memory
 constexpr int kHelpRing = 6;            // tiles (L tile + P block) a helper's feeder keeps in flight
 #ifndef GCM_FASTBACK
@@ -264,7 +292,7 @@ constexpr int kHelpRing = 6;            // tiles (L tile + P block) a helper's f
 #endif
 constexpr int kFastBack = GCM_FASTBACK;         // tiles before the hand-off tile that also read P from pfast
 constexpr int kHelpCompute = 256;       // helper compute threads (warps 0..7); warp 8 feeds
-static_assert((kSvcWarp + 2) * 32 <= kTrsvThreads, "chain CTA needs publisher and loader warps");
+static_assert((kSvcWarp + 1) * 32 <= kTrsvThreads, "chain CTA needs a loader warp");
 
 // Tile (tb, s) takes P_tb from pfast (no progress word, no bulk copy) when it is
 // the strip's hand-off tile or one of the kFastBack before it: those sit on the
@@ -308,18 +336,17 @@ __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, unsig
                  : "memory");
 }
 
-// Shared-memory plan of a chain CTA (doubles).  A "stage" holds the operands of
-// one row block tb: the lookahead segment (rows (tb-kLookC)*32 .. (tb-1)*32-1 of
-// the block's 32 columns), M_tb^T and X_tb (row-major).  Three stages rotate.
+// Shared-memory plan of a chain CTA (doubles).  A "stage" holds block tb's
+// precomputed operands (N, M^T, X: one bulk copy of kMXStride doubles); three
+// stages rotate.
 struct ChainSmem {
-    static constexpr int seg = kDT * kLdS;
-    static constexpr int stage = seg + 2 * kDT * kDT;
+    static constexpr int stage = kMXStride;
     static constexpr int off_stage = 0;                                   // [3][stage]
-    static constexpr int off_pwin = off_stage + 3 * stage;                // [kLookC][kDT][kRPC]
-    static constexpr int off_part = off_pwin + kLookC * kDT * kRPC;       // [kPrepWarps][kDT][kRPC]
-    static constexpr int off_acc = off_part + kPrepWarps * kDT * kRPC;    // [kDT][kRPC]
-    static constexpr int off_prepx = off_acc + kDT * kRPC;                // [2][kDT][kRPC]
-    static constexpr int off_bar = off_prepx + 2 * kDT * kRPC;            // 3 mbarriers (u64)
+    static constexpr int off_pwin = off_stage + 3 * stage;                // [kWin][kRPC]  p by row & (kWin-1)
+    static constexpr int off_part = off_pwin + kWin * kRPC;               // [kPrepWarps][kDT][kRPC]
+    static constexpr int off_hand = off_part + kPrepWarps * kDT * kRPC;   // [kDT][kRPC]  hand-off residual
+    static constexpr int off_prepx = off_hand + kDT * kRPC;               // [2][kDT][kRPC]
+    static constexpr int off_bar = off_prepx + 2 * kDT * kRPC;            // 3 mbarriers (u64) + pcount
     static constexpr int total = off_bar + 4;
 };
 
@@ -328,11 +355,12 @@ struct ChainSmem {
 // 32 rows (one block tb) per step:
 //   critical warps (one per RHS, lane = row j):  p_tb = prepX_tb - M_tb p_{tb-1}
 //        with M_tb = X_tb^T L_{tb-1,tb}^T precomputed by the helpers (X_tb = L_tb,tb^{-1});
-//   prep warps: prepX_{tb+1} = X_{tb+1}^T ( r^{(tb+1-kLookC)} - sum_{i=2..kLookC} L_{tb+1-i,tb+1}^T p_{tb+1-i} ),
-//        r^{(.)} handed over by the helper owning strip tb+1;
-//   service warp: publishes progress and streams block tb+3's operands with TMA
-//        bulk copies (one per column segment) on a per-stage mbarrier.
-// The k right-hand sides are independent, so chain CTAs never talk to each other.
+//   prep warps: prepX_{tb+1} = X_{tb+1}^T r^{(tb+1-kLookC)} - N_{tb+1} p_{rows of blocks tb-kLookC+2 .. tb-1},
+//        r^{(.)} handed over by the helper owning strip tb+1 (its load is issued first),
+//        N = X^T L_seg^T precomputed, the rows split evenly over the prep warps;
+//   loader warp: streams block tb+3's operands (one bulk copy) on a per-stage mbarrier.
+// The k right-hand sides are independent, so chain CTAs never talk to each other;
+// the helpers read p from the self-validating copy pfast (no progress words).
 __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
     using S = ChainSmem;
     const int t = threadIdx.x;
@@ -342,126 +370,125 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
     const int e0 = c * kRPC;
     double *pwin = smem + S::off_pwin;
     double *part = smem + S::off_part;
-    double *accs = smem + S::off_acc;
+    double *hand = smem + S::off_hand;
     double *prepx = smem + S::off_prepx;
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + S::off_bar);
     auto stage_of = [&](int tb) { return smem + S::off_stage + (tb % 3) * S::stage; };
-    const bool bulk = a.bulk_ok;
 
-    // service warp: bring block tb's operands into stage tb % 3
+    // loader warp: bring block tb's operands into stage tb % 3
     auto issue_loads = [&](int tb) {
-        double *st = stage_of(tb);
-        unsigned long long *bar = bars + (tb % 3);
-        const int64_t c0 = (int64_t)tb * kDT;
-        const int nc = (int)imin64(kDT, a.n - c0);
-        const int64_t rs = (int64_t)(tb - kLookC) * kDT;  // first segment row (may be < 0)
-        const int skip = rs < 0 ? (int)imin64(-rs, kSeg) : 0;
-        if (lane == 0)
+        if (lane == 0) {
             while (ld_acquire(a.lflag + tb) != a.epoch) {
             }
-        __syncwarp();
-        if (bulk) {
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.global;" ::: "memory");  // helpers' generic stores -> TMA reads
-                const unsigned bytes = (unsigned)(kSeg * kDT) * 8u + 2u * kDT * kDT * 8u;
-                mbar_arrive_expect_tx(bar, bytes);
-                // one 2-D TMA box: rows rs .. rs+kSeg-1 (negative rows are zero-filled), columns c0..c0+31
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-                    "[%4];" ::"r"(smem_u32(st)),
-                    "l"(reinterpret_cast<uint64_t>(&a.tmapL)), "r"((int)rs), "r"((int)c0), "r"(smem_u32(bar))
-                    : "memory");
-                bulk_g2s(st + S::seg, a.MX + (int64_t)tb * 2 * kDT * kDT, 2u * kDT * kDT * 8u, bar);
-            }
-        } else {
-            for (int j = 0; j < nc; ++j)
-                for (int r = skip + lane; r < kSeg; r += 32)
-                    cp_async8(st + j * kLdS + r, a.L + (rs + r) + (c0 + j) * a.ldl);
-            for (int i = lane; i < 2 * kDT * kDT; i += 32)
-                cp_async8(st + S::seg + i, a.MX + (int64_t)tb * 2 * kDT * kDT + i);
-            cp_async_commit();
-            cp_async_wait_all();
-            mbar_arrive(bar);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // helpers' generic stores -> bulk read
+            unsigned long long *bar = bars + (tb % 3);
+            mbar_arrive_expect_tx(bar, (unsigned)kMXStride * 8u);
+            bulk_g2s(stage_of(tb), a.MX + (int64_t)tb * kMXStride, (unsigned)kMXStride * 8u, bar);
         }
+        __syncwarp();
     };
 
     // critical warps count published p blocks here (monotonic; a named barrier
     // could be overrun because the critical warps may run two steps ahead of the
-    // service warp)
+    // loader warp)
     volatile unsigned *pcount = reinterpret_cast<volatile unsigned *>(bars + 3);
+    volatile unsigned *prepdone = pcount + 1;  // prep steps finished (prep warp 0 counts)
     if (t == 0) {
-        for (int i = 0; i < 3; ++i) mbar_init(bars + i, bulk ? 1u : 32u);
+        for (int i = 0; i < 3; ++i) mbar_init(bars + i, 1u);
         *pcount = 0u;
+        *prepdone = 0u;
     }
+    for (int i = t; i < kWin * kRPC; i += blockDim.x) pwin[i] = 0.0;  // rows < 0 of early segments (N is 0 there)
     __syncthreads();
-    if (warp == kSvcWarp + 1)
+    if (warp == kSvcWarp)
         for (int tb = 0; tb < 3 && tb < NT; ++tb) issue_loads(tb);
 
     // prep warps: prepX for block tb (needs p up to tb-2, i.e. <= step tb-1 of the critical warps)
     const int pt = t - kRPC * 32;
     auto do_prep = [&](int tb) {
         const double *st = stage_of(tb);
-        mbar_wait(bars + (tb % 3), (unsigned)((tb / 3) & 1));
-        if (pt == 0) TRACE(3, tb - 1);
-        const int pw = pt >> 5, j = lane;
-        // tasks: (lookahead block i = 2..kLookC, half h of its 32 rows); lane j = column
-        constexpr int kTasks = 2 * (kLookC - 1);
-        double acc[kRPC];
-#pragma unroll
-        for (int w = 0; w < kRPC; ++w) acc[w] = 0.0;
-        for (int task = pw; task < kTasks; task += kPrepWarps) {
-            const int i = 2 + (task >> 1), h = task & 1;
-            const int blk = tb - i;
-            if (blk < 0) continue;
-            // segment rows of block blk start at (kLookC - i) * 32
-            const double *col = st + j * kLdS + (kLookC - i) * kDT + h * 16;
-            const double *pp = pwin + ((blk % kLookC) * kDT + h * 16) * kRPC;
-            double s0[kRPC], s1[kRPC];
-#pragma unroll
-            for (int w = 0; w < kRPC; ++w) s0[w] = s1[w] = 0.0;
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int m = (q + j) & 15;  // per-lane rotation: spreads the even-stride reads over banks
-                const double l = col[m];
-#pragma unroll
-                for (int w = 0; w < kRPC; ++w) {
-                    if (q & 1) s1[w] = fma(-l, pp[m * kRPC + w], s1[w]);
-                    else s0[w] = fma(-l, pp[m * kRPC + w], s0[w]);
-                }
-            }
-#pragma unroll
-            for (int w = 0; w < kRPC; ++w) acc[w] += s0[w] + s1[w];
-        }
-#pragma unroll
-        for (int w = 0; w < kRPC; ++w) part[(pw * kDT + j) * kRPC + w] = acc[w];
-        if (pt == 0) TRACE(4, tb - 1);
-        named_bar(2, kPrepThreads);
+        // the hand-off value is usually stored before it is needed: issue its load
+        // first so its L2 round trip overlaps the stage wait and the partial sums
+        double *hptr = nullptr;
+        unsigned long long hv = 0ull;  // rows past n / padded RHS: 0
         if (pt < kDT * kRPC) {
             const int jj = pt / kRPC, w = pt % kRPC;
             const int e = e0 + w;
             const int64_t row = (int64_t)tb * kDT + jj;
-            double acc = 0.0;
-#pragma unroll
-            for (int q = 0; q < kPrepWarps; ++q) acc += part[(q * kDT + jj) * kRPC + w];
-            if (pt == 0 && c == 0) HTRACE(0, 3500 + tb);
-            if (e < k && row < a.n) acc += ld_handoff(a.rchain + (int64_t)tb * kDT * k + (int64_t)jj * k + e);
-            if (pt == 0 && c == 0) HTRACE(6, 3000 + tb);
-            accs[jj * kRPC + w] = acc;
+            if (e < k && row < a.n) {
+                hptr = a.rchain + (int64_t)tb * kDT * k + (int64_t)jj * k + e;
+                hv = ld_relaxed_u64(hptr);
+            }
         }
+        mbar_wait(bars + (tb % 3), (unsigned)((tb / 3) & 1));
+        if (pt == 0) TRACE(3, tb - 1);
+        const int pw = pt >> 5, j = lane;
+        const int rs = (tb - kLookC) * kDT;  // first segment row (may be < 0: N is zero there)
+        double acc0[kRPC], acc1[kRPC];
+#pragma unroll
+        for (int w = 0; w < kRPC; ++w) acc0[w] = acc1[w] = 0.0;
+#ifndef GCM_EXP_NOPART
+        {  // - N p over this warp's share of the kSeg segment rows
+            constexpr int kPer = (kSeg + kPrepWarps - 1) / kPrepWarps;
+            const int r0 = pw * kPer;
+            const double *nrow = st + j * kLdN;
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                const int R = r0 + q;
+                if (R < kSeg) {
+                    const double l = nrow[R];
+                    const double2 pv = *reinterpret_cast<const double2 *>(pwin + ((rs + R) & (kWin - 1)) * kRPC);
+                    if (q & 1) {
+                        acc1[0] = fma(-l, pv.x, acc1[0]);
+                        acc1[1] = fma(-l, pv.y, acc1[1]);
+                    } else {
+                        acc0[0] = fma(-l, pv.x, acc0[0]);
+                        acc0[1] = fma(-l, pv.y, acc0[1]);
+                    }
+                }
+            }
+        }
+#endif
+        if (pt == 0) TRACE(4, tb - 1);
+        if (hptr) {
+            if (pt == 0 && c == 0) HTRACE(0, 3500 + tb);
+            if (hv == kEmpty) {
+                hv = __double_as_longlong(ld_handoff(hptr));
+            } else {  // prefetched: re-arm the slot for the next call
+                asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(hptr), "l"(kEmpty) : "memory");
+            }
+            if (pt == 0 && c == 0) HTRACE(6, 3000 + tb);
+        }
+        if (pt < kDT * kRPC) hand[pt] = __longlong_as_double((long long)hv);
         if (pt == 0) TRACE(5, tb - 1);
         named_bar(2, kPrepThreads);
-        if (pt < kDT * kRPC) {  // prepX[j][w] = sum_q X(q, j) acc[q][w]   (X row-major in the stage)
-            const int jj = pt % kDT, w = pt / kDT;
-            const double *X = st + S::seg + kDT * kDT;
-            double x0 = 0.0, x1 = 0.0;
+#ifndef GCM_EXP_NOX
+        {  // + X^T r^{hand} over this warp's share of the 32 rows q
+            constexpr int kPerX = (kDT + kPrepWarps - 1) / kPrepWarps;
+            const double *X = st + kMXN + kDT * kDT;
 #pragma unroll
-            for (int q = 0; q < kDT; q += 2) {
-                x0 = fma(X[q * kDT + jj], accs[q * kRPC + w], x0);
-                x1 = fma(X[(q + 1) * kDT + jj], accs[(q + 1) * kRPC + w], x1);
+            for (int u = 0; u < kPerX; ++u) {
+                const int q = pw * kPerX + u;
+                if (q < kDT) {
+                    const double x = X[q * kDT + j];
+                    const double2 hvv = *reinterpret_cast<const double2 *>(hand + q * kRPC);
+                    acc0[0] = fma(x, hvv.x, acc0[0]);
+                    acc0[1] = fma(x, hvv.y, acc0[1]);
+                }
             }
-            prepx[(tb & 1) * kDT * kRPC + jj * kRPC + w] = x0 + x1;
+        }
+#endif
+#pragma unroll
+        for (int w = 0; w < kRPC; ++w) part[(pw * kDT + j) * kRPC + w] = acc0[w] + acc1[w];
+        named_bar(2, kPrepThreads);
+        if (pt < kDT * kRPC) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < kPrepWarps; ++q) acc += part[q * kDT * kRPC + pt];
+            prepx[(tb & 1) * kDT * kRPC + pt] = acc;
         }
     };
+    static_assert(kRPC == 2, "prep vectorises the two right-hand sides");
 
     double mrow[kDT];  // critical warps: row j of M_tb in registers
     if (warp >= kRPC && warp < kSvcWarp) do_prep(0);
@@ -469,36 +496,30 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         const double *st = stage_of(0);
         mbar_wait(bars + 0, 0u);
 #pragma unroll
-        for (int m = 0; m < kDT; ++m) mrow[m] = st[S::seg + m * kDT + lane];  // M^T stored: (m, j)
+        for (int m = 0; m < kDT; ++m) mrow[m] = st[kMXN + m * kDT + lane];  // M^T stored: (m, j)
     }
     if (warp < kSvcWarp) named_bar(1, kSvcWarp * 32);  // B_0
 
-    if (warp == kSvcWarp) {  // publisher: no memory traffic of its own, so its fence is cheap
-        for (int tb = 0; tb < NT; ++tb) {
-            if (lane == 0) {
-                while (*pcount < (unsigned)(kRPC * (tb + 1))) {
-                }
-#if GCM_PUB_FENCE
-                __threadfence();
-#endif
-                st_release64(a.prog + c * kProgStride, ((unsigned long long)a.epoch << 32) | (unsigned)(tb + 1));
-            }
-            __syncwarp();
-        }
-        return;
-    }
-    if (warp == kSvcWarp + 1) {  // loader: block tb+3 into stage tb%3 once step tb is under way
+    if (warp == kSvcWarp) {  // loader: block tb+3 into stage tb%3 once step tb is under way
         for (int tb = 0; tb + 3 < NT; ++tb) {
-            if (lane == 0)
+            if (lane == 0) {
+#if GCM_LATE_LOAD
+                // after prep(tb+1) is done: the bulk copy's smem writes then overlap the
+                // critical step, not the prep's shared-memory reads
+                while (*prepdone < (unsigned)(tb + 1)) {
+                }
+#else
                 while (*pcount < (unsigned)(kRPC * (tb + 1))) {
                 }
+#endif
+            }
             __syncwarp();
             issue_loads(tb + 3);
             if (lane == 0) TRACE(7, tb);
         }
         return;
     }
-    if (warp > kSvcWarp + 1) return;
+    if (warp > kSvcWarp) return;
     for (int tb = 0; tb < NT; ++tb) {
         if (warp < kRPC) {
             const int w = warp, j = lane;
@@ -506,7 +527,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
             double a0 = prepx[(tb & 1) * kDT * kRPC + j * kRPC + w], a1 = 0.0, a2 = 0.0, a3 = 0.0;
             if (t == 0 && c == 0) HTRACE(7, 3000 + tb);
             if (tb > 0) {
-                const double *pprev = pwin + ((tb - 1) % kLookC) * kDT * kRPC + w;
+                const double *pprev = pwin + (((tb - 1) * kDT) & (kWin - 1)) * kRPC + w;
 #pragma unroll
                 for (int m = 0; m < kDT; m += 4) {
                     a0 = fma(-mrow[m], pprev[m * kRPC], a0);
@@ -516,12 +537,12 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
                 }
             }
             const double p = (a0 + a1) + (a2 + a3);
-            pwin[((tb % kLookC) * kDT + j) * kRPC + w] = p;
+            pwin[(((tb * kDT) & (kWin - 1)) + j) * kRPC + w] = p;
             const int e = e0 + w;
             const int64_t row = (int64_t)tb * kDT + j;
             if (e < k && row < a.n) {
+                st_handoff(a.pfast + row * k + e, p);  // polled by the helpers (every tile) and the Gram path
                 a.P[row * k + e] = p;
-                st_handoff(a.pfast + row * k + e, p);  // polled by the helpers of strips tb+kLookC+1..
                 if (t == 0 && c == 0) HTRACE(0, 3000 + tb + kLookC + 1);
             }
             if (t == 0) TRACE(1, tb);
@@ -534,12 +555,15 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
                 const double *st = stage_of(tb + 1);
                 mbar_wait(bars + ((tb + 1) % 3), (unsigned)(((tb + 1) / 3) & 1));
 #pragma unroll
-                for (int m = 0; m < kDT; ++m) mrow[m] = st[S::seg + m * kDT + lane];
+                for (int m = 0; m < kDT; ++m) mrow[m] = st[kMXN + m * kDT + lane];
             }
         } else if (tb + 1 < NT) {
             if (pt == 0) TRACE(2, tb);
             do_prep(tb + 1);
-            if (pt == 0) TRACE(6, tb);
+            if (pt == 0) {
+                TRACE(6, tb);
+                *prepdone = (unsigned)(tb + 1);
+            }
         }
         named_bar(1, kSvcWarp * 32);  // B_{tb+1}: p_tb and prepX_{tb+1} ready
     }
@@ -547,7 +571,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
 
 // ---------------------------------------------------------------- helper CTAs
 template <int KB>
-__device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
+__device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
     constexpr int NQ = (kDT * KB + kTrsvThreads - 1) / kTrsvThreads;
     double *Lb = smem;                      // [kDT][kLdT]
     double *Pt = Lb + kDT * kLdT;           // [kDT][max(KB, kLdT)]  (P block; X during J1)
@@ -589,8 +613,16 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             const int q = idx / kDT, m = idx % kDT;
             Lb[q * kLdT + m] = (tb > 0 && q < nr) ? a.L[(r0 - kDT + m) + (r0 + q) * a.ldl] : 0.0;
         }
+        // segment (rows rs .. rs+kSeg-1 = blocks tb-kLookC .. tb-2, columns of block tb) into the
+        // (still idle) tile ring:  sg[q][R] = L(rs + R, tb*32 + q), zero above row 0
+        double *sg = rs + kHelpMaxOwn * kDT * KB;
+        const int64_t rseg = r0 - (int64_t)kLookC * kDT;
+        for (int idx = t; idx < kDT * kSeg; idx += kTrsvThreads) {
+            const int q = idx / kSeg, R = idx % kSeg;
+            sg[q * kLdN + R] = (q < nr && rseg + R >= 0) ? a.L[(rseg + R) + (r0 + q) * a.ldl] : 0.0;
+        }
         __syncthreads();
-        double *mx = a.MX + (int64_t)tb * 2 * kDT * kDT;
+        double *mx = a.MX + (int64_t)tb * kMXStride;
         for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
             const int m = idx / kDT, j = idx % kDT;  // M(j, m) = sum_q X(q, j) L(m, q)
             double s0 = 0.0, s1 = 0.0;
@@ -599,8 +631,18 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                 s0 = fma(Xs[q * kLdT + j], Lb[q * kLdT + m], s0);
                 s1 = fma(Xs[(q + 1) * kLdT + j], Lb[(q + 1) * kLdT + m], s1);
             }
-            mx[m * kDT + j] = s0 + s1;                        // M^T row-major: (m, j)
-            mx[kDT * kDT + m * kDT + j] = Xs[m * kLdT + j];   // X row-major: (q=m, j)
+            mx[kMXN + m * kDT + j] = s0 + s1;                        // M^T row-major: (m, j)
+            mx[kMXN + kDT * kDT + m * kDT + j] = Xs[m * kLdT + j];   // X row-major: (q=m, j)
+        }
+        for (int idx = t; idx < kDT * kSeg; idx += kTrsvThreads) {
+            const int j = idx / kSeg, R = idx % kSeg;  // N(j, R) = sum_q X(q, j) L(rs + R, q)
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+            for (int q = 0; q < kDT; q += 2) {
+                s0 = fma(Xs[q * kLdT + j], sg[q * kLdN + R], s0);
+                s1 = fma(Xs[(q + 1) * kLdT + j], sg[(q + 1) * kLdN + R], s1);
+            }
+            mx[j * kLdN + R] = s0 + s1;
         }
         cta_publish(a.lflag + tb, a.epoch);
     }
@@ -662,7 +704,6 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
     const int warp = t >> 5, lane = t & 31;
     if (warp == kHelpCompute / 32) {
         // ------------------------------------------------------------ feeder
-        int known = 0;
         int seq = 0;
         for (It it{0, first_owned_after(0)}; valid(it); advance(it), ++seq) {
             const int slot = seq % kHelpRing, use = seq / kHelpRing;
@@ -678,42 +719,33 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                 if (lane == 0) mbar_arrive(full + slot);
                 continue;
             }
-            if (it.tb >= known) {  // wait until every chain has published block tb
-                unsigned mm;
-                for (;;) {
-                    unsigned cnt = 0xffffffffu;
-                    if (lane < a.NC) {
-                        const unsigned long long v = ld_poll64(a.prog + lane * kProgStride);
-                        cnt = (unsigned)(v >> 32) == a.epoch ? (unsigned)v : 0u;
-                    }
-                    mm = __reduce_min_sync(kFull, cnt);
-                    if ((int)mm > it.tb) {
-#if GCM_POLL_RELAXED
-                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#endif
-                        break;
-                    }
-                    __nanosleep(GCM_POLL_NS);
-                }
-                known = (int)mm;
+            if (GCM_FEEDER_POLL && lane < a.NC) {  // wait until each chain's last row of P_tb is visible (the data itself,
+                                // no progress word), so the bulk copy below rarely brings empties
+                const double *q = a.pfast + ((int64_t)it.tb * kDT + kDT - 1) * k + min(k - 1, kRPC * lane + 1);
+                while (ld_relaxed_u64(q) == kEmpty) __nanosleep(GCM_POLL_NS);
             }
             __syncwarp();
-            if (lane == 0) {  // P_tb (32 x k, contiguous) with one bulk copy
-                asm volatile("fence.proxy.async.global;" ::: "memory");  // chains' generic stores -> bulk read
+            if (lane == 0) {  // P_tb (32 x k, contiguous) from pfast with one bulk copy; values still
+                              // empty on arrival are polled by the compute warps
+                asm volatile("fence.proxy.async.global;" ::: "memory");
                 const unsigned bytes = (unsigned)(kDT * k) * 8u;
                 mbar_arrive_expect_tx(full + slot, bytes);
-                bulk_g2s(stg + kDT * kLdT, a.P + (int64_t)it.tb * kDT * k, bytes, full + slot);
+                bulk_g2s(stg + kDT * kLdT, a.pfast + (int64_t)it.tb * kDT * k, bytes, full + slot);
             }
         }
         cp_async_wait_all();
-        return;
+        return full;
     }
     // ---------------------------------------------------------------- compute warps
     int seq = 0;
     for (It pit{0, first_owned_after(0)}; valid(pit); advance(pit), ++seq) {
         const int tb = pit.tb;
         const int slot = seq % kHelpRing;
+        HPT(0, clock64());
         mbar_wait(full + slot, (unsigned)((seq / kHelpRing) & 1));
+        HPT(1, clock64());
+        HPT(6, (long long)pit.tb);
+        HPT(7, (long long)(h + pit.ii * H));
         if (t == 0 && pit.tb + 1 == h + pit.ii * H - kLookC) HTRACE(1, 3000 + h + pit.ii * H);
         const int ii = pit.ii;
         const int s = h + ii * H;
@@ -731,6 +763,31 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
         const bool chain_handoff = (tb + 1 == s - kLookC);
         const int b64 = (tb + 1) / 2, s64 = s / 2;
         const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 & (a.CI - 1)) == 0;
+        if (!fast_tile(tb, s)) {  // bulk-copied P_tb: poll the values that were still empty
+            double *Pw = const_cast<double *>(Pt);
+            const double *src = a.pfast + (int64_t)tb * kDT * k;
+            constexpr int kPerV = (kDT * KB + kHelpCompute - 1) / kHelpCompute;
+            unsigned long long u[kPerV];
+            unsigned miss = 0u;
+#pragma unroll
+            for (int q = 0; q < kPerV; ++q) {  // every missing value's load in flight at once
+                const int o = t + q * kHelpCompute;
+                u[q] = 0ull;
+                if (o < kDT * k && __double_as_longlong(Pw[o]) == (long long)kEmpty) {
+                    u[q] = ld_relaxed_u64(src + o);
+                    miss |= 1u << q;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kPerV; ++q) {
+                if (miss >> q & 1u) {
+                    const int o = t + q * kHelpCompute;
+                    if (u[q] == kEmpty) u[q] = (unsigned long long)__double_as_longlong(ld_value(src + o));
+                    Pw[o] = __longlong_as_double((long long)u[q]);
+                }
+            }
+            named_bar(1, kHelpCompute);
+        }
         if (fast_tile(tb, s)) {  // P_tb straight from the chains' self-validating copy
             double *Pw = const_cast<double *>(Pt);
             const double *src = a.pfast + (int64_t)tb * kDT * k;
@@ -753,6 +810,7 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             named_bar(1, kHelpCompute);
             if (t == 0 && chain_handoff) HTRACE(3, 3000 + s);
         }
+        HPT(2, clock64());
         constexpr int EG = KB / 2;
         constexpr int kGemmT = 16 * EG;
         static_assert(kGemmT <= kHelpCompute, "helper GEMM threads");
@@ -795,6 +853,7 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
             const double s10 = (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]);
             const double s11 = (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]);
             const double sv[2][2] = {{s00, s01}, {s10, s11}};
+            HPT(3, clock64());
             if (t == 0 && chain_handoff) HTRACE(4, 3000 + s);
             double vout[2][2];
 #pragma unroll
@@ -843,9 +902,11 @@ __device__ void trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
                 st_release(a.qflag + tb, a.epoch);
             }
         }
+        HPT(4, clock64());
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + slot);
     }
+    return full;
 }
 
 // U^{-1} for U = chol_lower(A), A a KB x KB SPD matrix, in one warp: Gaussian elimination
@@ -884,7 +945,9 @@ __device__ __forceinline__ void warp_chol_inv(double (&a)[KB], double *out) {
 // prefix G_b at every 64-row boundary, and the other warps turn each G_b into
 // U_b^{-1} (chol_lower(I + sigma G_b), inverted) -- so the diagonal sweeps and the
 // Apply tiles find U_b^{-1} ready when the solve ends (no Gram/scan kernels).
-__host__ __device__ constexpr bool gram_chol_here(int KB) { return KB <= 16; }
+// U_b^{-1} is formed by the diagonal sweep's coefficient warp (in parallel over blocks, while
+// the column threads form w); one Gram-CTA warp per block could not keep pace with the chains.
+__host__ __device__ constexpr bool gram_chol_here(int KB) { return false; }
 
 template <int KB>
 __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
@@ -896,6 +959,10 @@ __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
     if (t == 0) *gready = 0;
     for (int o = t; o < KB * KB; o += blockDim.x) a.Ui[o] = (o / KB == o % KB) ? 1.0 : 0.0;  // U_0 = I
     __syncthreads();
+    if (t == 0) {
+        __threadfence();
+        st_release(a.uflag, a.epoch);
+    }
     if (warp < kAccT / 32) {
         // prefix sums of the helpers' per-block Grams Q_tb (thread t owns entries t + 128u)
         constexpr int EPB = (KB * KB + kAccT - 1) / kAccT;
@@ -924,6 +991,10 @@ __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
                 if (t == 0) {
                     __threadfence_block();
                     *gready = bn;
+                    if (!gram_chol_here(KB)) {  // the sweep inverts G_b itself
+                        __threadfence();
+                        st_release(a.uflag + bn, a.epoch);
+                    }
                 }
             }
         }
@@ -936,8 +1007,8 @@ __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
     const double sg = a.sigma > 0 ? 1.0 : -1.0;
     for (int bn = 1 + cw; bn < NB; bn += nw) {
         if (lane == 0)
-            while (*gready < bn) {
-            }
+            while (*gready < bn) __nanosleep(256);  // a tight spin would flood the MIO queue the
+                                                     // computing warp's shuffles go through
         __syncwarp();
         __threadfence_block();
 #ifdef GCM_SWEEP_TRACE
@@ -949,37 +1020,29 @@ __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
         for (int j = 0; j < KB; ++j)
             row[j] = (lane < k && j < k) ? (lane == j ? 1.0 : 0.0) + sg * Gb[lane * KB + j] : (lane == j ? 1.0 : 0.0);
         warp_chol_inv<KB>(row, a.Ui + (int64_t)bn * KB * KB);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            st_release(a.uflag + bn, a.epoch);
+        }
 #ifdef GCM_SWEEP_TRACE
         if (lane == 0 && bn < 500) gcm_sweep_trace[1024 + bn] = clock64();
 #endif
     }
 }
 
-template <int KB>
-__global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_constant__ TrsvArgs a) {
-    extern __shared__ __align__(128) double smem_trsv[];
-    if ((int)blockIdx.x < a.NC)
-        trsv_chain(a, smem_trsv, blockIdx.x);
-    else if ((int)blockIdx.x == a.NC) {
-#ifndef GCM_NO_GRAM
-        trsv_gram<KB>(a, smem_trsv);
-#endif
-    }
-    else
-        trsv_helper<KB>(a, smem_trsv, blockIdx.x - a.NC - 1, gridDim.x - a.NC - 1);
-}
 
 // One CTA per 64-row diagonal block, all blocks in parallel.
 constexpr int kDiagNQ = 4;                        // threads per column in the diagonal sweep
 constexpr int kDiagThreads = kDiagNQ * kD + 32;  // column parts + the coefficient warp
 
+// The sweep of diagonal block b by one CTA of kDiagThreads threads (a bdiag_kernel CTA,
+// or a TRSV helper in worker mode: then P is read from the self-validating copy).
 template <int KB>
-__global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict__ L, int64_t n, int64_t ldl,
-                                                   double *__restrict__ V, int k, int sigma,
-                                                   const double *__restrict__ P, double *__restrict__ Ui,
-                                                   const double *__restrict__ G, double *__restrict__ panels,
-                                                   unsigned long long *key, int64_t ebase) {
-    extern __shared__ double smem_bdiag[];
+__device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, double *__restrict__ V, int k, int sigma,
+                           const double *__restrict__ P, bool p_poll, double *__restrict__ Ui,
+                           const double *__restrict__ G, double *__restrict__ panels, unsigned long long *key,
+                           int64_t ebase, int b, double *smem_bdiag) {
     double(*Ls)[kD + 1] = reinterpret_cast<double(*)[kD + 1]>(smem_bdiag);               // [kD][kD+1]
     double(*Ps)[KB + 1] = reinterpret_cast<double(*)[KB + 1]>(smem_bdiag + kD * (kD + 1)); // [kD][KB+1]
     double(*M)[KB + 1] = reinterpret_cast<double(*)[KB + 1]>(smem_bdiag + kD * (kD + 1) + kD * (KB + 1));
@@ -991,7 +1054,6 @@ __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict_
     double *imx = vt + kD * KB;
     double *Vs = imx + kD * KB;
     const int t = threadIdx.x;
-    const int b = blockIdx.x;
     const int64_t r0 = (int64_t)b * kD;
     const int Db = (int)imin64(kD, n - r0);
 #ifdef GCM_SWEEP_TRACE
@@ -1009,7 +1071,7 @@ __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict_
     }
     for (int o = t; o < kD * k; o += kDiagThreads) {
         const int m = o / k, e = o % k;
-        Ps[m][e] = m < Db ? P[(r0 + m) * k + e] : 0.0;
+        Ps[m][e] = m < Db ? (p_poll ? ld_value(P + (r0 + m) * k + e) : P[(r0 + m) * k + e]) : 0.0;
     }
     __syncthreads();
 #ifdef GCM_SWEEP_TRACE
@@ -1080,6 +1142,77 @@ __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict_
     for (int idx = t; idx < kD * kD; idx += kDiagThreads) {
         const int m = idx / kD, j = idx % kD;
         if (m < Db && j <= m) L[(r0 + j) + (r0 + m) * ldl] = Ls[m][j];
+    }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict__ L, int64_t n, int64_t ldl,
+                                                   double *__restrict__ V, int k, int sigma,
+                                                   const double *__restrict__ P, double *__restrict__ Ui,
+                                                   const double *__restrict__ G, double *__restrict__ panels,
+                                                   unsigned long long *key, int64_t ebase) {
+    extern __shared__ double smem_bdiag[];
+    bdiag_body<KB>(L, n, ldl, V, k, sigma, P, false, Ui, G, panels, key, ebase, blockIdx.x, smem_bdiag);
+}
+
+// ---------------------------------------------------------------- worker mode
+// A helper whose strips are all done takes tickets for the diagonal sweeps (block b =
+// ticket, so every sweep waits only on the chains, the Gram CTA and strip owners --
+// never on a later ticket): block b needs U_b^{-1} (or G_b for KB = 32) from the Gram
+// CTA and the owner of strip 2b+1 past its last tile (2b, 2b+1), the only other reader
+// of L_bb; P_b is polled from the self-validating copy.
+static_assert(kDiagThreads == kTrsvThreads, "helpers run the diagonal sweep with all their threads");
+template <int KB>
+__device__ void trsv_worker(const TrsvArgs &a, double *smem, unsigned long long *ring_bars) {
+    __shared__ unsigned s_task;
+    const int t = threadIdx.x;
+    const int NB = (int)((a.n + kD - 1) / kD);
+    const int NT = (int)((a.n + kDT - 1) / kDT);
+    __syncthreads();
+    if (t < 2 * kHelpRing)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(ring_bars + t)) : "memory");
+    for (;;) {
+        __syncthreads();
+        if (t == 0) s_task = atomicAdd(a.taskctr, 1u) + 1u;  // armed to all-ones: first ticket 0
+        __syncthreads();
+        const unsigned task = s_task;
+        if (task >= (unsigned)NB || !a.fuse) break;
+        const int b = (int)task;
+        if (t == 0) {
+#ifdef GCM_TRACE
+            g_htrace[(1000 + b) * 8 + 0] = gtime();
+            g_htrace[(1000 + b) * 8 + 3] = blockIdx.x;
+#endif
+            while (ld_acquire(a.uflag + b) != a.epoch) __nanosleep(64);
+#ifdef GCM_TRACE
+            g_htrace[(1000 + b) * 8 + 4] = gtime();
+#endif
+            if (2 * b + 1 < NT)
+                while (ld_acquire(a.qflag + 2 * b) != a.epoch) __nanosleep(64);
+#ifdef GCM_TRACE
+            g_htrace[(1000 + b) * 8 + 1] = gtime();
+#endif
+        }
+        __syncthreads();
+        bdiag_body<KB>(const_cast<double *>(a.L), a.n, a.ldl, a.Vw, a.k, a.sigma, a.pfast, true, a.Ui, a.G,
+                       a.panels, a.key, a.ebase, b, smem);
+#ifdef GCM_TRACE
+        __syncthreads();
+        if (t == 0) g_htrace[(1000 + b) * 8 + 2] = gtime();
+#endif
+    }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_constant__ TrsvArgs a) {
+    extern __shared__ __align__(128) double smem_trsv[];
+    if ((int)blockIdx.x < a.NC)
+        trsv_chain(a, smem_trsv, blockIdx.x);
+    else if ((int)blockIdx.x == a.NC) {
+        trsv_gram<KB>(a, smem_trsv);
+    } else {
+        unsigned long long *bars = trsv_helper<KB>(a, smem_trsv, blockIdx.x - a.NC - 1, gridDim.x - a.NC - 1);
+        trsv_worker<KB>(a, smem_trsv, bars);
     }
 }
 
@@ -1470,9 +1603,6 @@ bool encode_tmap(CUtensorMap *m, const double *L, int64_t n, int64_t ldl, unsign
               CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-bool encode_tmap_L(CUtensorMap *m, const double *L, int64_t n, int64_t ldl) {
-    return encode_tmap(m, L, n, ldl, (unsigned)kSeg, (unsigned)kDT, CU_TENSOR_MAP_SWIZZLE_NONE);
-}
 
 template <int KB>
 gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, int sigma, unsigned long long *key,
@@ -1488,8 +1618,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.rchain = reinterpret_cast<double *>(wsbase + lay.rchain);
     a.pfast = reinterpret_cast<double *>(wsbase + lay.pfast);
     a.MX = reinterpret_cast<double *>(wsbase + lay.MX);
-    a.bulk_ok = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0) && n <= 0x7fffffff &&
-                encode_tmap_L(&a.tmapL, L, n, ldl);
+    a.bulk_ok = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0) && n <= 0x7fffffff;
     a.chk = reinterpret_cast<double *>(wsbase + lay.chk);
     a.CI = lay.CI;
     a.CIlog = 0;
@@ -1502,6 +1631,15 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.epoch = epoch;
 
     a.NC = (k + kRPC - 1) / kRPC;
+    a.Vw = V;
+    a.panels = reinterpret_cast<double *>(wsbase + lay.panels);
+    a.key = key;
+    a.ebase = ebase;
+    a.uflag = a.qflag + lay.NT;
+    a.taskctr = reinterpret_cast<unsigned *>(a.pfast + (size_t)lay.NT * kDT * k);
+    // KB = 32: helper tiles are twice as long and the sweep (95 ticks) twice as deep, so
+    // fused sweeps slow the chain's helpers more than they save; they run after the solve
+    a.fuse = KB <= 16;
     a.G = reinterpret_cast<double *>(wsbase + lay.G);
     a.Ui = reinterpret_cast<double *>(wsbase + lay.U);
     a.sigma = sigma;
@@ -1513,7 +1651,10 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     const size_t smem_help = (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + kHelpMaxOwn * kDT * KB +
                                       kHelpRing * (kDT * kLdT + kDT * (KB + 1)) + 2 * kHelpRing) *
                              sizeof(double);
-    const size_t smem = std::max(smem_chain, smem_help);
+    const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 +
+                                      4 * kD * KB + kD) *
+                             sizeof(double);
+    const size_t smem = std::max(std::max(smem_chain, smem_help), smem_diag);
     st = check_cuda(cudaFuncSetAttribute(trsv_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (st != GCM_OK) return st;
     int per_sm = 0;
@@ -1524,8 +1665,8 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (grid <= a.NC + 1) return GCM_ECUDA;
     void *args[] = {&a};
     // hand-off slots start empty (all-ones); consumers re-arm what they read
-    st = check_cuda(cudaMemsetAsync(a.rchain, 0xff, lay.pfast - lay.rchain + (size_t)lay.NT * kDT * k * sizeof(double),
-                                    stream));
+    st = check_cuda(cudaMemsetAsync(a.rchain, 0xff,
+                                    lay.pfast - lay.rchain + ((size_t)lay.NT * kDT * k + 1) * sizeof(double), stream));
     if (st != GCM_OK) return st;
     {
         ProfScope ps("trsv", stream);
@@ -1536,15 +1677,13 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
 
     double *U = reinterpret_cast<double *>(wsbase + lay.U);
     double *panels = reinterpret_cast<double *>(wsbase + lay.panels);
-    const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 +
-                                      4 * kD * KB + kD) *
-                             sizeof(double);
-    st = check_cuda(cudaFuncSetAttribute(bdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_diag));
-    if (st != GCM_OK) return st;
-    {
+    if (!a.fuse) {  // else the diagonal sweeps ran inside trsv_kernel (worker mode)
+        st = check_cuda(
+            cudaFuncSetAttribute(bdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_diag));
+        if (st != GCM_OK) return st;
         ProfScope ps("bdiag", stream);
-        bdiag_kernel<KB><<<lay.NB, kDiagThreads, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, U, a.G, panels, key,
-                                                                      ebase);
+        bdiag_kernel<KB><<<lay.NB, kDiagThreads, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, U, a.G, panels,
+                                                                      key, ebase);
     }
     if (lay.NB > 1) {
         const size_t smem_apply = (size_t)(2 * kD * KB + kD + KB + KB * KB + 2 * kD * kLdC) * sizeof(double);

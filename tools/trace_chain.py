@@ -45,3 +45,27 @@ print(f"  mean {step.mean():.0f} p90 {np.percentile(step, 90):.0f} max {step.max
 wait = np.array([h[s, 6] - reach[s] for s in rows])
 print(f"chain waits for the hand-off (seen - reached poll): median {np.median(wait):.0f} p90 {np.percentile(wait,90):.0f} ns")
 print(f"hand-off stored - chain reached poll: median {np.median([h[s,5]-reach[s] for s in rows]):.0f} ns (negative = stored before needed)")
+
+# chain CTA 0 phase timing (clock64 of one SM; needs GCM_TRACE): per step tb
+#  0 crit start  1 p stored  2 prep(tb+1) start  3 stage ready  4 partials done  5 hand-off read  6 prep done  7 loader issued
+cb = (ctypes.c_longlong * (4096 * 8))()
+lib.gcm_debug_trace(cb, 4096 * 8)
+ct = np.frombuffer(cb, dtype=np.int64).reshape(4096, 8).astype(np.float64)[12:NT - 2]
+print("chain CTA 0, cycles relative to crit start of the same step (median):")
+for i, nm in [(1, "p stored"), (2, "prep start"), (3, "stage ready"), (4, "partials done"), (5, "hand-off read"),
+              (6, "prep done")]:
+    print(f"  {nm:16s} {np.median(ct[:, i] - ct[:, 0]):8.0f}")
+print(f"  step (crit start to crit start) {np.median(np.diff(ct[:, 0])):.0f} cycles")
+
+# fused diagonal sweeps (worker mode): per block b, globaltimer ns relative to chain 0's first P store
+NB = (n + 63) // 64
+w = hall[1000:1000 + NB]
+t0 = h[12, 7]
+ok = w[:, 2] > 0
+if ok.any():
+    print("worker sweeps (us after chain span start): ticket / U ready / L free / done, CTA")
+    for b in list(range(0, NB, 8)) + [NB - 2, NB - 1]:
+        r = w[b]
+        print(f"  b={b:3d}  {(r[0]-t0)/1e3:8.1f} {(r[4]-t0)/1e3:8.1f} {(r[1]-t0)/1e3:8.1f} {(r[2]-t0)/1e3:8.1f}  cta {int(r[3])}")
+    dur = w[ok, 2] - w[ok, 1]
+    print(f"  sweep duration median {np.median(dur)/1e3:.1f} us, max {dur.max()/1e3:.1f}")
