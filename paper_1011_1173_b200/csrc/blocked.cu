@@ -70,6 +70,9 @@ constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per 
 #ifndef GCM_PUB_FENCE
 #define GCM_PUB_FENCE 1
 #endif
+#ifndef GCM_FUSE_APPLY
+#define GCM_FUSE_APPLY 0
+#endif
 #ifndef GCM_FEEDER_POLL
 #define GCM_FEEDER_POLL 1
 #endif
@@ -91,7 +94,7 @@ struct Layout {
     int k;
     int NT, NB, CI;
     int64_t nchk;
-    size_t P, rcur, rchain, pfast, MX, chk, G, Q, U, panels, flags, total;
+    size_t P, rcur, rchain, pfast, MX, chk, G, Q, U, panels, flags, hprog, total;
 };
 
 __host__ __device__ inline int64_t chk_count_before(int64_t s, int CI) {
@@ -141,8 +144,9 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
     l.Q = take((size_t)l.NT * kb_of(k) * kb_of(k));     // per 32-row block P_tb^T P_tb (helpers)
     l.U = take((size_t)l.NB * kb_of(k) * kb_of(k));       // U_b^{-1}, KB x KB, zero padded
     l.panels = take((size_t)l.NB * panel_doubles(kb_of(k)));  // coefficient panels, stride KB
-    l.flags = take(((2ull * l.NT + l.NB) * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
-                   8);  // prog[16 * kProgStride], lflag, qflag, uflag
+    l.flags = take(((2ull * l.NT + 2ull * l.NB) * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
+                   8);  // prog[16 * kProgStride], lflag, qflag, uflag, bflag
+    l.hprog = take((size_t)l.NT + 1);
     l.total = o;
     return l;
 }
@@ -277,6 +281,11 @@ struct TrsvArgs {
     unsigned *uflag;          // [NB] epoch when what block b's sweep needs from the Gram CTA is stored
     unsigned *taskctr;        // ticket counter (armed to all-ones by the pass's memset)
     int fuse;                 // 1: the diagonal sweeps run here (else bdiag_kernel after this kernel)
+    int fuse_apply;           // 1: so do the Apply tiles (needs fuse, CI = 1 and the TMA map tm2)
+    int H;                    // helper CTAs (strip s is owned by helper s % H)
+    unsigned *bflag;          // [NB] epoch when block b's sweep (panel, U_b^{-1}) is stored
+    unsigned long long *hprog;  // [H] (epoch << 32) | tile rows a helper has finished (published by its feeder)
+    CUtensorMap tm2;          // 8 x 256 boxes over L, 64B swizzle (the Apply tiles)
 };
 
 constexpr int kRPC = 2;                 // right-hand sides per chain CTA
@@ -704,10 +713,24 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
     const int warp = t >> 5, lane = t & 31;
     if (warp == kHelpCompute / 32) {
         // ------------------------------------------------------------ feeder
+        // progress for the fused Apply tiles: once a slot's previous tile is consumed, the
+        // tile rows it completed are published (a ring's lag behind the compute warps)
+        int slot_row[kHelpRing];
+#pragma unroll
+        for (int i = 0; i < kHelpRing; ++i) slot_row[i] = -1;
+        auto publish = [&](int rows) {
+            if (lane == 0) st_release64(a.hprog + h, ((unsigned long long)a.epoch << 32) | (unsigned)rows);
+        };
         int seq = 0;
         for (It it{0, first_owned_after(0)}; valid(it); advance(it), ++seq) {
             const int slot = seq % kHelpRing, use = seq / kHelpRing;
             if (use > 0) mbar_wait(empty + slot, (unsigned)((use - 1) & 1));
+#pragma unroll
+            for (int i = 0; i < kHelpRing; ++i)
+                if (i == slot) {
+                    if (use > 0 && slot_row[i] >= 0 && a.fuse_apply) publish(slot_row[i] + 1);
+                    slot_row[i] = it.ii == nown - 1 ? it.tb : -1;
+                }
             double *stg = ring + slot * kSlot;
             const int s = h + it.ii * H;
             const int64_t c0 = (int64_t)s * kDT;
@@ -734,6 +757,11 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
             }
         }
         cp_async_wait_all();
+        if (a.fuse_apply) {  // every tile consumed: all rows
+            for (int q = seq - kHelpRing > 0 ? seq - kHelpRing : 0; q < seq; ++q)
+                mbar_wait(empty + q % kHelpRing, (unsigned)((q / kHelpRing) & 1));
+            publish(NT);
+        }
         return full;
     }
     // ---------------------------------------------------------------- compute warps
@@ -1155,66 +1183,6 @@ __global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict_
     bdiag_body<KB>(L, n, ldl, V, k, sigma, P, false, Ui, G, panels, key, ebase, blockIdx.x, smem_bdiag);
 }
 
-// ---------------------------------------------------------------- worker mode
-// A helper whose strips are all done takes tickets for the diagonal sweeps (block b =
-// ticket, so every sweep waits only on the chains, the Gram CTA and strip owners --
-// never on a later ticket): block b needs U_b^{-1} (or G_b for KB = 32) from the Gram
-// CTA and the owner of strip 2b+1 past its last tile (2b, 2b+1), the only other reader
-// of L_bb; P_b is polled from the self-validating copy.
-static_assert(kDiagThreads == kTrsvThreads, "helpers run the diagonal sweep with all their threads");
-template <int KB>
-__device__ void trsv_worker(const TrsvArgs &a, double *smem, unsigned long long *ring_bars) {
-    __shared__ unsigned s_task;
-    const int t = threadIdx.x;
-    const int NB = (int)((a.n + kD - 1) / kD);
-    const int NT = (int)((a.n + kDT - 1) / kDT);
-    __syncthreads();
-    if (t < 2 * kHelpRing)
-        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(ring_bars + t)) : "memory");
-    for (;;) {
-        __syncthreads();
-        if (t == 0) s_task = atomicAdd(a.taskctr, 1u) + 1u;  // armed to all-ones: first ticket 0
-        __syncthreads();
-        const unsigned task = s_task;
-        if (task >= (unsigned)NB || !a.fuse) break;
-        const int b = (int)task;
-        if (t == 0) {
-#ifdef GCM_TRACE
-            g_htrace[(1000 + b) * 8 + 0] = gtime();
-            g_htrace[(1000 + b) * 8 + 3] = blockIdx.x;
-#endif
-            while (ld_acquire(a.uflag + b) != a.epoch) __nanosleep(64);
-#ifdef GCM_TRACE
-            g_htrace[(1000 + b) * 8 + 4] = gtime();
-#endif
-            if (2 * b + 1 < NT)
-                while (ld_acquire(a.qflag + 2 * b) != a.epoch) __nanosleep(64);
-#ifdef GCM_TRACE
-            g_htrace[(1000 + b) * 8 + 1] = gtime();
-#endif
-        }
-        __syncthreads();
-        bdiag_body<KB>(const_cast<double *>(a.L), a.n, a.ldl, a.Vw, a.k, a.sigma, a.pfast, true, a.Ui, a.G,
-                       a.panels, a.key, a.ebase, b, smem);
-#ifdef GCM_TRACE
-        __syncthreads();
-        if (t == 0) g_htrace[(1000 + b) * 8 + 2] = gtime();
-#endif
-    }
-}
-
-template <int KB>
-__global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_constant__ TrsvArgs a) {
-    extern __shared__ __align__(128) double smem_trsv[];
-    if ((int)blockIdx.x < a.NC)
-        trsv_chain(a, smem_trsv, blockIdx.x);
-    else if ((int)blockIdx.x == a.NC) {
-        trsv_gram<KB>(a, smem_trsv);
-    } else {
-        unsigned long long *bars = trsv_helper<KB>(a, smem_trsv, blockIdx.x - a.NC - 1, gridDim.x - a.NC - 1);
-        trsv_worker<KB>(a, smem_trsv, bars);
-    }
-}
 
 // One CTA per (checkpoint segment g, 64-column strip s): tiles b in
 // [g*CI, min(g*CI+CI, s)).  Thread = column; the tile streams through shared
@@ -1454,18 +1422,20 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, int c0, int 
                  : "memory");
 }
 
+// Apply of panel b to the 64 x 256 tile at 64-column strip s0 by threads 0..kT2Threads-1
+// (a btma_kernel CTA, or a TRSV helper in worker mode: then `bar` is a named barrier id
+// for those threads only; tm must be a __grid_constant__ parameter).
 template <int KB>
-__global__ void __launch_bounds__(kT2Threads, 2) btma_kernel(const __grid_constant__ CUtensorMap tm, int64_t n, int k,
-                                                              const double *__restrict__ chk,
-                                                              const double *__restrict__ Ui,
-                                                              const double *__restrict__ panels, int NB) {
+__device__ void btma_body(const CUtensorMap &tm, int64_t n, int k, const double *__restrict__ chk,
+                          const double *__restrict__ Ui, const double *__restrict__ panels, int NB, int b, int s0,
+                          unsigned char *smem_t2, int bar) {
     constexpr int C = t2_cols_per_thread(KB);
     constexpr int NBOX = C / 2;  // TMA boxes per chunk
     constexpr unsigned kStage = kT2BoxBytes * NBOX;
-    const int b = blockIdx.x;
-    const int s0 = b + 1 + t2_strips(KB) * blockIdx.y;
-    if (s0 >= NB) return;
-    extern __shared__ __align__(16) unsigned char smem_t2[];
+    auto sync = [&]() {
+        if (bar == 0) __syncthreads();
+        else named_bar(bar, kT2Threads);
+    };
     const unsigned sbase = smem_u32(smem_t2);
     unsigned char *st = smem_t2 + (((sbase + 1023u) & ~1023u) - sbase);  // swizzled boxes: 1 KB aligned
     double2 *cs = reinterpret_cast<double2 *>(st + kT2Stages * kStage);   // [kD][KB] (gamma, delta)
@@ -1485,7 +1455,7 @@ __global__ void __launch_bounds__(kT2Threads, 2) btma_kernel(const __grid_consta
         for (int i = 0; i <= kT2Stages; ++i) mbar_init(bars + i, 1u);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    sync();
     if (t == 0) {
         const unsigned pbytes = (unsigned)panel_doubles(KB) * 8u, ubytes = (unsigned)(KB * KB) * 8u;
         mbar_arrive_expect_tx(bars + kT2Stages, pbytes + ubytes);
@@ -1564,7 +1534,7 @@ __global__ void __launch_bounds__(kT2Threads, 2) btma_kernel(const __grid_consta
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> TMA store
-        __syncthreads();
+        sync();
         if (t == 0) {
 #pragma unroll
             for (int x = 0; x < NBOX; ++x) tma_store_2d(&tm, rb + ch * kT2Rows, col0 + x * kT2Box, buf + x * kT2BoxBytes);
@@ -1577,6 +1547,128 @@ __global__ void __launch_bounds__(kT2Threads, 2) btma_kernel(const __grid_consta
         }
     }
     if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    sync();  // the shared memory (and its mbarriers) may be reused by the caller
+    if (t <= kT2Stages) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bars + t)) : "memory");
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kT2Threads, 2) btma_kernel(const __grid_constant__ CUtensorMap tm, int64_t n, int k,
+                                                              const double *__restrict__ chk,
+                                                              const double *__restrict__ Ui,
+                                                              const double *__restrict__ panels, int NB) {
+    const int s0 = blockIdx.x + 1 + t2_strips(KB) * blockIdx.y;
+    if (s0 >= NB) return;
+    extern __shared__ __align__(16) unsigned char smem_t2[];
+    btma_body<KB>(tm, n, k, chk, Ui, panels, NB, blockIdx.x, s0, smem_t2, 0);
+}
+
+// ---------------------------------------------------------------- worker mode
+// A helper whose strips are all done takes tickets for the diagonal sweeps (block b =
+// ticket, so every sweep waits only on the chains, the Gram CTA and strip owners --
+// never on a later ticket): block b needs U_b^{-1} (or G_b for KB = 32) from the Gram
+// CTA and the owner of strip 2b+1 past its last tile (2b, 2b+1), the only other reader
+// of L_bb; P_b is polled from the self-validating copy.
+static_assert(kDiagThreads == kTrsvThreads, "helpers run the diagonal sweep with all their threads");
+template <int KB>
+__device__ void trsv_worker(const TrsvArgs &a, double *smem, unsigned long long *ring_bars) {
+    __shared__ unsigned s_task;
+    const int t = threadIdx.x;
+    const int NB = (int)((a.n + kD - 1) / kD);
+    const int NT = (int)((a.n + kDT - 1) / kDT);
+    __syncthreads();
+    if (t < 2 * kHelpRing)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(ring_bars + t)) : "memory");
+    constexpr int kGS = t2_strips(KB);  // 64-column strips per Apply tile
+    for (;;) {
+        __syncthreads();
+        if (t == 0) {
+            const unsigned task = atomicAdd(a.taskctr, 1u) + 1u;  // armed to all-ones: first ticket 0
+            // tickets: the NB sweeps first (block order; they sit on the critical path), then the
+            // Apply tiles (b, g) in block order -- an Apply tile only waits on a sweep already handed out
+            int bb = 0, gg = -1;
+            if (task < (unsigned)NB) {
+                bb = (int)task;
+            } else {
+                unsigned o = NB;
+                for (; bb < NB; ++bb) {
+                    const unsigned cnt = a.fuse_apply ? (unsigned)((NB - 1 - bb + kGS - 1) / kGS) : 0u;
+                    if (task < o + cnt) {
+                        gg = (int)(task - o);
+                        break;
+                    }
+                    o += cnt;
+                }
+            }
+            s_task = bb < NB && a.fuse ? (unsigned)bb | ((unsigned)(gg + 1) << 16) : 0xffffffffu;
+        }
+        __syncthreads();
+        const unsigned task = s_task;
+        if (task == 0xffffffffu) break;
+        const int b = (int)(task & 0xffff), g = (int)(task >> 16) - 1;
+        if (g < 0) {  // the diagonal sweep of block b
+            if (t == 0) {
+#ifdef GCM_TRACE
+                g_htrace[(1000 + b) * 8 + 0] = gtime();
+                g_htrace[(1000 + b) * 8 + 3] = blockIdx.x;
+#endif
+                while (ld_acquire(a.uflag + b) != a.epoch) __nanosleep(64);
+#ifdef GCM_TRACE
+                g_htrace[(1000 + b) * 8 + 4] = gtime();
+#endif
+                if (2 * b + 1 < NT)
+                    while (ld_acquire(a.qflag + 2 * b) != a.epoch) __nanosleep(64);
+#ifdef GCM_TRACE
+                g_htrace[(1000 + b) * 8 + 1] = gtime();
+#endif
+            }
+            __syncthreads();
+            bdiag_body<KB>(const_cast<double *>(a.L), a.n, a.ldl, a.Vw, a.k, a.sigma, a.pfast, true, a.Ui, a.G,
+                           a.panels, a.key, a.ebase, b, smem);
+            __syncthreads();
+            if (t == 0) {
+#ifdef GCM_TRACE
+                g_htrace[(1000 + b) * 8 + 2] = gtime();
+#endif
+                if (a.fuse_apply) {
+                    __threadfence();
+                    st_release(a.bflag + b, a.epoch);
+                }
+            }
+        } else {  // Apply tile (b, 64-column strips s0 .. s0 + kGS - 1)
+            const int s0 = b + 1 + kGS * g;
+            if (t == 0) {
+                while (ld_acquire(a.bflag + b) != a.epoch) __nanosleep(128);
+                const int slo = 2 * s0, shi = min(NT, 2 * (s0 + kGS));
+                for (int s32 = slo; s32 < shi; ++s32) {  // owners past tile rows 2b, 2b+1 (checkpoint + L reads)
+                    const unsigned long long *hp = a.hprog + s32 % a.H;
+                    for (;;) {
+                        const unsigned long long v = ld_acquire64(hp);
+                        if ((unsigned)(v >> 32) == a.epoch && (int)(unsigned)v >= 2 * b + 2) break;
+                        __nanosleep(128);
+                    }
+                }
+                for (int tb = 2 * b + 2; tb <= min(NT - 1, 2 * b + 1 + kLookC); ++tb)  // J1 reads of rows of block b
+                    while (ld_acquire(a.lflag + tb) != a.epoch) __nanosleep(64);
+            }
+            __syncthreads();
+            if (t < kT2Threads)
+                btma_body<KB>(a.tm2, a.n, a.k, a.chk, a.Ui, a.panels, NB, b, s0,
+                              reinterpret_cast<unsigned char *>(smem), 3);
+        }
+    }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_constant__ TrsvArgs a) {
+    extern __shared__ __align__(128) double smem_trsv[];
+    if ((int)blockIdx.x < a.NC)
+        trsv_chain(a, smem_trsv, blockIdx.x);
+    else if ((int)blockIdx.x == a.NC) {
+        trsv_gram<KB>(a, smem_trsv);
+    } else {
+        unsigned long long *bars = trsv_helper<KB>(a, smem_trsv, blockIdx.x - a.NC - 1, gridDim.x - a.NC - 1);
+        trsv_worker<KB>(a, smem_trsv, bars);
+    }
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
@@ -1640,6 +1732,13 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     // KB = 32: helper tiles are twice as long and the sweep (95 ticks) twice as deep, so
     // fused sweeps slow the chain's helpers more than they save; they run after the solve
     a.fuse = KB <= 16;
+    a.bflag = a.uflag + lay.NB;
+    a.hprog = reinterpret_cast<unsigned long long *>(wsbase + lay.hprog);
+    // Fused Apply tiles (GCM_FUSE_APPLY=1) are correct but measured slower (0.52 vs 0.43 ms at
+    // n=5000, k=16): their 200 MB stream competes with the helpers' latency-bound tile loads
+    // and stretches the chain by half; by default the Apply runs as btma_kernel afterwards.
+    a.fuse_apply = GCM_FUSE_APPLY && a.fuse && lay.NB > 1 && lay.CI == 1 && a.bulk_ok &&
+                   encode_tmap(&a.tm2, L, n, ldl, (unsigned)kT2Rows, (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B);
     a.G = reinterpret_cast<double *>(wsbase + lay.G);
     a.Ui = reinterpret_cast<double *>(wsbase + lay.U);
     a.sigma = sigma;
@@ -1654,7 +1753,8 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 +
                                       4 * kD * KB + kD) *
                              sizeof(double);
-    const size_t smem = std::max(std::max(smem_chain, smem_help), smem_diag);
+    size_t smem = std::max(std::max(smem_chain, smem_help), smem_diag);
+    if (a.fuse_apply) smem = std::max(smem, t2_smem_bytes(KB));
     st = check_cuda(cudaFuncSetAttribute(trsv_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (st != GCM_OK) return st;
     int per_sm = 0;
@@ -1663,6 +1763,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (per_sm < 1) return GCM_ECUDA;
     const int grid = (int)std::min<int64_t>((int64_t)nsm * per_sm, a.NC + 1 + lay.NT);
     if (grid <= a.NC + 1) return GCM_ECUDA;
+    a.H = grid - a.NC - 1;
     void *args[] = {&a};
     // hand-off slots start empty (all-ones); consumers re-arm what they read
     st = check_cuda(cudaMemsetAsync(a.rchain, 0xff,
@@ -1685,7 +1786,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
         bdiag_kernel<KB><<<lay.NB, kDiagThreads, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, U, a.G, panels,
                                                                       key, ebase);
     }
-    if (lay.NB > 1) {
+    if (lay.NB > 1 && !a.fuse_apply) {
         const size_t smem_apply = (size_t)(2 * kD * KB + kD + KB + KB * KB + 2 * kD * kLdC) * sizeof(double);
         st = check_cuda(
             cudaFuncSetAttribute(bapply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_apply));
