@@ -10,7 +10,8 @@ the same V so the factor stays bounded; V is restored from a pristine copy and
 L2 is flushed (256 MiB write) between steps, outside the timed events.
 
 Configs (BASELINE.json): "n5000_k16" (default, configs[1]: the metric's config),
-"n5000_k1" / "n5000_k4" / "n5000_k64" (configs[2] sweep), "batched" (configs[4]:
+"n5000_k1" / "n5000_k4" / "n5000_k64" (configs[2] sweep), "n100000_k32" (configs[3] at one
+GPU: 80 GB factor drawn on the device, column-norm pin at full size), "batched" (configs[4]:
 4096 factors n=512, k=8; weak-sharded over ranks).
 
 --impl reference times the CPU oracle (oracle/, plain serial C) on the same
@@ -45,6 +46,9 @@ CONFIGS = {
     "n5000_k4": dict(n=5000, k=4),
     "n5000_k64": dict(n=5000, k=64),
     "batched": dict(n=512, k=8, batch=4096),
+    # BASELINE configs[3] at one GPU: 80 GB factor, direct-L construction generated on the
+    # device (R18), checked by the column-norm identity at full size
+    "n100000_k32": dict(n=100000, k=32, direct=True),
 }
 
 
@@ -172,7 +176,17 @@ def run_ours(args, world, rank, local):
     batch = cfg.get("batch", 1)
     stream = torch.cuda.current_stream(dev)
 
-    if batch == 1:
+    if cfg.get("direct"):
+        # direct-L instance (R18) drawn on the device with torch's seeded Philox
+        # generator: L_ii ~ U[1,2), L_ij ~ (2U-1)/sqrt(n), V ~ U/sqrt(n); update then downdate
+        g = torch.Generator(device=dev)
+        g.manual_seed(synth.SEED_ROOT + rank)
+        L = torch.empty((n, n), dtype=torch.float64, device=dev)
+        L.uniform_(-1.0 / n ** 0.5, 1.0 / n ** 0.5, generator=g)
+        L.diagonal().uniform_(1.0, 2.0, generator=g)
+        V0 = torch.rand((k, n), dtype=torch.float64, device=dev, generator=g) / n ** 0.5
+        Lbuf = Vbuf = None
+    elif batch == 1:
         Lbuf, Vbuf, _ = synth.paper_instance(n, k, +1, seed=synth.SEED_ROOT + rank)
         L = torch.from_numpy(Lbuf).to(dev)
         V0 = torch.from_numpy(Vbuf).to(dev)
@@ -220,6 +234,21 @@ def run_ours(args, world, rank, local):
     gcm.profile_enable(False)
     prof = gcm.profile_read()
     clk = clocks.stop(first_sample)
+    check = None
+    if cfg.get("direct"):
+        # full-size property pin: ||L~_{:,c}||^2 = ||L_{:,c}||^2 + sigma ||V_{c,:}||^2
+        # on 256 sampled columns, one more (untimed) update
+        cols = torch.randperm(n, device=dev, generator=torch.Generator(device=dev).manual_seed(7))[:256]
+        mask = torch.arange(n, device=dev)[None, :] <= cols[:, None]
+        before = ((L[cols] * mask) ** 2).sum(1)
+        V.copy_(V0)
+        vnorm = (V0[:, cols] ** 2).sum(0)
+        call(+1)
+        torch.cuda.synchronize()
+        after = ((L[cols] * mask) ** 2).sum(1)
+        rel = ((after - before - vnorm).abs() / after).max().item()
+        check = {"pin": "column-norm identity on 256 sampled columns (SURVEY 8(c) P4)",
+                 "max_rel_err": rel, "ok": rel <= 1e-11}
 
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = max_over_ranks(sum(step_ms), world)
@@ -260,12 +289,16 @@ def run_ours(args, world, rank, local):
                    "n": n, "k": k, "batch_per_gpu": batch, "algo": args.algo if batch == 1 else "batched",
                    "sigma": "alternating +1/-1 by the same V", "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"replicas x{world}" if batch == 1 else f"factor-sharded x{world}",
-                   "instance": "paper construction (PAPER.md 111): B,V ~ U[0,1), A = B^T B + I, seed 10111173+rank"},
+                   "instance": ("direct-L (DESIGN.md R18) on the device, torch Philox seed 10111173+rank"
+                                if cfg.get("direct") else
+                                "paper construction (PAPER.md 111): B,V ~ U[0,1), A = B^T B + I, seed 10111173+rank")},
         "roofline": roofline, "roofline_path": roofline_path, "gpu_launches": int(launches),
         "kernels": {kname: {"launches": c, "ms_total": round(m, 4)} for kname, (c, m) in prof.items()},
         "clocks": clk, "wall_s": round(wall, 4),
     }
-    if rank == 0 and batch == 1 and not args.no_e2e:
+    if check is not None:
+        out["check"] = check
+    if rank == 0 and batch == 1 and not args.no_e2e and Lbuf is not None:
         out["e2e"] = run_e2e(gcm, torch, Lbuf, Vbuf, n, k, flops)
     if rank == 0 and not args.no_cpu:
         out["cpu_baseline"] = run_cpu_baseline(n, k)
@@ -342,7 +375,13 @@ def run_cpu_baseline(n, k, budget_s=20.0):
     import oracle
     import synth
     cores = 1  # the oracle is single-threaded by construction
-    Lbuf, Vbuf, _ = synth.paper_instance(n, k, +1, seed=synth.SEED_ROOT)
+    sample_note = ""
+    if n > 20000:  # bounded sample: the same construction at n = 4000 (the oracle is O(n^2 k) serial)
+        n = 4000
+        Lbuf, Vbuf = synth.direct_instance(n, k, seed=synth.SEED_ROOT)
+        sample_note = " (direct-L construction, leading-size sample of the n=100000 workload)"
+    else:
+        Lbuf, Vbuf, _ = synth.paper_instance(n, k, +1, seed=synth.SEED_ROOT)
     calls, t_tot = 0, 0.0
     while t_tot < budget_s and calls < 4:
         L = Lbuf.copy()
@@ -355,7 +394,7 @@ def run_cpu_baseline(n, k, budget_s=20.0):
             break
     _, flops, _ = algorithmic(n, k)
     return {"value": round(flops * calls / t_tot / 1e9, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
-            "sample": f"{calls} full oracle call(s) of n={n}, k={k} update ({t_tot:.2f} s)",
+            "sample": f"{calls} full oracle call(s) of n={n}, k={k} update ({t_tot:.2f} s){sample_note}",
             "ms_per_call": round(t_tot / calls * 1e3, 1)}
 
 

@@ -70,11 +70,17 @@ constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per 
 #ifndef GCM_PUB_FENCE
 #define GCM_PUB_FENCE 1
 #endif
+#ifndef GCM_FUSE_DIAG
+#define GCM_FUSE_DIAG 1
+#endif
+#ifndef GCM_GRAM_CHOL
+#define GCM_GRAM_CHOL 0
+#endif
 #ifndef GCM_FUSE_APPLY
 #define GCM_FUSE_APPLY 0
 #endif
 #ifndef GCM_FEEDER_POLL
-#define GCM_FEEDER_POLL 1
+#define GCM_FEEDER_POLL 0
 #endif
 #ifndef GCM_LATE_LOAD
 #define GCM_LATE_LOAD 0
@@ -975,7 +981,7 @@ __device__ __forceinline__ void warp_chol_inv(double (&a)[KB], double *out) {
 // Apply tiles find U_b^{-1} ready when the solve ends (no Gram/scan kernels).
 // U_b^{-1} is formed by the diagonal sweep's coefficient warp (in parallel over blocks, while
 // the column threads form w); one Gram-CTA warp per block could not keep pace with the chains.
-__host__ __device__ constexpr bool gram_chol_here(int KB) { return false; }
+__host__ __device__ constexpr bool gram_chol_here(int KB) { return GCM_GRAM_CHOL && KB <= 16; }
 
 template <int KB>
 __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
@@ -1731,7 +1737,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.taskctr = reinterpret_cast<unsigned *>(a.pfast + (size_t)lay.NT * kDT * k);
     // KB = 32: helper tiles are twice as long and the sweep (95 ticks) twice as deep, so
     // fused sweeps slow the chain's helpers more than they save; they run after the solve
-    a.fuse = KB <= 16;
+    a.fuse = GCM_FUSE_DIAG && KB <= 16;
     a.bflag = a.uflag + lay.NB;
     a.hprog = reinterpret_cast<unsigned long long *>(wsbase + lay.hprog);
     // Fused Apply tiles (GCM_FUSE_APPLY=1) are correct but measured slower (0.52 vs 0.43 ms at
