@@ -73,6 +73,9 @@ constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per 
 #ifndef GCM_FUSE_DIAG
 #define GCM_FUSE_DIAG 1
 #endif
+#ifndef GCM_FUSE_KB32
+#define GCM_FUSE_KB32 0
+#endif
 #ifndef GCM_GRAM_CHOL
 #define GCM_GRAM_CHOL 0
 #endif
@@ -709,6 +712,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
     double *ring = rs + kHelpMaxOwn * kDT * KB;  // [kHelpRing][kSlot]
     unsigned long long *full = reinterpret_cast<unsigned long long *>(ring + kHelpRing * kSlot);
     unsigned long long *empty = full + kHelpRing;
+    volatile int *pmode = reinterpret_cast<volatile int *>(empty + kHelpRing);  // [kHelpRing] 1: P not copied
     if (t == 0) {
         for (int i = 0; i < kHelpRing; ++i) {
             mbar_init(full + i, 33u);  // 1 noinc arrival per feeder lane (L batch) + the P bulk copy's arrive
@@ -727,7 +731,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
         auto publish = [&](int rows) {
             if (lane == 0) st_release64(a.hprog + h, ((unsigned long long)a.epoch << 32) | (unsigned)rows);
         };
-        int seq = 0;
+        int seq = 0, known = 0;
         for (It it{0, first_owned_after(0)}; valid(it); advance(it), ++seq) {
             const int slot = seq % kHelpRing, use = seq / kHelpRing;
             if (use > 0) mbar_wait(empty + slot, (unsigned)((use - 1) & 1));
@@ -748,12 +752,28 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
                 if (lane == 0) mbar_arrive(full + slot);
                 continue;
             }
-            if (GCM_FEEDER_POLL && lane < a.NC) {  // wait until each chain's last row of P_tb is visible (the data itself,
-                                // no progress word), so the bulk copy below rarely brings empties
+            if (GCM_FEEDER_POLL == 1 && lane < a.NC) {  // wait until each chain's last row of P_tb is visible
                 const double *q = a.pfast + ((int64_t)it.tb * kDT + kDT - 1) * k + min(k - 1, kRPC * lane + 1);
                 while (ld_relaxed_u64(q) == kEmpty) __nanosleep(GCM_POLL_NS);
             }
+            if (GCM_FEEDER_POLL == 2 && it.tb >= known) {
+                // one look (no waiting) at each chain's last row of P_tb: a block that is already
+                // out is bulk-copied (a helper catching up gets complete tiles); a fresh one is
+                // left to the compute warps, which poll pfast directly (one round trip after it lands)
+                unsigned long long u = 0ull;
+                if (lane < a.NC)
+                    u = ld_relaxed_u64(a.pfast + ((int64_t)it.tb * kDT + kDT - 1) * k + min(k - 1, kRPC * lane + 1));
+                if (__all_sync(kFull, u != kEmpty)) known = it.tb + 1;
+            }
             __syncwarp();
+            if (GCM_FEEDER_POLL == 2 && it.tb >= known) {
+                if (lane == 0) {
+                    pmode[slot] = 1;
+                    mbar_arrive(full + slot);
+                }
+                continue;
+            }
+            if (GCM_FEEDER_POLL == 2 && lane == 0) pmode[slot] = 0;
             if (lane == 0) {  // P_tb (32 x k, contiguous) from pfast with one bulk copy; values still
                               // empty on arrival are polled by the compute warps
                 asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -797,7 +817,8 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
         const bool chain_handoff = (tb + 1 == s - kLookC);
         const int b64 = (tb + 1) / 2, s64 = s / 2;
         const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 & (a.CI - 1)) == 0;
-        if (!fast_tile(tb, s)) {  // bulk-copied P_tb: poll the values that were still empty
+        const bool direct = fast_tile(tb, s) || (GCM_FEEDER_POLL == 2 && pmode[slot] == 1);
+        if (!direct) {  // bulk-copied P_tb: poll the values that were still empty
             double *Pw = const_cast<double *>(Pt);
             const double *src = a.pfast + (int64_t)tb * kDT * k;
             constexpr int kPerV = (kDT * KB + kHelpCompute - 1) / kHelpCompute;
@@ -822,7 +843,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
             }
             named_bar(1, kHelpCompute);
         }
-        if (fast_tile(tb, s)) {  // P_tb straight from the chains' self-validating copy
+        if (direct) {  // P_tb straight from the chains' self-validating copy
             double *Pw = const_cast<double *>(Pt);
             const double *src = a.pfast + (int64_t)tb * kDT * k;
             constexpr int kPer = (kDT * KB + kHelpCompute - 1) / kHelpCompute;
@@ -1099,13 +1120,38 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
     double *Uis = reinterpret_cast<double *>(M);  // [KB][KB] in the (KB x KB+1) slot
     if (gram_chol_here(KB))
         for (int o = t; o < KB * KB; o += kDiagThreads) Uis[o] = Ui[(int64_t)b * KB * KB + o];
-    for (int idx = t; idx < kD * kD; idx += kDiagThreads) {
-        const int m = idx / kD, j = idx % kD;
-        if (m < Db && j <= m) Ls[m][j] = L[(r0 + j) + (r0 + m) * ldl];
-    }
-    for (int o = t; o < kD * k; o += kDiagThreads) {
-        const int m = o / k, e = o % k;
-        Ps[m][e] = m < Db ? (p_poll ? ld_value(P + (r0 + m) * k + e) : P[(r0 + m) * k + e]) : 0.0;
+    {  // every load in flight before the first use (one memory latency, not one per element)
+        constexpr int kLI = (kD * kD + kDiagThreads - 1) / kDiagThreads;
+        double lv[kLI];
+#pragma unroll
+        for (int q = 0; q < kLI; ++q) {
+            const int idx = t + q * kDiagThreads, m = idx / kD, j = idx % kD;
+            lv[q] = (idx < kD * kD && m < Db && j <= m) ? L[(r0 + j) + (r0 + m) * ldl] : 0.0;
+        }
+        constexpr int kPI = (kD * KB + kDiagThreads - 1) / kDiagThreads;
+        unsigned long long pv[kPI];
+#pragma unroll
+        for (int q = 0; q < kPI; ++q) {
+            const int o = t + q * kDiagThreads, m = k > 0 ? o / k : 0;
+            pv[q] = 0ull;
+            if (o < kD * k && m < Db)
+                pv[q] = p_poll ? ld_relaxed_u64(P + (r0 + m) * k + o % k)
+                               : (unsigned long long)__double_as_longlong(P[(r0 + m) * k + o % k]);
+        }
+#pragma unroll
+        for (int q = 0; q < kLI; ++q) {
+            const int idx = t + q * kDiagThreads, m = idx / kD, j = idx % kD;
+            if (idx < kD * kD && m < Db && j <= m) Ls[m][j] = lv[q];
+        }
+#pragma unroll
+        for (int q = 0; q < kPI; ++q) {
+            const int o = t + q * kDiagThreads;
+            if (o < kD * k) {
+                const int m = o / k, e = o % k;
+                if (p_poll && m < Db && pv[q] == kEmpty) pv[q] = __double_as_longlong(ld_value(P + (r0 + m) * k + e));
+                Ps[m][e] = __longlong_as_double((long long)pv[q]);
+            }
+        }
     }
     __syncthreads();
 #ifdef GCM_SWEEP_TRACE
@@ -1157,7 +1203,9 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
         for (int i = 0; i < EPT; ++i) {
             const int e = cq * EPT + i;
             double acc = 0.0;
-            for (int ep = 0; ep <= e; ++ep) acc = fma(Uis[e * KB + ep], vt[cm * KB + ep], acc);
+#pragma unroll
+            for (int ep = 0; ep < KB; ++ep)  // U^{-1} lower triangular; vt past column k is scratch
+                if (ep <= e) acc = fma(Uis[e * KB + ep], vt[cm * KB + ep], acc);
             Vs[cm * KB + e] = (cm < Db && e < k) ? acc : 0.0;
         }
     }
@@ -1737,7 +1785,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.taskctr = reinterpret_cast<unsigned *>(a.pfast + (size_t)lay.NT * kDT * k);
     // KB = 32: helper tiles are twice as long and the sweep (95 ticks) twice as deep, so
     // fused sweeps slow the chain's helpers more than they save; they run after the solve
-    a.fuse = GCM_FUSE_DIAG && KB <= 16;
+    a.fuse = GCM_FUSE_DIAG && (KB <= 16 || GCM_FUSE_KB32);
     a.bflag = a.uflag + lay.NB;
     a.hprog = reinterpret_cast<unsigned long long *>(wsbase + lay.hprog);
     // Fused Apply tiles (GCM_FUSE_APPLY=1) are correct but measured slower (0.52 vs 0.43 ms at
@@ -1754,7 +1802,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (st != GCM_OK) return st;
     const size_t smem_chain = (size_t)ChainSmem::total * sizeof(double);
     const size_t smem_help = (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + kHelpMaxOwn * kDT * KB +
-                                      kHelpRing * (kDT * kLdT + kDT * (KB + 1)) + 2 * kHelpRing) *
+                                      kHelpRing * (kDT * kLdT + kDT * (KB + 1)) + 3 * kHelpRing) *
                              sizeof(double);
     const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 +
                                       4 * kD * KB + kD) *

@@ -9,6 +9,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest.log 2>&1; echo "py
 for c in n5000_k16 n5000_k1 n5000_k4 n5000_k64 batched; do
   timeout 600 python bench.py --config $c --steps 20 --warmup 4 > $out/bench_$c.json 2> $out/bench_$c.err
 done
+timeout 600 python bench.py --config n100000_k32 --steps 3 --warmup 3 > $out/bench_n100000_k32.json 2> $out/bench_n100000_k32.err
 timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > $out/bench_reference.json 2> $out/bench_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $out/ncu_launch.log 2>&1
