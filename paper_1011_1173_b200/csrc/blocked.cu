@@ -73,6 +73,9 @@ constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per 
 #ifndef GCM_FUSE_DIAG
 #define GCM_FUSE_DIAG 1
 #endif
+#ifndef GCM_PDL_APPLY
+#define GCM_PDL_APPLY 1
+#endif
 #ifndef GCM_FUSE_KB32
 #define GCM_FUSE_KB32 0
 #endif
@@ -291,6 +294,7 @@ struct TrsvArgs {
     unsigned *taskctr;        // ticket counter (armed to all-ones by the pass's memset)
     int fuse;                 // 1: the diagonal sweeps run here (else bdiag_kernel after this kernel)
     int fuse_apply;           // 1: so do the Apply tiles (needs fuse, CI = 1 and the TMA map tm2)
+    int publish;              // 1: publish sweep flags and helper tile-row progress (fused or overlapped Apply)
     int H;                    // helper CTAs (strip s is owned by helper s % H)
     unsigned *bflag;          // [NB] epoch when block b's sweep (panel, U_b^{-1}) is stored
     unsigned long long *hprog;  // [H] (epoch << 32) | tile rows a helper has finished (published by its feeder)
@@ -738,7 +742,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
 #pragma unroll
             for (int i = 0; i < kHelpRing; ++i)
                 if (i == slot) {
-                    if (use > 0 && slot_row[i] >= 0 && a.fuse_apply) publish(slot_row[i] + 1);
+                    if (use > 0 && slot_row[i] >= 0 && a.publish && (slot_row[i] & 1)) publish(slot_row[i] + 1);  // 64-row steps
                     slot_row[i] = it.ii == nown - 1 ? it.tb : -1;
                 }
             double *stg = ring + slot * kSlot;
@@ -783,7 +787,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
             }
         }
         cp_async_wait_all();
-        if (a.fuse_apply) {  // every tile consumed: all rows
+        if (a.publish) {  // every tile consumed: all rows
             for (int q = seq - kHelpRing > 0 ? seq - kHelpRing : 0; q < seq; ++q)
                 mbar_wait(empty + q % kHelpRing, (unsigned)((q / kHelpRing) & 1));
             publish(NT);
@@ -1605,13 +1609,54 @@ __device__ void btma_body(const CUtensorMap &tm, int64_t n, int k, const double 
     if (t <= kT2Stages) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bars + t)) : "memory");
 }
 
+// Flags an Apply grid launched while the TRSV kernel still runs (programmatic dependent
+// launch) waits on: tile (b, s0..) needs sweep b, the strip owners past tile rows 2b, 2b+1
+// (checkpoints written, L rows of block b read) and J1 done with the rows of block b.
+struct ApplyWait {
+    const unsigned *bflag;  // nullptr: plain stream order, no waits
+    const unsigned long long *hprog;
+    const unsigned *lflag;
+    unsigned epoch;
+    int H, NT;
+};
+// bounded spin: a lost flag becomes a kernel error (trap), never a hang
+__device__ __forceinline__ void spin_wait(bool (*ok)(const void *, unsigned, int), const void *p, unsigned epoch,
+                                          int need) {
+    long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (!ok(p, epoch, need)) {
+        __nanosleep(256);
+        long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 4000000000ll) __trap();  // 4 s
+    }
+}
+__device__ bool flag_ok(const void *p, unsigned epoch, int) { return ld_acquire((const unsigned *)p) == epoch; }
+__device__ bool prog_ok(const void *p, unsigned epoch, int need) {
+    const unsigned long long v = ld_acquire64((const unsigned long long *)p);
+    return (unsigned)(v >> 32) == epoch && (int)(unsigned)v >= need;
+}
+
 template <int KB>
 __global__ void __launch_bounds__(kT2Threads, 2) btma_kernel(const __grid_constant__ CUtensorMap tm, int64_t n, int k,
                                                               const double *__restrict__ chk,
                                                               const double *__restrict__ Ui,
-                                                              const double *__restrict__ panels, int NB) {
+                                                              const double *__restrict__ panels, int NB,
+                                                              ApplyWait w) {
     const int s0 = blockIdx.x + 1 + t2_strips(KB) * blockIdx.y;
     if (s0 >= NB) return;
+    if (w.bflag) {
+        const int b = blockIdx.x;
+        if (threadIdx.x == 0) {
+            spin_wait(flag_ok, w.bflag + b, w.epoch, 0);
+            const int slo = 2 * s0, shi = min(w.NT, 2 * (s0 + t2_strips(KB)));
+            for (int s32 = slo; s32 < shi; ++s32) spin_wait(prog_ok, w.hprog + s32 % w.H, w.epoch, 2 * b + 2);
+            for (int tb = 2 * b + 2; tb <= min(w.NT - 1, 2 * b + 1 + kLookC); ++tb)
+                spin_wait(flag_ok, w.lflag + tb, w.epoch, 0);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // sweep's generic stores -> bulk copies
+        }
+        __syncthreads();
+    }
     extern __shared__ __align__(16) unsigned char smem_t2[];
     btma_body<KB>(tm, n, k, chk, Ui, panels, NB, blockIdx.x, s0, smem_t2, 0);
 }
@@ -1683,7 +1728,7 @@ __device__ void trsv_worker(const TrsvArgs &a, double *smem, unsigned long long 
 #ifdef GCM_TRACE
                 g_htrace[(1000 + b) * 8 + 2] = gtime();
 #endif
-                if (a.fuse_apply) {
+                if (a.publish) {
                     __threadfence();
                     st_release(a.bflag + b, a.epoch);
                 }
@@ -1715,6 +1760,9 @@ __device__ void trsv_worker(const TrsvArgs &a, double *smem, unsigned long long 
 template <int KB>
 __global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_constant__ TrsvArgs a) {
     extern __shared__ __align__(128) double smem_trsv[];
+    // every CTA is resident (cooperative launch): the Apply grid may be scheduled onto SMs
+    // as our CTAs exit (programmatic dependent launch); it waits on our flags, not on us
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if ((int)blockIdx.x < a.NC)
         trsv_chain(a, smem_trsv, blockIdx.x);
     else if ((int)blockIdx.x == a.NC) {
@@ -1793,6 +1841,14 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     // and stretches the chain by half; by default the Apply runs as btma_kernel afterwards.
     a.fuse_apply = GCM_FUSE_APPLY && a.fuse && lay.NB > 1 && lay.CI == 1 && a.bulk_ok &&
                    encode_tmap(&a.tm2, L, n, ldl, (unsigned)kT2Rows, (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B);
+    // Overlapped Apply (default for fused sweeps): btma_kernel is launched as a programmatic
+    // dependent of the TRSV kernel and takes SMs as TRSV CTAs exit, each tile waiting on its
+    // sweep's flag and the strip owners' progress -- so the Apply of the early blocks runs
+    // under the last diagonal sweeps instead of after them.
+    CUtensorMap tm2;
+    const bool pdl = GCM_PDL_APPLY && a.fuse && !a.fuse_apply && lay.NB > 1 && lay.CI == 1 && a.bulk_ok &&
+                     encode_tmap(&tm2, L, n, ldl, (unsigned)kT2Rows, (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B);
+    a.publish = a.fuse_apply || pdl;
     a.G = reinterpret_cast<double *>(wsbase + lay.G);
     a.Ui = reinterpret_cast<double *>(wsbase + lay.U);
     a.sigma = sigma;
@@ -1823,6 +1879,32 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     st = check_cuda(cudaMemsetAsync(a.rchain, 0xff,
                                     lay.pfast - lay.rchain + ((size_t)lay.NT * kDT * k + 1) * sizeof(double), stream));
     if (st != GCM_OK) return st;
+    double *U = reinterpret_cast<double *>(wsbase + lay.U);
+    double *panels = reinterpret_cast<double *>(wsbase + lay.panels);
+    if (pdl) {  // one profiling scope: an event between the two launches would serialise them
+        const size_t smem_t2 = t2_smem_bytes(KB);
+        st = check_cuda(
+            cudaFuncSetAttribute(btma_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t2));
+        if (st != GCM_OK) return st;
+        ProfScope ps("blocked", stream);
+        st = check_cuda(cudaLaunchCooperativeKernel((const void *)trsv_kernel<KB>, dim3(grid), dim3(kTrsvThreads),
+                                                    args, smem, stream));
+        if (st != GCM_OK) return st;
+        ApplyWait w{a.bflag, a.hprog, a.lflag, epoch, a.H, lay.NT};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(lay.NB - 1, (lay.NB - 1 + t2_strips(KB) - 1) / t2_strips(KB));
+        cfg.blockDim = dim3(kT2Threads);
+        cfg.dynamicSmemBytes = smem_t2;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const double *chk = a.chk;
+        return check_cuda(cudaLaunchKernelEx(&cfg, btma_kernel<KB>, tm2, n, k, chk, (const double *)U,
+                                             (const double *)panels, (int)lay.NB, w));
+    }
     {
         ProfScope ps("trsv", stream);
         st = check_cuda(cudaLaunchCooperativeKernel((const void *)trsv_kernel<KB>, dim3(grid), dim3(kTrsvThreads),
@@ -1830,8 +1912,6 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     }
     if (st != GCM_OK) return st;
 
-    double *U = reinterpret_cast<double *>(wsbase + lay.U);
-    double *panels = reinterpret_cast<double *>(wsbase + lay.panels);
     if (!a.fuse) {  // else the diagonal sweeps ran inside trsv_kernel (worker mode)
         st = check_cuda(
             cudaFuncSetAttribute(bdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_diag));
@@ -1845,7 +1925,6 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
         st = check_cuda(
             cudaFuncSetAttribute(bapply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_apply));
         if (st != GCM_OK) return st;
-        CUtensorMap tm2;
         if (lay.CI == 1 && a.bulk_ok &&
             encode_tmap(&tm2, L, n, ldl, (unsigned)kT2Rows, (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B)) {
             const size_t smem_t2 = t2_smem_bytes(KB);
@@ -1854,7 +1933,8 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
             if (st != GCM_OK) return st;
             const dim3 gridt(lay.NB - 1, (lay.NB - 1 + t2_strips(KB) - 1) / t2_strips(KB));
             ProfScope ps("bapply", stream);
-            btma_kernel<KB><<<gridt, kT2Threads, smem_t2, stream>>>(tm2, n, k, a.chk, U, panels, lay.NB);
+            btma_kernel<KB><<<gridt, kT2Threads, smem_t2, stream>>>(tm2, n, k, a.chk, U, panels, lay.NB,
+                                                                    ApplyWait{nullptr, nullptr, nullptr, 0u, 1, 1});
             return check_cuda(cudaGetLastError());
         }
         if (lay.CI == 1) {
