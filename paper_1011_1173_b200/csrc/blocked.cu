@@ -73,6 +73,9 @@ constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per 
 #ifndef GCM_FUSE_DIAG
 #define GCM_FUSE_DIAG 1
 #endif
+#ifndef GCM_PUB_EVERY
+#define GCM_PUB_EVERY -1  // >= 0: publish progress when rows done is a multiple of GCM_PUB_EVERY+1
+#endif
 #ifndef GCM_PDL_APPLY
 #define GCM_PDL_APPLY 1
 #endif
@@ -732,6 +735,9 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
         int slot_row[kHelpRing];
 #pragma unroll
         for (int i = 0; i < kHelpRing; ++i) slot_row[i] = -1;
+        // each publication is a release (the feeder stalls until the checkpoints are out), so
+        // publish every 64 rows for KB = 16 and every 128 for smaller ranks (same-box A/B)
+        constexpr int kPubEvery = GCM_PUB_EVERY >= 0 ? GCM_PUB_EVERY : (KB >= 16 ? 1 : 3);
         auto publish = [&](int rows) {
             if (lane == 0) st_release64(a.hprog + h, ((unsigned long long)a.epoch << 32) | (unsigned)rows);
         };
@@ -742,7 +748,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
 #pragma unroll
             for (int i = 0; i < kHelpRing; ++i)
                 if (i == slot) {
-                    if (use > 0 && slot_row[i] >= 0 && a.publish && (slot_row[i] & 1)) publish(slot_row[i] + 1);  // 64-row steps
+                    if (use > 0 && slot_row[i] >= 0 && a.publish && (slot_row[i] & kPubEvery) == kPubEvery) publish(slot_row[i] + 1);
                     slot_row[i] = it.ii == nown - 1 ? it.tb : -1;
                 }
             double *stg = ring + slot * kSlot;
