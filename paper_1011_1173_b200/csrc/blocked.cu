@@ -80,7 +80,7 @@ constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per 
 #define GCM_PDL_APPLY 1
 #endif
 #ifndef GCM_FUSE_KB32
-#define GCM_FUSE_KB32 0
+#define GCM_FUSE_KB32 1
 #endif
 #ifndef GCM_GRAM_CHOL
 #define GCM_GRAM_CHOL 0
@@ -1837,8 +1837,8 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.ebase = ebase;
     a.uflag = a.qflag + lay.NT;
     a.taskctr = reinterpret_cast<unsigned *>(a.pfast + (size_t)lay.NT * kDT * k);
-    // KB = 32: helper tiles are twice as long and the sweep (95 ticks) twice as deep, so
-    // fused sweeps slow the chain's helpers more than they save; they run after the solve
+    // diagonal sweeps fused for every rank (KB = 32 alone: 1.39 ms at k = 64 with the sweeps
+    // after the solve, 1.17 ms fused with the overlapped Apply -- same-box A/B)
     a.fuse = GCM_FUSE_DIAG && (KB <= 16 || GCM_FUSE_KB32);
     a.bflag = a.uflag + lay.NB;
     a.hprog = reinterpret_cast<unsigned long long *>(wsbase + lay.hprog);
