@@ -326,8 +326,10 @@ def kernel_units(name, n, k, batch):
     """Algorithmic work of ONE launch of each kernel family."""
     tri = 8 * n * (n + 1) // 2  # bytes of the upper triangle
     if name == "blocked":  # TRSV kernel + the Apply grid overlapped with it (one profiling scope)
-        return {"bound": "alu", "bytes": 8 * n * (n + 1) + 16 * n * k, "flops": 6 * k * n * (n - 1) / 2,
-                "what": "whole path (TRSV + fused sweeps + overlapped Apply): 6 flops per Apply"}
+        return {"bound": "hbm" if k < 16 else "alu", "bytes": 8 * n * (n + 1) + 16 * n * k,
+                "flops": 6 * k * n * (n - 1) / 2,
+                "what": "whole path (TRSV + fused sweeps + overlapped Apply): upper triangle read+write once "
+                        "+ V; 6 flops per Apply"}
     if name == "trsv":  # reads the triangle once for P = L^-T V (k FMA per element)
         return {"bound": "hbm", "bytes": tri + 16 * n * k, "flops": n * n * k,
                 "what": "L triangle read once + V read + P write; n^2 k flops"}

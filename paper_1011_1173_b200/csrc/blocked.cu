@@ -190,9 +190,20 @@ __device__ long long g_trace[4096 * 8];
 
 // Bytes of Apply checkpoints before the checkpoint interval CI doubles (2 GiB;
 // GCM_CHK_BUDGET overrides it per call -- the tests use it to exercise CI > 1).
-size_t chk_budget() {
+Layout make_layout(int64_t n, int k, size_t chk_budget);
+size_t chk_budget(int64_t n, int kc) {
     const char *e = std::getenv("GCM_CHK_BUDGET");
-    return e ? (size_t)std::strtoull(e, nullptr, 10) : (size_t)(2ull << 30);
+    if (e) return (size_t)std::strtoull(e, nullptr, 10);
+    // at least 2 GiB, up to a quarter of the free device memory when more lets the checkpoint
+    // interval drop to 1 (n = 100000: 20 GB of checkpoints next to its 80 GB factor, and the
+    // TMA Apply path). Sticky: the cached workspace keeps what it was granted, and
+    // cudaMemGetInfo (milliseconds) is only asked when the current budget gives CI > 1.
+    static size_t high_water = (size_t)(2ull << 30);
+    if (make_layout(n, kc, high_water).CI > 1) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) high_water = std::max(high_water, free_b / 4);
+    }
+    return high_water;
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -1979,7 +1990,7 @@ extern "C" int gcm_debug_htrace(long long *host, int count) {
 
 size_t blocked_workspace_bytes(int64_t n, int64_t k) {
     const int kc = (int)std::min<int64_t>(k, kBKMax);
-    return make_layout(n, kc, chk_budget()).total;
+    return make_layout(n, kc, chk_budget(n, kc)).total;
 }
 
 gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
@@ -1988,7 +1999,15 @@ gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_
     char *base = reinterpret_cast<char *>(ws->panels);
     for (int64_t e0 = 0; e0 < k; e0 += kBKMax) {
         const int kc = (int)std::min<int64_t>(kBKMax, k - e0);
-        const Layout lay = make_layout(n, kc, chk_budget());
+        // the layout must fit the workspace sized earlier (free memory may have changed since)
+        size_t budget = chk_budget(n, kc);
+        Layout lay = make_layout(n, kc, budget);
+        const size_t cap = ws->bytes - (size_t)(reinterpret_cast<char *>(ws->panels) - reinterpret_cast<char *>(ws->key));
+        while (lay.total > cap && lay.CI < lay.NB) {
+            budget /= 2;
+            lay = make_layout(n, kc, budget);
+        }
+        if (lay.total > cap) return GCM_ENOMEM;
         const unsigned epoch = ++ws->epoch;
         double *Vc = V + e0 * n;
         if (kc <= 4) st = blocked_pass<4>(L, n, ldl, Vc, kc, sigma, key, e0, base, lay, epoch, stream);
