@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/ab
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/ab/pytest.txt 2>&1
-timeout 600 python bench.py --config n100000_k32 --steps 3 --warmup 3 > gpurun_out/ab/n1e5.json 2> gpurun_out/ab/n1e5.err
-for c in n5000_k16 n5000_k1 n5000_k4 n5000_k64; do timeout 300 python bench.py --config $c --steps 20 --warmup 4 > gpurun_out/ab/bench_$c.json 2> gpurun_out/ab/bench_$c.err; done
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ab/smoke.txt 2>&1; echo "smoke exit $?" >> gpurun_out/ab/smoke.txt
+timeout 600 compute-sanitizer --tool memcheck --print-limit 20 python tools/one_call.py 700 16 > gpurun_out/ab/memcheck.txt 2>&1; echo "memcheck exit $?" >> gpurun_out/ab/memcheck.txt
+timeout 600 compute-sanitizer --tool synccheck --print-limit 20 python tools/one_call.py 700 16 > gpurun_out/ab/synccheck.txt 2>&1; echo "synccheck exit $?" >> gpurun_out/ab/synccheck.txt
