@@ -18,16 +18,17 @@
 //
 // Kernels (one pass per <= 32 update columns; k > 32 runs ceil(k/32) passes =
 // sequential rank-32 modifications, R3):
-//   trsv_kernel        persistent, cooperative: CTAs 0..NC-1 = the chains (P in
-//                      32-row blocks, kRPC right-hand sides each, lookahead
-//                      kLookC blocks), CTAs NC.. = strip owners
-//                      (right-looking residual updates + Apply checkpoints) and
-//                      diagonal-block inverses; device flags, no per-block launch.
-//   gram_kernel        Q_b = P_b^T P_b per 64-row block.
-//   bdiag_kernel       per 64-block (all in parallel): G_b, U_b, V-state, in-block
-//                      sweep (rot.cuh block_sweep) -> coefficient panel, V_exit, L~_bb.
-//   bapply_kernel      per (tile segment, column strip): V-state from the
-//                      checkpoint, then the scaled 2-FMA Apply of the panels.
+//   trsv_kernel   persistent, cooperative (one CTA per SM): CTAs 0..NC-1 = the chains
+//                 (P in 32-row blocks, kRPC right-hand sides each, operands N/M/X
+//                 precomputed), CTA NC = the Gram prefix sums, the rest = strip owners
+//                 (J1 operands, then right-looking residual updates + Apply checkpoints),
+//                 which take diagonal-sweep tickets once their strips are done (worker
+//                 mode: bdiag_body per 64-row block, in parallel as the chain advances).
+//   btma_kernel   Apply of each block's panel to 64 x 256 off-diagonal tiles (TMA boxes,
+//                 scaled 2-FMA rotations from the checkpointed V states); launched as a
+//                 programmatic dependent of trsv_kernel, waiting on per-block flags.
+//   bdiag_kernel / btile_kernel / bapply_kernel: the same steps as separate launches
+//                 (switches off, unaligned L, or checkpoint interval CI > 1).
 #include <cooperative_groups.h>
 #include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 
