@@ -187,6 +187,15 @@ def test_host_entry_point(gcm):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("k", [1, 4, 64])
+def test_parity_k_sweep_config(gcm, k):
+    """BASELINE configs[2]: n=5000, k in {1, 4, 64} (k=64 = two rank-32 passes), update and
+    downdate, full-size element-wise parity in the launch configuration bench.py times."""
+    for sigma in (1, -1):
+        check(*run_both(gcm, 5000, k, sigma, seed=synth.SEED_ROOT + k), 5000)
+
+
+@pytest.mark.slow
 def test_parity_headline_config(gcm):
     """BASELINE configs[1]: n=5000, k=16, update and downdate, full-size element-wise parity."""
     for sigma in (1, -1):
@@ -197,6 +206,7 @@ def test_parity_headline_config(gcm):
 @pytest.mark.parametrize("sigma", [1, -1])
 def test_parity_checkpoint_interval(gcm, monkeypatch, budget, n, k, sigma):
     """A small checkpoint budget forces CI > 1 (the very-large-n Apply walk, bapply_kernel),
-    which the default 2 GiB budget only reaches at n ~ 1e5."""
+    which the default budget (>= 2 GiB, up to a quarter of free memory) never reaches at
+    these sizes."""
     monkeypatch.setenv("GCM_CHK_BUDGET", str(budget))
     check(*run_both(gcm, n, k, sigma, seed=n + k, algo="blocked"), n)
