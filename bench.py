@@ -258,7 +258,8 @@ def run_ours(args, world, rank, local):
 
     # dominant kernel and its roofline (bytes/flops per launch from DESIGN.md "roofline")
     hbm, hbm_src = measured_peaks()
-    launches = sum(c for c, _ in prof.values())
+    # kernels per profiling scope: 'blocked' = trsv_kernel + its programmatic-dependent btma_kernel
+    launches = sum(c * (2 if name == "blocked" else 1) for name, (c, _) in prof.items())
     dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 0.0))
     dname, (dcount, dms) = dom
     per_launch_ms = dms / max(dcount, 1)
