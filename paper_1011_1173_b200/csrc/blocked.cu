@@ -322,7 +322,12 @@ constexpr int kPrepThreads = kPrepWarps * 32;
 constexpr int kSvcWarp = kRPC + kPrepWarps;  // loader warp
 constexpr int kWin = kLookC <= 4 ? 128 : kLookC <= 8 ? 256 : 512;  // rows of the chain's p window (pow2 >= kLookC*kDT)
 static_assert(kWin >= kLookC * kDT && kLookC <= 16, "p window indexed by row & (kWin - 1)");
-constexpr int kHelpMaxOwn = 4;          // strips whose residual a helper keeps in shared memory
+// strips whose residual a helper keeps in shared memory (the rest round-trip through L2 on
+// every tile): at large n a helper owns ~n/(32*139) strips (24 at n = 100000)
+#ifndef GCM_HELP_OWN
+#define GCM_HELP_OWN 1
+#endif
+__host__ __device__ constexpr int help_max_own(int KB) { return GCM_HELP_OWN ? (KB <= 16 ? 24 : 12) : 4; }
 constexpr int kHelpRing = 6;            // tiles (L tile + P block) a helper's feeder keeps in flight
 #ifndef GCM_FASTBACK
 #define GCM_FASTBACK 2
@@ -612,6 +617,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
     constexpr int NQ = (kDT * KB + kTrsvThreads - 1) / kTrsvThreads;
     double *Lb = smem;                      // [kDT][kLdT]
     double *Pt = Lb + kDT * kLdT;           // [kDT][max(KB, kLdT)]  (P block; X during J1)
+    constexpr int kHelpMaxOwn = help_max_own(KB);
     double *rs = Pt + kDT * (KB > kLdT ? KB : kLdT);  // [kHelpMaxOwn][kDT][KB] residuals of owned strips
     const int t = threadIdx.x;
     const int k = a.k;
@@ -1875,7 +1881,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (st == GCM_OK) st = check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     if (st != GCM_OK) return st;
     const size_t smem_chain = (size_t)ChainSmem::total * sizeof(double);
-    const size_t smem_help = (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + kHelpMaxOwn * kDT * KB +
+    const size_t smem_help = (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + help_max_own(KB) * kDT * KB +
                                       kHelpRing * (kDT * kLdT + kDT * (KB + 1)) + 3 * kHelpRing) *
                              sizeof(double);
     const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 +

@@ -210,3 +210,38 @@ def test_parity_checkpoint_interval(gcm, monkeypatch, budget, n, k, sigma):
     these sizes."""
     monkeypatch.setenv("GCM_CHK_BUDGET", str(budget))
     check(*run_both(gcm, n, k, sigma, seed=n + k, algo="blocked"), n)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n,k", [(24000, 16), (24000, 32)])
+def test_large_n_properties(gcm, n, k):
+    """Sizes where a strip owner holds more than a handful of strips (n/32/139 > 5) and the
+    oracle is too slow element-wise: full-size pins that hold at any size (SURVEY 8(c) P4,
+    P5) -- the column-norm identity ||L~_{:,c}||^2 = ||L_{:,c}||^2 + sigma ||V_{c,:}||^2 on
+    every column, and Freivalds' check L~^T L~ x = L^T L x + sigma V V^T x -- for an update
+    and the downdate back (direct-L instance, R18, drawn on the device)."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(synth.SEED_ROOT + n + k)
+    Lt = torch.empty((n, n), dtype=torch.float64, device=dev)  # row c = column c of L
+    Lt.uniform_(-1.0 / n ** 0.5, 1.0 / n ** 0.5, generator=g)
+    Lt.diagonal().uniform_(1.0, 2.0, generator=g)
+    V0 = torch.rand((k, n), dtype=torch.float64, device=dev, generator=g) / n ** 0.5
+    x = torch.rand((n, 2), dtype=torch.float64, device=dev, generator=g)
+    for sigma in (1, -1):
+        low = torch.tril(Lt)  # L^T (lower), the upper factor's entries only
+        col2 = (low ** 2).sum(1)
+        ax = low @ (low.T @ x)
+        del low
+        V = V0.clone()
+        gcm.modify(Lt, V, sigma)
+        torch.cuda.synchronize()
+        low = torch.tril(Lt)
+        vn = (V0 ** 2).sum(0)
+        rel = ((low ** 2).sum(1) - col2 - sigma * vn).abs() / (low ** 2).sum(1)
+        assert rel.max().item() <= 1e-11, f"column-norm identity {rel.max().item():.2e} (sigma={sigma})"
+        want = ax + sigma * (V0.T @ (V0 @ x))
+        got = low @ (low.T @ x)
+        fr = ((got - want).norm() / want.norm()).item()
+        assert fr <= 1e-11, f"Freivalds {fr:.2e} (sigma={sigma})"
+        del low
