@@ -65,9 +65,6 @@ constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per 
 #ifndef GCM_PROG_STRIDE
 #define GCM_PROG_STRIDE 16
 #endif
-#ifndef GCM_POLL_RELAXED
-#define GCM_POLL_RELAXED 0
-#endif
 #ifndef GCM_PUB_FENCE
 #define GCM_PUB_FENCE 1
 #endif
@@ -217,17 +214,6 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-// polling load: relaxed (no L1 invalidation per poll); the caller fences once it
-// has seen the value it waits for
-__device__ __forceinline__ unsigned long long ld_poll64(const unsigned long long *p) {
-    unsigned long long v;
-#if GCM_POLL_RELAXED
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-#else
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-#endif
-    return v;
-}
 // Hand-off values are self-validating: rchain starts all-ones (a NaN no
 // producer writes, see handoff_value) and each chain thread polls its own
 // 8-byte value, so the hand-off needs no flag, no fence and no second round trip.
@@ -264,15 +250,6 @@ __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned lon
 }
 __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// CTA-wide wait until *f == epoch (thread 0 spins; acquire, then barrier).
-__device__ __forceinline__ void cta_wait(const unsigned *f, unsigned epoch, bool sleep) {
-    if (threadIdx.x == 0) {
-        while (ld_acquire(f) != epoch) {
-            if (sleep) __nanosleep(64);
-        }
-    }
-    __syncthreads();
 }
 // CTA-wide publish: every thread's prior global stores, then *f = epoch.
 __device__ __forceinline__ void cta_publish(unsigned *f, unsigned epoch) {
@@ -614,7 +591,6 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
 // ---------------------------------------------------------------- helper CTAs
 template <int KB>
 __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int h, int H) {
-    constexpr int NQ = (kDT * KB + kTrsvThreads - 1) / kTrsvThreads;
     double *Lb = smem;                      // [kDT][kLdT]
     double *Pt = Lb + kDT * kLdT;           // [kDT][max(KB, kLdT)]  (P block; X during J1)
     constexpr int kHelpMaxOwn = help_max_own(KB);

@@ -20,7 +20,7 @@ constexpr int kKMax = 64;
 //   rho[j]  at offset 2*D*k,  nu[e] at offset 2*D*k + D.
 // gamma/delta/rho/nu are the rotation (c_{j,e}, s_{j,e}) of PAPER.md 44-49
 // restated for the scaled 2-FMA Apply.
-__host__ __device__ inline int64_t panel_doubles(int k) { return 2ll * kD * k + kD + k; }
+__host__ __device__ constexpr int64_t panel_doubles(int k) { return 2ll * kD * k + kD + k; }
 
 // Failure key: atomicMin over ((e << 41) | (row << 1) | (code == 2 ? 0 : 1)),
 // i.e. lexicographic (e, row) with code 2 first at equal (e, row).
