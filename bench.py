@@ -371,7 +371,7 @@ def run_e2e(gcm, torch, Lbuf, Vbuf, n, k, flops, steps=3):
         if i > 0:
             ts.append(dt)
     t = statistics.median(ts)
-    nb = Lh.numel() * 8 + Vh.numel() * 8
+    nb = gcm.modify_host_bytes(n, k)  # upper-triangle column blocks + V, each direction
     return {"value": round(flops / t / 1e9, 2), "unit": "GFLOP/s", "ms_per_step": round(t * 1e3, 3),
             "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "api": "gcm_modify_host (pinned host L, V)"}
 

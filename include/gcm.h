@@ -101,6 +101,12 @@ gcm_status_t gcm_modify_ex(double *L, int64_t n, int64_t ldl, double *V, int64_t
 gcm_status_t gcm_modify_host(double *L_host, int64_t n, int64_t ldl, double *V_host, int64_t k,
                              int sigma, gcm_info_t *h_info);
 
+/* Bytes gcm_modify_host moves in EACH direction for (n, k): the upper triangle
+ * as column blocks of 256 columns (block [j0, j1) carries rows 0..j1-1, so a
+ * little of the strictly lower part near the diagonal rides along and is
+ * written back unchanged) plus V.  Host-only, no CUDA call; -1 if n or k < 0. */
+int64_t gcm_modify_host_bytes(int64_t n, int64_t k);
+
 /* Batched variant: `batch` independent factors of the same n, k, sigma.
  * Factor b is L + b*strideL (n x n, ldl) and V + b*strideV (n x k, ld n).
  * strideL >= ldl*n, strideV >= n*k (the footprints must not overlap).

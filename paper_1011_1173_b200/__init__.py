@@ -20,7 +20,7 @@ import ctypes
 from . import _native
 from ._native import GcmError, GcmInfo
 
-__all__ = ["modify", "modify_batched", "modify_host", "new_info", "read_info", "GcmError", "lib_path",
+__all__ = ["modify", "modify_batched", "modify_host", "modify_host_bytes", "new_info", "read_info", "GcmError", "lib_path",
            "release_workspace", "version"]
 
 
@@ -92,6 +92,14 @@ def modify_host(L, V, sigma: int):
                                        int(sigma), ctypes.byref(info))
     _native.check("gcm_modify_host", st)
     return (info.code, info.col, info.row)
+
+
+def modify_host_bytes(n: int, k: int) -> int:
+    """Bytes modify_host moves in each direction for (n, k) (gcm_modify_host_bytes)."""
+    b = _native.lib().gcm_modify_host_bytes(int(n), int(k))
+    if b < 0:
+        raise ValueError("n and k must be >= 0")
+    return int(b)
 
 
 def modify_batched(L, V, sigma: int, info=None, stream=None) -> None:

@@ -204,6 +204,18 @@ gcm_status_t gcm_modify_ex(double *L, int64_t n, int64_t ldl, double *V, int64_t
     return modify_impl(L, n, ldl, V, k, sigma, d_info, algo, (cudaStream_t)stream);
 }
 
+static constexpr int64_t kHostCB = 256;
+
+int64_t gcm_modify_host_bytes(int64_t n, int64_t k) {
+    if (n < 0 || k < 0) return -1;
+    int64_t b = n * k;
+    for (int64_t j0 = 0; j0 < n; j0 += kHostCB) {
+        const int64_t j1 = std::min<int64_t>(n, j0 + kHostCB);
+        b += j1 * (j1 - j0);
+    }
+    return b * (int64_t)sizeof(double);
+}
+
 gcm_status_t gcm_modify_host(double *L_host, int64_t n, int64_t ldl, double *V_host, int64_t k, int sigma,
                              gcm_info_t *h_info) {
     gcm_status_t st = validate(L_host, n, ldl, V_host, k, sigma);
@@ -238,10 +250,21 @@ gcm_status_t gcm_modify_host(double *L_host, int64_t n, int64_t ldl, double *V_h
     double *dL = reinterpret_cast<double *>(base);
     double *dV = reinterpret_cast<double *>(base + lbytes);
     gcm_info_t *dinfo = reinterpret_cast<gcm_info_t *>(base + ((lbytes + vbytes + 255) / 256) * 256);
-    st = check_cuda(cudaMemcpyAsync(dL, L_host, lbytes, cudaMemcpyHostToDevice, s));
+    // Only the upper triangle is referenced (gcm.h): move it as column blocks of
+    // kHostCB columns, block [j0, j1) carrying rows 0..j1-1 (one 2-D copy each).
+    auto copy_tri = [&](double *dst, const double *src, cudaMemcpyKind kind) {
+        gcm_status_t r = GCM_OK;
+        for (int64_t j0 = 0; j0 < n && r == GCM_OK; j0 += kHostCB) {
+            const int64_t j1 = std::min<int64_t>(n, j0 + kHostCB);
+            r = check_cuda(cudaMemcpy2DAsync(dst + j0 * ldl, ldl * sizeof(double), src + j0 * ldl,
+                                             ldl * sizeof(double), j1 * sizeof(double), j1 - j0, kind, s));
+        }
+        return r;
+    };
+    st = copy_tri(dL, L_host, cudaMemcpyHostToDevice);
     if (st == GCM_OK) st = check_cuda(cudaMemcpyAsync(dV, V_host, vbytes, cudaMemcpyHostToDevice, s));
     if (st == GCM_OK) st = modify_impl(dL, n, ldl, dV, k, sigma, dinfo, GCM_ALGO_AUTO, s);
-    if (st == GCM_OK) st = check_cuda(cudaMemcpyAsync(L_host, dL, lbytes, cudaMemcpyDeviceToHost, s));
+    if (st == GCM_OK) st = copy_tri(L_host, dL, cudaMemcpyDeviceToHost);
     if (st == GCM_OK) st = check_cuda(cudaMemcpyAsync(V_host, dV, vbytes, cudaMemcpyDeviceToHost, s));
     if (st == GCM_OK && h_info)
         st = check_cuda(cudaMemcpyAsync(h_info, dinfo, sizeof(gcm_info_t), cudaMemcpyDeviceToHost, s));

@@ -73,3 +73,14 @@ def test_oracle_not_imported_by_product():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", src), f"{f} mentions the oracle in code"
+
+
+def test_host_bytes_counts_triangle_blocks(lib):
+    """gcm_modify_host_bytes is host-only arithmetic: 256-column blocks, block
+    [j0, j1) carrying rows 0..j1-1, plus V; at least the triangle, at most the square."""
+    assert lib.gcm_modify_host_bytes(257, 9) == 8 * (256 * 256 + 257 * 1 + 257 * 9)
+    assert lib.gcm_modify_host_bytes(0, 0) == 0
+    assert lib.gcm_modify_host_bytes(-1, 3) == -1
+    for n, k in [(1, 1), (255, 4), (5000, 16), (100000, 32)]:
+        b = lib.gcm_modify_host_bytes(n, k) // 8 - n * k
+        assert n * (n + 1) // 2 <= b <= n * n

@@ -173,17 +173,21 @@ def test_repeated_calls_and_streams(gcm):
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
-def test_host_entry_point(gcm):
-    n, k = 257, 9
+@pytest.mark.parametrize("n,k", [(257, 9), (600, 16)])  # one and three 256-column copy blocks, ragged
+def test_host_entry_point(gcm, n, k):
     for sigma in (1, -1):
         Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=14, ldl=n + 1)
         Lo, Vo = Lbuf.copy(), Vbuf.copy()
         oracle.modify_a(Lo, Vo, sigma)
-        Lh = torch.from_numpy(Lbuf.copy()).pin_memory()
+        lower = ~np.tril(np.ones(Lbuf.shape, bool))  # strictly lower part + padding row
+        Lin = Lbuf.copy()
+        Lin[lower] = np.nan  # never read: a NaN there must not reach the factor
+        Lh = torch.from_numpy(Lin).pin_memory()
         Vh = torch.from_numpy(Vbuf.copy()).pin_memory()
         assert gcm.modify_host(Lh, Vh, sigma) == (0, 0, 0)
         assert rel_fro(upper(Lh.numpy()), upper(Lo)) <= TOL_L
         assert rel_fro(Vh.numpy(), Vo) <= TOL_V
+        assert np.isnan(Lh.numpy()[lower]).all()  # left as the caller had it
 
 
 @pytest.mark.slow
