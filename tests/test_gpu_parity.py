@@ -173,7 +173,7 @@ def test_repeated_calls_and_streams(gcm):
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
-@pytest.mark.parametrize("n,k", [(257, 9), (600, 16)])  # one and three 256-column copy blocks, ragged
+@pytest.mark.parametrize("n,k", [(257, 9), (600, 16), (600, 40)])  # 1 and 3 256-column copy blocks, ragged; k=40: two passes
 def test_host_entry_point(gcm, n, k):
     for sigma in (1, -1):
         Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=14, ldl=n + 1)
