@@ -1092,8 +1092,12 @@ __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
 
 
 // One CTA per 64-row diagonal block, all blocks in parallel.
-constexpr int kDiagNQ = 4;                        // threads per column in the diagonal sweep
-constexpr int kDiagThreads = kDiagNQ * kD + 32;  // column parts + the coefficient warp
+#ifndef GCM_DIAG_NQ
+#define GCM_DIAG_NQ 4
+#endif
+constexpr int kDiagNQ = GCM_DIAG_NQ;  // threads per column in the diagonal sweep
+constexpr int kDiagThreads = 4 * kD + 32;  // up to 4 column parts + the coefficient warp
+static_assert(kDiagNQ == 1 || kDiagNQ == 2 || kDiagNQ == 4, "kDiagNQ * kD + 32 <= kDiagThreads");
 
 // The sweep of diagonal block b by one CTA of kDiagThreads threads (a bdiag_kernel CTA,
 // or a TRSV helper in worker mode: then P is read from the self-validating copy).
