@@ -92,9 +92,6 @@ constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per 
 #ifndef GCM_LATE_LOAD
 #define GCM_LATE_LOAD 0
 #endif
-#ifndef GCM_HPREFETCH
-#define GCM_HPREFETCH 1
-#endif
 #ifndef GCM_POLL_NS
 #define GCM_POLL_NS 20
 #endif
