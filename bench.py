@@ -35,10 +35,10 @@ import numpy as np  # noqa: E402
 
 METRIC = "rank-k modify ms & fp64 GFLOP/s (n=5000,k=16); % of HBM/FP64 roofline"
 # FP64 vector peak derived from the unit counts and clock (B200_PROFILING.md: 148 SMs,
-# 1965 MHz max; 64 FP64 FMA/clk/SM): 148*64*2*1.965e9.  tools/fp64_peak.cu measured
-# 34.2 TFLOP/s on this pool.
+# 1965 MHz max; 64 FP64 FMA/clk/SM): 148*64*2*1.965e9 -- the fallback when no measured
+# figure is committed.  The measured one is tools/fp64_peak.cu's JSON line, committed as
+# profiles/*fp64_peak*.json.
 FP64_PEAK_TFLOPS_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
-FP64_PEAK_TFLOPS_MEASURED = 34.2
 
 CONFIGS = {
     "n5000_k16": dict(n=5000, k=16),
@@ -59,6 +59,37 @@ def measured_peaks():
         return float(mp["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def fp64_peak():
+    """(TFLOP/s, source, link latencies) from the newest committed tools/fp64_peak.cu output."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_fp64_peak.json")))
+    if files:
+        try:
+            d = json.load(open(files[-1]))
+            return float(d["fp64_tflops"]), f"measured ({os.path.basename(files[-1])}, tools/fp64_peak.cu)", d
+        except Exception:
+            pass
+    return FP64_PEAK_TFLOPS_DERIVED, "derived (148 SM x 64 FMA/clk x 2 x 1.965 GHz)", {}
+
+
+def chain_floor(n, k, links, sm_mhz):
+    """SURVEY 8(d) latency bound beside the roofline: T_chain = (n + k - 1) t_link for the
+    literal sweep (the paper's Compute link, sqrt + div, measured by tools/fp64_peak.cu), and
+    this path's own serial chain: ceil(n/32) TRSV steps, each at least one inter-SM hand-off
+    (one-way relaxed store -> polling load, tools/pingpong.cu: 750 cycles)."""
+    mhz = sm_mhz or 1965.0
+    t_link = links.get("t_link_compute_cycles")
+    out = {"clock_mhz": mhz}
+    if t_link:
+        out["literal_sweep"] = {"links": n + k - 1, "t_link_cycles": t_link,
+                                "ms": round((n + k - 1) * t_link / mhz / 1e3, 4)}
+    steps = (n + 31) // 32
+    out["blocked_trsv"] = {"steps": steps, "t_step_floor_cycles": 750,
+                           "ms": round(steps * 750 / mhz / 1e3, 4),
+                           "note": "one inter-SM hand-off per 32-row TRSV step (tools/pingpong.cu)"}
+    return out
 
 
 def algorithmic(n, k, batch=1):
@@ -263,22 +294,30 @@ def run_ours(args, world, rank, local):
     dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 0.0))
     dname, (dcount, dms) = dom
     per_launch_ms = dms / max(dcount, 1)
-    kb = kernel_units(dname, n, k, batch)
+    # launches of the dominant scope per step: k > 32 runs ceil(k/32) passes (R3),
+    # each launch does 1/passes of the step's work
+    per_step = max(1, round(dcount / args.steps))
+    kb = kernel_units(dname, n, k, batch, per_step)
+    f64, f64_src, links = fp64_peak()
     if kb["bound"] == "hbm":
         achieved = kb["bytes"] / (per_launch_ms * 1e-3) / 1e9
         peak, unit = hbm, "GB/s"
     else:
         achieved = kb["flops"] / (per_launch_ms * 1e-3) / 1e12
-        peak, unit = FP64_PEAK_TFLOPS_DERIVED, "TFLOP/s"
+        peak, unit = f64, "TFLOP/s"
+    traffic = ncu_traffic(dname, args.config)
     roofline = {"kernel": dname, "bound": kb["bound"], "achieved": round(achieved, 3), "peak": peak,
-                "peak_source": hbm_src if kb["bound"] == "hbm" else "derived (148 SM x 64 FMA/clk x 2 x 1.965 GHz)",
-                "unit": unit, "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, args.config),
+                "peak_source": hbm_src if kb["bound"] == "hbm" else f64_src,
+                "unit": unit, "frac": round(achieved / peak, 4),
+                "traffic": traffic["bytes"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None,
+                "algorithmic_bytes": kb["bytes"], "algorithmic_flops": kb["flops"], "launches_per_step": per_step,
                 "algorithmic": kb["what"], "share_of_step": round(dms / max(sum(m for _, m in prof.values()), 1e-9), 3)}
     # whole-path roofline: T_roof = max(flops/F64, bytes/HBM)
-    t_roof = max(flops / (FP64_PEAK_TFLOPS_DERIVED * 1e12), bytes_ / (hbm * 1e9))
+    t_roof = max(flops / (f64 * 1e12), bytes_ / (hbm * 1e9))
     roofline_path = {"t_roof_ms": round(t_roof * 1e3, 4), "t_step_ms": round(ms_per_step, 4),
                      "frac": round(t_roof * 1e3 / ms_per_step, 4),
-                     "bound": "fp64" if flops / FP64_PEAK_TFLOPS_DERIVED / 1e12 > bytes_ / hbm / 1e9 else "hbm",
+                     "bound": "fp64" if flops / f64 / 1e12 > bytes_ / hbm / 1e9 else "hbm",
                      "achieved_gbs": round(bytes_ / (ms_per_step * 1e-3) / 1e9, 1),
                      "achieved_gflops": round(flops / (ms_per_step * 1e-3) / 1e9, 1)}
 
@@ -293,7 +332,9 @@ def run_ours(args, world, rank, local):
                    "instance": ("direct-L (DESIGN.md R18) on the device, torch Philox seed 10111173+rank"
                                 if cfg.get("direct") else
                                 "paper construction (PAPER.md 111): B,V ~ U[0,1), A = B^T B + I, seed 10111173+rank")},
-        "roofline": roofline, "roofline_path": roofline_path, "gpu_launches": int(launches),
+        "roofline": roofline, "roofline_path": roofline_path,
+        "chain_floor": chain_floor(n, k, links, clk.get("sm_mhz")) if batch == 1 else None,
+        "gpu_launches": int(launches),
         "kernels": {kname: {"launches": c, "ms_total": round(m, 4)} for kname, (c, m) in prof.items()},
         "clocks": clk, "wall_s": round(wall, 4),
     }
@@ -307,42 +348,45 @@ def run_ours(args, world, rank, local):
 
 
 def ncu_traffic(kernel, config):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the newest
-    committed `ncu --set full` summary (profiles/r*_ncu_summary.json, captured on the
-    default n5000_k16 workload), else None."""
-    if config != "n5000_k16":
-        return None
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the newest
+    committed `ncu --set full` summary OF THIS CONFIG (profiles/r*_ncu_<config>.json, written
+    by tools/ncu_summary.py from a capture of `bench.py --config <config>`), else None."""
     import glob
-    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_ncu_summary.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{config}.json")))
+    if not files and config == "n5000_k16":
+        files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
     if not files:
         return None
     try:
         d = json.load(open(files[-1]))["kernels"].get(kernel)
-        return None if d is None else d["traffic_bytes"]
+        if d is None or d.get("traffic_bytes") is None:
+            return None
+        return {"bytes": d["traffic_bytes"], "source": os.path.basename(files[-1])}
     except Exception:
         return None
 
 
-def kernel_units(name, n, k, batch):
-    """Algorithmic work of ONE launch of each kernel family."""
+def kernel_units(name, n, k, batch, per_step=1):
+    """Algorithmic work of ONE launch of each kernel family.  A step
+    with k > 32 runs ceil(k/32) passes (per_step launches of the same scope): each launch
+    carries its pass's share of the update columns (the triangle is read and written once
+    PER PASS, so the bytes are per pass too)."""
     tri = 8 * n * (n + 1) // 2  # bytes of the upper triangle
+    kp = k / per_step  # update columns per launch (average)
     if name == "blocked":  # TRSV kernel + the Apply grid overlapped with it (one profiling scope)
-        return {"bound": "hbm" if k < 16 else "alu", "bytes": 8 * n * (n + 1) + 16 * n * k,
-                "flops": 6 * k * n * (n - 1) / 2,
-                "what": "whole path (TRSV + fused sweeps + overlapped Apply): upper triangle read+write once "
-                        "+ V; 6 flops per Apply"}
+        return {"bound": "hbm" if kp < 16 else "alu", "bytes": 8 * n * (n + 1) + 16 * n * kp,
+                "flops": 6 * kp * n * (n - 1) / 2,
+                "what": f"one pass of {kp:g} update columns (TRSV + fused sweeps + overlapped Apply): upper "
+                        "triangle read+write once + V; 6 flops per Apply"}
     if name == "trsv":  # reads the triangle once for P = L^-T V (k FMA per element)
-        return {"bound": "hbm", "bytes": tri + 16 * n * k, "flops": n * n * k,
+        return {"bound": "hbm", "bytes": tri + 16 * n * kp, "flops": n * n * kp,
                 "what": "L triangle read once + V read + P write; n^2 k flops"}
     if name == "bapply":  # off-diagonal tiles read+write once, 2k FMA per element
         off = 2 * tri * (1 - 64.0 / n)
-        return {"bound": "hbm" if k < 16 else "alu", "bytes": off, "flops": 6 * k * n * (n - 1) / 2 * (1 - 64.0 / n),
+        return {"bound": "hbm" if kp < 16 else "alu", "bytes": off, "flops": 6 * kp * n * (n - 1) / 2 * (1 - 64.0 / n),
                 "what": "off-diagonal triangle read+write; 6 flops per Apply"}
-    if name in ("bdiag", "diag_chain"):
-        return {"bound": "alu", "bytes": 16 * 64 * n, "flops": 6 * k * 64 * n / 2,
-                "what": "diagonal blocks (64 x 64 per block) Compute+Apply"}
     if name == "panel_apply":
-        return {"bound": "hbm", "bytes": 2 * tri / max(1, (n + 63) // 64), "flops": 6 * k * n * 64 / 2,
+        return {"bound": "hbm", "bytes": 2 * tri / max(1, (n + 63) // 64), "flops": 6 * kp * n * 64 / 2,
                 "what": "one 64-row panel read+write (average)"}
     if name == "batched":
         return {"bound": "hbm", "bytes": batch * (2 * tri + 16 * n * k), "flops": batch * 6 * k * n * (n - 1) / 2,

@@ -53,6 +53,15 @@ def _check_L_V(L, V):
         raise ValueError("L and V must be contiguous")
 
 
+def _info_ptr(info, device, count):
+    """Device pointer of an info buffer made by new_info (None -> NULL), checked for size/device."""
+    if info is None:
+        return None
+    if not info.is_cuda or info.device != device or info.numel() * info.element_size() < count * ctypes.sizeof(GcmInfo):
+        raise ValueError(f"info must be a CUDA buffer on {device} with room for {count} gcm_info_t records")
+    return ctypes.c_void_p(info.data_ptr())
+
+
 def new_info(device, count: int = 1):
     """Device buffer for `count` gcm_info_t records (16 bytes each)."""
     import torch
@@ -70,23 +79,41 @@ def read_info(info):
 def modify(L, V, sigma: int, info=None, algo: str = "auto", stream=None) -> None:
     """In place: L~^T L~ = L^T L + sigma V V^T. Asynchronous."""
     _check_L_V(L, V)
+    if L.dim() != 2:
+        raise ValueError("L must have shape (n, ldl)")
     n, ldl = L.shape
+    if ldl < max(1, n):
+        raise ValueError("L must be (n, ldl) with ldl >= n")
     k = V.shape[0] if V.dim() == 2 else 0
     if V.dim() != 2 or (V.shape[1] != n and V.numel()):
         raise ValueError("V must have shape (k, n)")
-    ip = ctypes.c_void_p(info.data_ptr()) if info is not None else None
-    st = _native.lib().gcm_modify_ex(ctypes.c_void_p(L.data_ptr()), n, ldl, ctypes.c_void_p(V.data_ptr()), k,
-                                     int(sigma), ip, _native.ALGO[algo], _stream_ptr(stream, L.device))
+    ip = _info_ptr(info, L.device, 1)
+    import torch
+    with torch.cuda.device(L.device):  # the library sizes workspaces on the current device
+        st = _native.lib().gcm_modify_ex(ctypes.c_void_p(L.data_ptr()), n, ldl, ctypes.c_void_p(V.data_ptr()), k,
+                                         int(sigma), ip, _native.ALGO[algo], _stream_ptr(stream, L.device))
     _native.check("gcm_modify_ex", st)
 
 
 def modify_host(L, V, sigma: int):
     """End-to-end call with HOST (ideally pinned) tensors; synchronous.  Returns (code, col, row)."""
     import torch
+    if not (isinstance(L, torch.Tensor) and isinstance(V, torch.Tensor)):
+        raise TypeError("L and V must be torch tensors")
     if L.dtype != torch.float64 or V.dtype != torch.float64 or L.is_cuda or V.is_cuda:
         raise ValueError("modify_host takes float64 host tensors")
+    # the library copies n*ldl doubles of L and n*k of V through these raw pointers:
+    # shapes and contiguity are checked here so it can never read or write past them
+    if L.dim() != 2 or V.dim() != 2:
+        raise ValueError("L must be (n, ldl) and V (k, n)")
+    if not (L.is_contiguous() and V.is_contiguous()):
+        raise ValueError("L and V must be contiguous")
     n, ldl = L.shape
     k = V.shape[0]
+    if ldl < max(1, n):
+        raise ValueError("L must be (n, ldl) with ldl >= n")
+    if V.shape[1] != n and V.numel():
+        raise ValueError("V must have shape (k, n)")
     info = GcmInfo()
     st = _native.lib().gcm_modify_host(ctypes.c_void_p(L.data_ptr()), n, ldl, ctypes.c_void_p(V.data_ptr()), k,
                                        int(sigma), ctypes.byref(info))
@@ -105,14 +132,18 @@ def modify_host_bytes(n: int, k: int) -> int:
 def modify_batched(L, V, sigma: int, info=None, stream=None) -> None:
     """Batched in-place modification.  L: (batch, n, ldl), V: (batch, k, n), both contiguous fp64 CUDA."""
     _check_L_V(L, V)
+    if L.dim() != 3 or V.dim() != 3:
+        raise ValueError("L must be (batch, n, ldl) and V (batch, k, n)")
     batch, n, ldl = L.shape
     k = V.shape[1]
     if V.shape[0] != batch or V.shape[2] != n:
         raise ValueError("V must have shape (batch, k, n)")
-    ip = ctypes.c_void_p(info.data_ptr()) if info is not None else None
-    st = _native.lib().gcm_modify_batched(ctypes.c_void_p(L.data_ptr()), n, ldl, n * ldl,
-                                          ctypes.c_void_p(V.data_ptr()), k * n, k, int(sigma), batch, ip,
-                                          _stream_ptr(stream, L.device))
+    ip = _info_ptr(info, L.device, batch)
+    import torch
+    with torch.cuda.device(L.device):
+        st = _native.lib().gcm_modify_batched(ctypes.c_void_p(L.data_ptr()), n, ldl, n * ldl,
+                                              ctypes.c_void_p(V.data_ptr()), k * n, k, int(sigma), batch, ip,
+                                              _stream_ptr(stream, L.device))
     _native.check("gcm_modify_batched", st)
 
 

@@ -16,6 +16,12 @@
 
 namespace gcm {
 
+// Every ABI entry point that enqueues work first consumes a stale sticky-free error a
+// previous failed call may have left (cudaGetLastError), so a later launch check never
+// reports an old failure after new work was already enqueued (gcm.h: an error return
+// means nothing was enqueued by THIS call's failing step).
+void clear_stale_error() { (void)cudaGetLastError(); }
+
 gcm_status_t check_cuda(cudaError_t e) {
     if (e == cudaSuccess) return GCM_OK;
     if (std::getenv("GCM_DEBUG")) std::fprintf(stderr, "gcm: CUDA error %d: %s\n", (int)e, cudaGetErrorString(e));
@@ -71,6 +77,16 @@ namespace {
 
 std::mutex g_ws_mutex;
 std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+
+// gcm_modify_host's per-device staging: its own non-blocking stream and one device
+// buffer (L + V + info), grown on demand and freed by gcm_release_workspace.
+struct HostStage {
+    cudaStream_t stream = nullptr;
+    void *buf = nullptr;
+    size_t cap = 0;
+};
+std::mutex g_host_mutex;
+std::map<int, HostStage> g_host;
 
 __global__ void info_finalize_kernel(const unsigned long long *key, gcm_info_t *info, int64_t count) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -129,7 +145,10 @@ gcm_status_t get_workspace(cudaStream_t stream, size_t bytes, size_t nkeys, Work
         const size_t alloc = need + need / 4;
         void *p = nullptr;
         st = check_cuda(cudaMalloc(&p, alloc));
-        if (st != GCM_OK) return st;
+        if (st != GCM_OK) {
+            clear_stale_error();
+            return st;
+        }
         // device flags compare against a per-call epoch: start from all-zero
         st = check_cuda(cudaMemsetAsync(p, 0, alloc, stream));
         if (st != GCM_OK) return st;
@@ -170,6 +189,7 @@ static gcm_status_t modify_impl(double *L, int64_t n, int64_t ldl, double *V, in
                                 gcm_info_t *d_info, gcm_algo_t algo, cudaStream_t stream) {
     gcm_status_t st = validate(L, n, ldl, V, k, sigma);
     if (st != GCM_OK) return st;
+    clear_stale_error();
     if (n == 0 || k == 0) {
         if (d_info) return check_cuda(cudaMemsetAsync(d_info, 0, sizeof(gcm_info_t), stream));
         return GCM_OK;
@@ -224,29 +244,35 @@ gcm_status_t gcm_modify_host(double *L_host, int64_t n, int64_t ldl, double *V_h
         if (h_info) std::memset(h_info, 0, sizeof(*h_info));
         return GCM_OK;
     }
-    static std::mutex m;
-    static std::map<int, std::pair<cudaStream_t, void *>> bufs;  // device -> (stream, buffer)
-    static std::map<int, size_t> cap;
-    std::lock_guard<std::mutex> lock(m);
+    clear_stale_error();
+    std::lock_guard<std::mutex> lock(g_host_mutex);
     int dev = 0;
     st = check_cuda(cudaGetDevice(&dev));
     if (st != GCM_OK) return st;
-    auto &slot = bufs[dev];
-    if (!slot.first) {
-        st = check_cuda(cudaStreamCreateWithFlags(&slot.first, cudaStreamNonBlocking));
+    HostStage &slot = g_host[dev];
+    if (!slot.stream) {
+        st = check_cuda(cudaStreamCreateWithFlags(&slot.stream, cudaStreamNonBlocking));
         if (st != GCM_OK) return st;
     }
     const size_t lbytes = (size_t)n * ldl * sizeof(double), vbytes = (size_t)n * k * sizeof(double);
     const size_t need = lbytes + vbytes + 256 + sizeof(gcm_info_t);
-    if (cap[dev] < need) {
-        if (slot.second) cudaFree(slot.second);
-        slot.second = nullptr;
-        st = check_cuda(cudaMalloc(&slot.second, need));
-        if (st != GCM_OK) return st;
-        cap[dev] = need;
+    if (slot.cap < need) {
+        // the previous call synchronised its stream: the old buffer is idle; drop it first
+        // (its memory may be needed), and leave the slot empty if the new allocation fails
+        if (slot.buf) cudaFree(slot.buf);
+        slot.buf = nullptr;
+        slot.cap = 0;
+        void *p = nullptr;
+        st = check_cuda(cudaMalloc(&p, need));
+        if (st != GCM_OK) {
+            clear_stale_error();
+            return st;
+        }
+        slot.buf = p;
+        slot.cap = need;
     }
-    cudaStream_t s = slot.first;
-    char *base = static_cast<char *>(slot.second);
+    cudaStream_t s = slot.stream;
+    char *base = static_cast<char *>(slot.buf);
     double *dL = reinterpret_cast<double *>(base);
     double *dV = reinterpret_cast<double *>(base + lbytes);
     gcm_info_t *dinfo = reinterpret_cast<gcm_info_t *>(base + ((lbytes + vbytes + 255) / 256) * 256);
@@ -279,6 +305,7 @@ gcm_status_t gcm_modify_batched(double *L, int64_t n, int64_t ldl, int64_t strid
     if (st != GCM_OK) return st;
     if (batch > 1 && (strideL < ldl * n || strideV < n * k)) return GCM_EINVAL;
     if (batch == 0) return GCM_OK;
+    clear_stale_error();
     if (n == 0 || k == 0) {
         if (d_info) return check_cuda(cudaMemsetAsync(d_info, 0, sizeof(gcm_info_t) * batch, (cudaStream_t)stream));
         return GCM_OK;
@@ -332,18 +359,33 @@ const char *gcm_status_string(gcm_status_t s) {
 }
 
 gcm_status_t gcm_release_workspace(void) {
-    std::lock_guard<std::mutex> lock(g_ws_mutex);
     int cur = 0;
     cudaGetDevice(&cur);
-    for (auto &kv : g_ws) {
-        if (kv.second.key) {
-            cudaSetDevice(kv.first.first);
-            cudaStreamSynchronize(kv.first.second);
-            cudaFree(kv.second.key);
+    {
+        std::lock_guard<std::mutex> lock(g_ws_mutex);
+        for (auto &kv : g_ws) {
+            if (kv.second.key) {
+                cudaSetDevice(kv.first.first);
+                cudaStreamSynchronize(kv.first.second);
+                cudaFree(kv.second.key);
+            }
+        }
+        g_ws.clear();
+    }
+    {
+        std::lock_guard<std::mutex> lock(g_host_mutex);
+        for (auto &kv : g_host) {  // the staging stream is kept; its buffer (n*ldl doubles) is not
+            if (kv.second.buf) {
+                cudaSetDevice(kv.first);
+                cudaStreamSynchronize(kv.second.stream);
+                cudaFree(kv.second.buf);
+                kv.second.buf = nullptr;
+                kv.second.cap = 0;
+            }
         }
     }
-    g_ws.clear();
     cudaSetDevice(cur);
+    clear_stale_error();
     return GCM_OK;
 }
 

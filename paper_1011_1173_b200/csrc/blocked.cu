@@ -27,8 +27,8 @@
 //   btma_kernel   Apply of each block's panel to 64 x 256 off-diagonal tiles (TMA boxes,
 //                 scaled 2-FMA rotations from the checkpointed V states); launched as a
 //                 programmatic dependent of trsv_kernel, waiting on per-block flags.
-//   bdiag_kernel / btile_kernel / bapply_kernel: the same steps as separate launches
-//                 (switches off, unaligned L, or checkpoint interval CI > 1).
+//   btile_kernel / bapply_kernel: the Apply as a plain launch after the TRSV kernel
+//                 (unaligned L or odd ldl, or checkpoint interval CI > 1).
 #include <cooperative_groups.h>
 #include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 
@@ -62,42 +62,9 @@ constexpr int kLdN = kSeg + 1;            // row stride of N (odd: lane = j read
 constexpr int kMXN = kDT * kLdN;
 constexpr int kMXStride = ((kMXN + 2 * kDT * kDT) + 1) / 2 * 2;  // doubles per block (16-byte multiple)
 
-#ifndef GCM_PROG_STRIDE
-#define GCM_PROG_STRIDE 16
-#endif
-#ifndef GCM_PUB_FENCE
-#define GCM_PUB_FENCE 1
-#endif
-#ifndef GCM_FUSE_DIAG
-#define GCM_FUSE_DIAG 1
-#endif
-#ifndef GCM_PUB_EVERY
-#define GCM_PUB_EVERY -1  // >= 0: publish progress when rows done is a multiple of GCM_PUB_EVERY+1
-#endif
-#ifndef GCM_PDL_APPLY
-#define GCM_PDL_APPLY 1
-#endif
-#ifndef GCM_FUSE_KB32
-#define GCM_FUSE_KB32 1
-#endif
-#ifndef GCM_GRAM_CHOL
-#define GCM_GRAM_CHOL 0
-#endif
-#ifndef GCM_FUSE_APPLY
-#define GCM_FUSE_APPLY 0
-#endif
-#ifndef GCM_FEEDER_POLL
-#define GCM_FEEDER_POLL 0
-#endif
-#ifndef GCM_LATE_LOAD
-#define GCM_LATE_LOAD 0
-#endif
 #ifndef GCM_POLL_NS
 #define GCM_POLL_NS 20
 #endif
-// Each chain's progress word sits in its own 128-byte line: 140 helper feeders
-// poll them, and one shared line would serialise those polls on one L2 slice.
-constexpr int kProgStride = GCM_PROG_STRIDE;
 
 struct Layout {
     int64_t n;
@@ -147,16 +114,18 @@ Layout make_layout(int64_t n, int k, size_t chk_budget) {
     l.P = take((size_t)l.NT * kDT * k);  // padded to whole 32-row blocks (bulk copies)
     l.rcur = take((size_t)l.NT * kDT * k);
     l.rchain = take((size_t)l.NT * kDT * k);
-    l.pfast = take((size_t)l.NT * kDT * k + 2);  // must follow rchain (one memset arms both); + ticket counter
+    // rchain .. hprog are armed by ONE memset (all-ones) at the start of every pass: the
+    // hand-off slots and pfast start empty, the ticket counter at -1, and no flag or
+    // progress word can equal the pass's epoch (never 0 or all-ones) before it is published
+    l.pfast = take((size_t)l.NT * kDT * k + 2);  // + ticket counter
+    l.flags = take(((2ull * l.NT + 2ull * l.NB) * sizeof(unsigned) + 7) / 8);  // lflag, qflag, uflag, bflag
+    l.hprog = take((size_t)l.NT + 1);
     l.MX = take((size_t)l.NT * kMXStride);
     l.chk = take((size_t)l.nchk * kD * k);
     l.G = take((size_t)l.NB * kb_of(k) * kb_of(k));     // Gram prefixes G_b (KB x KB)
     l.Q = take((size_t)l.NT * kb_of(k) * kb_of(k));     // per 32-row block P_tb^T P_tb (helpers)
     l.U = take((size_t)l.NB * kb_of(k) * kb_of(k));       // U_b^{-1}, KB x KB, zero padded
     l.panels = take((size_t)l.NB * panel_doubles(kb_of(k)));  // coefficient panels, stride KB
-    l.flags = take(((2ull * l.NT + 2ull * l.NB) * sizeof(unsigned) + 16 * kProgStride * sizeof(unsigned long long) + 7) /
-                   8);  // prog[16 * kProgStride], lflag, qflag, uflag, bflag
-    l.hprog = take((size_t)l.NT + 1);
     l.total = o;
     return l;
 }
@@ -267,7 +236,6 @@ struct TrsvArgs {
     bool bulk_ok;     // L 16-byte aligned and ldl even (the Apply's TMA path)
     int CI, CIlog;  // checkpoint interval (a power of two) and its log2
     int NC;           // chain CTAs (each solves kRPC right-hand sides)
-    unsigned long long *prog;  // [NC] chain progress: (epoch << 32) | blocks published
     unsigned *lflag;
     unsigned epoch;
     double *G, *Ui;   // Gram prefixes G_b = P_{<b}^T P_{<b} and U_b^{-1} (U_b = chol_lower(I + sigma G_b))
@@ -281,13 +249,11 @@ struct TrsvArgs {
     int64_t ebase;            // first update column of this pass
     unsigned *uflag;          // [NB] epoch when what block b's sweep needs from the Gram CTA is stored
     unsigned *taskctr;        // ticket counter (armed to all-ones by the pass's memset)
-    int fuse;                 // 1: the diagonal sweeps run here (else bdiag_kernel after this kernel)
-    int fuse_apply;           // 1: so do the Apply tiles (needs fuse, CI = 1 and the TMA map tm2)
-    int publish;              // 1: publish sweep flags and helper tile-row progress (fused or overlapped Apply)
+    int publish;              // 1: publish sweep flags and helper tile-row progress (overlapped Apply)
+    int own_cap;              // strip residuals a helper keeps in shared memory (<= help_max_own(KB))
     int H;                    // helper CTAs (strip s is owned by helper s % H)
     unsigned *bflag;          // [NB] epoch when block b's sweep (panel, U_b^{-1}) is stored
     unsigned long long *hprog;  // [H] (epoch << 32) | tile rows a helper has finished (published by its feeder)
-    CUtensorMap tm2;          // 8 x 256 boxes over L, 64B swizzle (the Apply tiles)
 };
 
 constexpr int kRPC = 2;                 // right-hand sides per chain CTA
@@ -298,10 +264,9 @@ constexpr int kWin = kLookC <= 4 ? 128 : kLookC <= 8 ? 256 : 512;  // rows of th
 static_assert(kWin >= kLookC * kDT && kLookC <= 16, "p window indexed by row & (kWin - 1)");
 // strips whose residual a helper keeps in shared memory (the rest round-trip through L2 on
 // every tile): at large n a helper owns ~n/(32*139) strips (24 at n = 100000)
-#ifndef GCM_HELP_OWN
-#define GCM_HELP_OWN 1
-#endif
-__host__ __device__ constexpr int help_max_own(int KB) { return GCM_HELP_OWN ? (KB <= 16 ? 24 : 12) : 4; }
+// (GCM_HELP_OWN_CAP=<m> lowers it at run time: the tests use it to drive the spill path,
+// which the default only reaches at n > ~50k (KB = 32) / ~107k (KB <= 16))
+__host__ __device__ constexpr int help_max_own(int KB) { return KB <= 16 ? 24 : 12; }
 constexpr int kHelpRing = 6;            // tiles (L tile + P block) a helper's feeder keeps in flight
 #ifndef GCM_FASTBACK
 #define GCM_FASTBACK 2
@@ -408,11 +373,9 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
     // could be overrun because the critical warps may run two steps ahead of the
     // loader warp)
     volatile unsigned *pcount = reinterpret_cast<volatile unsigned *>(bars + 3);
-    volatile unsigned *prepdone = pcount + 1;  // prep steps finished (prep warp 0 counts)
     if (t == 0) {
         for (int i = 0; i < 3; ++i) mbar_init(bars + i, 1u);
         *pcount = 0u;
-        *prepdone = 0u;
     }
     for (int i = t; i < kWin * kRPC; i += blockDim.x) pwin[i] = 0.0;  // rows < 0 of early segments (N is 0 there)
     __syncthreads();
@@ -443,7 +406,6 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         double acc0[kRPC], acc1[kRPC];
 #pragma unroll
         for (int w = 0; w < kRPC; ++w) acc0[w] = acc1[w] = 0.0;
-#ifndef GCM_EXP_NOPART
         {  // - N p over this warp's share of the kSeg segment rows
             constexpr int kPer = (kSeg + kPrepWarps - 1) / kPrepWarps;
             const int r0 = pw * kPer;
@@ -464,7 +426,6 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
                 }
             }
         }
-#endif
         if (pt == 0) TRACE(4, tb - 1);
         if (hptr) {
             if (pt == 0 && c == 0) HTRACE(0, 3500 + tb);
@@ -478,7 +439,6 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         if (pt < kDT * kRPC) hand[pt] = __longlong_as_double((long long)hv);
         if (pt == 0) TRACE(5, tb - 1);
         named_bar(2, kPrepThreads);
-#ifndef GCM_EXP_NOX
         {  // + X^T r^{hand} over this warp's share of the 32 rows q
             constexpr int kPerX = (kDT + kPrepWarps - 1) / kPrepWarps;
             const double *X = st + kMXN + kDT * kDT;
@@ -493,7 +453,6 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
                 }
             }
         }
-#endif
 #pragma unroll
         for (int w = 0; w < kRPC; ++w) part[(pw * kDT + j) * kRPC + w] = acc0[w] + acc1[w];
         named_bar(2, kPrepThreads);
@@ -519,15 +478,8 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
     if (warp == kSvcWarp) {  // loader: block tb+3 into stage tb%3 once step tb is under way
         for (int tb = 0; tb + 3 < NT; ++tb) {
             if (lane == 0) {
-#if GCM_LATE_LOAD
-                // after prep(tb+1) is done: the bulk copy's smem writes then overlap the
-                // critical step, not the prep's shared-memory reads
-                while (*prepdone < (unsigned)(tb + 1)) {
-                }
-#else
                 while (*pcount < (unsigned)(kRPC * (tb + 1))) {
                 }
-#endif
             }
             __syncwarp();
             issue_loads(tb + 3);
@@ -576,10 +528,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         } else if (tb + 1 < NT) {
             if (pt == 0) TRACE(2, tb);
             do_prep(tb + 1);
-            if (pt == 0) {
-                TRACE(6, tb);
-                *prepdone = (unsigned)(tb + 1);
-            }
+            if (pt == 0) TRACE(6, tb);
         }
         named_bar(1, kSvcWarp * 32);  // B_{tb+1}: p_tb and prepX_{tb+1} ready
     }
@@ -665,9 +614,9 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
 
     // J2: column strips s = h, h+H, ...
     auto rptr = [&](int i, int s) -> double * {  // residual of owned strip #i (smem or global)
-        return i < kHelpMaxOwn ? rs + i * kDT * KB : a.rcur + (int64_t)s * kDT * k;
+        return i < a.own_cap ? rs + i * kDT * KB : a.rcur + (int64_t)s * kDT * k;
     };
-    auto rstride = [&](int i) { return i < kHelpMaxOwn ? KB : k; };
+    auto rstride = [&](int i) { return i < a.own_cap ? KB : k; };
     int last = -1, i = 0;
     for (int s = h; s < NT; s += H, ++i) {
         last = s;
@@ -710,7 +659,6 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
     double *ring = rs + kHelpMaxOwn * kDT * KB;  // [kHelpRing][kSlot]
     unsigned long long *full = reinterpret_cast<unsigned long long *>(ring + kHelpRing * kSlot);
     unsigned long long *empty = full + kHelpRing;
-    volatile int *pmode = reinterpret_cast<volatile int *>(empty + kHelpRing);  // [kHelpRing] 1: P not copied
     if (t == 0) {
         for (int i = 0; i < kHelpRing; ++i) {
             mbar_init(full + i, 33u);  // 1 noinc arrival per feeder lane (L batch) + the P bulk copy's arrive
@@ -728,11 +676,11 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
         for (int i = 0; i < kHelpRing; ++i) slot_row[i] = -1;
         // each publication is a release (the feeder stalls until the checkpoints are out), so
         // publish every 64 rows for KB = 16 and every 128 for smaller ranks (same-box A/B)
-        constexpr int kPubEvery = GCM_PUB_EVERY >= 0 ? GCM_PUB_EVERY : (KB >= 16 ? 1 : 3);
+        constexpr int kPubEvery = KB >= 16 ? 1 : 3;
         auto publish = [&](int rows) {
             if (lane == 0) st_release64(a.hprog + h, ((unsigned long long)a.epoch << 32) | (unsigned)rows);
         };
-        int seq = 0, known = 0;
+        int seq = 0;
         for (It it{0, first_owned_after(0)}; valid(it); advance(it), ++seq) {
             const int slot = seq % kHelpRing, use = seq / kHelpRing;
             if (use > 0) mbar_wait(empty + slot, (unsigned)((use - 1) & 1));
@@ -753,28 +701,6 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
                 if (lane == 0) mbar_arrive(full + slot);
                 continue;
             }
-            if (GCM_FEEDER_POLL == 1 && lane < a.NC) {  // wait until each chain's last row of P_tb is visible
-                const double *q = a.pfast + ((int64_t)it.tb * kDT + kDT - 1) * k + min(k - 1, kRPC * lane + 1);
-                while (ld_relaxed_u64(q) == kEmpty) __nanosleep(GCM_POLL_NS);
-            }
-            if (GCM_FEEDER_POLL == 2 && it.tb >= known) {
-                // one look (no waiting) at each chain's last row of P_tb: a block that is already
-                // out is bulk-copied (a helper catching up gets complete tiles); a fresh one is
-                // left to the compute warps, which poll pfast directly (one round trip after it lands)
-                unsigned long long u = 0ull;
-                if (lane < a.NC)
-                    u = ld_relaxed_u64(a.pfast + ((int64_t)it.tb * kDT + kDT - 1) * k + min(k - 1, kRPC * lane + 1));
-                if (__all_sync(kFull, u != kEmpty)) known = it.tb + 1;
-            }
-            __syncwarp();
-            if (GCM_FEEDER_POLL == 2 && it.tb >= known) {
-                if (lane == 0) {
-                    pmode[slot] = 1;
-                    mbar_arrive(full + slot);
-                }
-                continue;
-            }
-            if (GCM_FEEDER_POLL == 2 && lane == 0) pmode[slot] = 0;
             if (lane == 0) {  // P_tb (32 x k, contiguous) from pfast with one bulk copy; values still
                               // empty on arrival are polled by the compute warps
                 asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -818,7 +744,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
         const bool chain_handoff = (tb + 1 == s - kLookC);
         const int b64 = (tb + 1) / 2, s64 = s / 2;
         const bool checkpoint = ((tb + 1) % 2 == 0) && b64 < s64 && (b64 & (a.CI - 1)) == 0;
-        const bool direct = fast_tile(tb, s) || (GCM_FEEDER_POLL == 2 && pmode[slot] == 1);
+        const bool direct = fast_tile(tb, s);
         if (!direct) {  // bulk-copied P_tb: poll the values that were still empty
             double *Pw = const_cast<double *>(Pt);
             const double *src = a.pfast + (int64_t)tb * kDT * k;
@@ -997,22 +923,17 @@ __device__ __forceinline__ void warp_chol_inv(double (&a)[KB], double *out) {
 }
 
 // ---------------------------------------------------------------- Gram CTA
-// Accumulates G = P^T P block by block as the chains publish P (warps 0..3), stores the
-// prefix G_b at every 64-row boundary, and the other warps turn each G_b into
-// U_b^{-1} (chol_lower(I + sigma G_b), inverted) -- so the diagonal sweeps and the
-// Apply tiles find U_b^{-1} ready when the solve ends (no Gram/scan kernels).
-// U_b^{-1} is formed by the diagonal sweep's coefficient warp (in parallel over blocks, while
-// the column threads form w); one Gram-CTA warp per block could not keep pace with the chains.
-__host__ __device__ constexpr bool gram_chol_here(int KB) { return GCM_GRAM_CHOL && KB <= 16; }
+// Accumulates G = P^T P block by block as the helpers publish per-block Grams (warps 0..3)
+// and stores the prefix G_b at every 64-row boundary (no Gram/scan kernels).  U_b^{-1}
+// (chol_lower(I + sigma G_b), inverted) is formed by block b's diagonal sweep in its
+// coefficient warp (in parallel over blocks, while the column threads form w): one
+// Gram-CTA warp per block could not keep pace with the chains.
 
 template <int KB>
 __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const int k = a.k;
+    const int t = threadIdx.x, warp = t >> 5;
     const int NB = (int)((a.n + kD - 1) / kD);
     constexpr int kAccT = 128;
-    volatile int *gready = reinterpret_cast<volatile int *>(smem);
-    if (t == 0) *gready = 0;
     for (int o = t; o < KB * KB; o += blockDim.x) a.Ui[o] = (o / KB == o % KB) ? 1.0 : 0.0;  // U_0 = I
     __syncthreads();
     if (t == 0) {
@@ -1045,45 +966,12 @@ __device__ void trsv_gram(const TrsvArgs &a, double *smem) {
                 }
                 named_bar(1, kAccT);
                 if (t == 0) {
-                    __threadfence_block();
-                    *gready = bn;
-                    if (!gram_chol_here(KB)) {  // the sweep inverts G_b itself
-                        __threadfence();
-                        st_release(a.uflag + bn, a.epoch);
-                    }
+                    __threadfence();
+                    st_release(a.uflag + bn, a.epoch);
                 }
             }
         }
         return;
-    }
-    // U_b^{-1} warps: block bn by warp 4 + (bn - 1) % nw (for KB = 32 the inversion is too
-    // slow to keep pace with the chains; the diagonal kernel does it, see gram_chol_here)
-    if (!gram_chol_here(KB)) return;
-    const int nw = (int)(blockDim.x >> 5) - kAccT / 32, cw = warp - kAccT / 32;
-    const double sg = a.sigma > 0 ? 1.0 : -1.0;
-    for (int bn = 1 + cw; bn < NB; bn += nw) {
-        if (lane == 0)
-            while (*gready < bn) __nanosleep(256);  // a tight spin would flood the MIO queue the
-                                                     // computing warp's shuffles go through
-        __syncwarp();
-        __threadfence_block();
-#ifdef GCM_SWEEP_TRACE
-        if (lane == 0 && bn < 500) gcm_sweep_trace[1536 + bn] = clock64();
-#endif
-        const double *Gb = a.G + (int64_t)bn * KB * KB;
-        double row[KB];
-#pragma unroll
-        for (int j = 0; j < KB; ++j)
-            row[j] = (lane < k && j < k) ? (lane == j ? 1.0 : 0.0) + sg * Gb[lane * KB + j] : (lane == j ? 1.0 : 0.0);
-        warp_chol_inv<KB>(row, a.Ui + (int64_t)bn * KB * KB);
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence();
-            st_release(a.uflag + bn, a.epoch);
-        }
-#ifdef GCM_SWEEP_TRACE
-        if (lane == 0 && bn < 500) gcm_sweep_trace[1024 + bn] = clock64();
-#endif
     }
 }
 
@@ -1096,8 +984,8 @@ constexpr int kDiagNQ = GCM_DIAG_NQ;  // threads per column in the diagonal swee
 constexpr int kDiagThreads = 4 * kD + 32;  // up to 4 column parts + the coefficient warp
 static_assert(kDiagNQ == 1 || kDiagNQ == 2 || kDiagNQ == 4, "kDiagNQ * kD + 32 <= kDiagThreads");
 
-// The sweep of diagonal block b by one CTA of kDiagThreads threads (a bdiag_kernel CTA,
-// or a TRSV helper in worker mode: then P is read from the self-validating copy).
+// The sweep of diagonal block b by one CTA of kDiagThreads threads (a TRSV helper in
+// worker mode; P is read from the self-validating copy when p_poll).
 template <int KB>
 __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, double *__restrict__ V, int k, int sigma,
                            const double *__restrict__ P, bool p_poll, double *__restrict__ Ui,
@@ -1120,11 +1008,9 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1000] = clock64();
 #endif
 
-    // U_b^{-1}: computed by the TRSV kernel's Gram CTA from G_b (KB <= 16), else here by
-    // the coefficient warp (idle until the sweep) while the column threads form w
+    // U_b^{-1} from G_b, by the coefficient warp (idle until the sweep) while the column
+    // threads form w
     double *Uis = reinterpret_cast<double *>(M);  // [KB][KB] in the (KB x KB+1) slot
-    if (gram_chol_here(KB))
-        for (int o = t; o < KB * KB; o += kDiagThreads) Uis[o] = Ui[(int64_t)b * KB * KB + o];
     {  // every load in flight before the first use (one memory latency, not one per element)
         constexpr int kLI = (kD * kD + kDiagThreads - 1) / kDiagThreads;
         double lv[kLI];
@@ -1181,7 +1067,7 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
 #ifdef GCM_SWEEP_TRACE
         if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1005] = clock64();
 #endif
-    } else if (!gram_chol_here(KB)) {
+    } else {
 
         const int lane = t & 31;
         if (b == 0) {
@@ -1232,15 +1118,6 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
     }
 }
 
-template <int KB>
-__global__ void __launch_bounds__(kDiagThreads) bdiag_kernel(double *__restrict__ L, int64_t n, int64_t ldl,
-                                                   double *__restrict__ V, int k, int sigma,
-                                                   const double *__restrict__ P, double *__restrict__ Ui,
-                                                   const double *__restrict__ G, double *__restrict__ panels,
-                                                   unsigned long long *key, int64_t ebase) {
-    extern __shared__ double smem_bdiag[];
-    bdiag_body<KB>(L, n, ldl, V, k, sigma, P, false, Ui, G, panels, key, ebase, blockIdx.x, smem_bdiag);
-}
 
 
 // One CTA per (checkpoint segment g, 64-column strip s): tiles b in
@@ -1620,16 +1497,22 @@ struct ApplyWait {
     unsigned epoch;
     int H, NT;
 };
-// bounded spin: a lost flag becomes a kernel error (trap), never a hang
+// polite spin (no timeout: every flag waited on is published unconditionally by a CTA of the
+// co-resident TRSV grid, and a trap would poison the whole CUDA context under a debugger or
+// time-slicing; GCM_SPIN_TRAP_NS=<ns> builds a debug variant that traps instead of hanging)
 __device__ __forceinline__ void spin_wait(bool (*ok)(const void *, unsigned, int), const void *p, unsigned epoch,
                                           int need) {
+#ifdef GCM_SPIN_TRAP_NS
     long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
     while (!ok(p, epoch, need)) {
         __nanosleep(256);
+#ifdef GCM_SPIN_TRAP_NS
         long long t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (t1 - t0 > 4000000000ll) __trap();  // 4 s
+        if (t1 - t0 > (long long)(GCM_SPIN_TRAP_NS)) __trap();
+#endif
     }
 }
 __device__ bool flag_ok(const void *p, unsigned epoch, int) { return ld_acquire((const unsigned *)p) == epoch; }
@@ -1678,34 +1561,17 @@ __device__ void trsv_worker(const TrsvArgs &a, double *smem, unsigned long long 
     __syncthreads();
     if (t < 2 * kHelpRing)
         asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(ring_bars + t)) : "memory");
-    constexpr int kGS = t2_strips(KB);  // 64-column strips per Apply tile
     for (;;) {
         __syncthreads();
         if (t == 0) {
             const unsigned task = atomicAdd(a.taskctr, 1u) + 1u;  // armed to all-ones: first ticket 0
-            // tickets: the NB sweeps first (block order; they sit on the critical path), then the
-            // Apply tiles (b, g) in block order -- an Apply tile only waits on a sweep already handed out
-            int bb = 0, gg = -1;
-            if (task < (unsigned)NB) {
-                bb = (int)task;
-            } else {
-                unsigned o = NB;
-                for (; bb < NB; ++bb) {
-                    const unsigned cnt = a.fuse_apply ? (unsigned)((NB - 1 - bb + kGS - 1) / kGS) : 0u;
-                    if (task < o + cnt) {
-                        gg = (int)(task - o);
-                        break;
-                    }
-                    o += cnt;
-                }
-            }
-            s_task = bb < NB && a.fuse ? (unsigned)bb | ((unsigned)(gg + 1) << 16) : 0xffffffffu;
+            s_task = task < (unsigned)NB ? task : 0xffffffffu;  // tickets in block order
         }
         __syncthreads();
         const unsigned task = s_task;
         if (task == 0xffffffffu) break;
-        const int b = (int)(task & 0xffff), g = (int)(task >> 16) - 1;
-        if (g < 0) {  // the diagonal sweep of block b
+        const int b = (int)task;
+        {  // the diagonal sweep of block b
             if (t == 0) {
 #ifdef GCM_TRACE
                 g_htrace[(1000 + b) * 8 + 0] = gtime();
@@ -1734,26 +1600,6 @@ __device__ void trsv_worker(const TrsvArgs &a, double *smem, unsigned long long 
                     st_release(a.bflag + b, a.epoch);
                 }
             }
-        } else {  // Apply tile (b, 64-column strips s0 .. s0 + kGS - 1)
-            const int s0 = b + 1 + kGS * g;
-            if (t == 0) {
-                while (ld_acquire(a.bflag + b) != a.epoch) __nanosleep(128);
-                const int slo = 2 * s0, shi = min(NT, 2 * (s0 + kGS));
-                for (int s32 = slo; s32 < shi; ++s32) {  // owners past tile rows 2b, 2b+1 (checkpoint + L reads)
-                    const unsigned long long *hp = a.hprog + s32 % a.H;
-                    for (;;) {
-                        const unsigned long long v = ld_acquire64(hp);
-                        if ((unsigned)(v >> 32) == a.epoch && (int)(unsigned)v >= 2 * b + 2) break;
-                        __nanosleep(128);
-                    }
-                }
-                for (int tb = 2 * b + 2; tb <= min(NT - 1, 2 * b + 1 + kLookC); ++tb)  // J1 reads of rows of block b
-                    while (ld_acquire(a.lflag + tb) != a.epoch) __nanosleep(64);
-            }
-            __syncthreads();
-            if (t < kT2Threads)
-                btma_body<KB>(a.tm2, a.n, a.k, a.chk, a.Ui, a.panels, NB, b, s0,
-                              reinterpret_cast<unsigned char *>(smem), 3);
         }
     }
 }
@@ -1819,8 +1665,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.CIlog = 0;
     while ((1 << a.CIlog) < lay.CI) ++a.CIlog;
     unsigned *flags = reinterpret_cast<unsigned *>(wsbase + lay.flags);
-    a.prog = reinterpret_cast<unsigned long long *>(flags);
-    a.lflag = flags + 2 * 16 * kProgStride;
+    a.lflag = flags;
     a.qflag = a.lflag + lay.NT;
     a.Q = reinterpret_cast<double *>(wsbase + lay.Q);
     a.epoch = epoch;
@@ -1832,24 +1677,22 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     a.ebase = ebase;
     a.uflag = a.qflag + lay.NT;
     a.taskctr = reinterpret_cast<unsigned *>(a.pfast + (size_t)lay.NT * kDT * k);
-    // diagonal sweeps fused for every rank (KB = 32 alone: 1.39 ms at k = 64 with the sweeps
-    // after the solve, 1.17 ms fused with the overlapped Apply -- same-box A/B)
-    a.fuse = GCM_FUSE_DIAG && (KB <= 16 || GCM_FUSE_KB32);
+    // the diagonal sweeps always run inside the TRSV kernel (worker mode; KB = 32 alone:
+    // 1.39 ms at k = 64 with the sweeps after the solve, 1.17 ms fused -- same-box A/B)
     a.bflag = a.uflag + lay.NB;
     a.hprog = reinterpret_cast<unsigned long long *>(wsbase + lay.hprog);
-    // Fused Apply tiles (GCM_FUSE_APPLY=1) are correct but measured slower (0.52 vs 0.43 ms at
-    // n=5000, k=16): their 200 MB stream competes with the helpers' latency-bound tile loads
-    // and stretches the chain by half; by default the Apply runs as btma_kernel afterwards.
-    a.fuse_apply = GCM_FUSE_APPLY && a.fuse && lay.NB > 1 && lay.CI == 1 && a.bulk_ok &&
-                   encode_tmap(&a.tm2, L, n, ldl, (unsigned)kT2Rows, (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B);
-    // Overlapped Apply (default for fused sweeps): btma_kernel is launched as a programmatic
-    // dependent of the TRSV kernel and takes SMs as TRSV CTAs exit, each tile waiting on its
-    // sweep's flag and the strip owners' progress -- so the Apply of the early blocks runs
-    // under the last diagonal sweeps instead of after them.
+    a.own_cap = help_max_own(KB);
+    if (const char *e = std::getenv("GCM_HELP_OWN_CAP")) a.own_cap = std::max(0, std::min(a.own_cap, std::atoi(e)));
+    // Overlapped Apply: btma_kernel is launched as a programmatic dependent of the TRSV
+    // kernel and takes SMs as TRSV CTAs exit, each tile waiting on its sweep's flag and the
+    // strip owners' progress -- so the Apply of the early blocks runs under the last
+    // diagonal sweeps instead of after them.  (Apply tiles as worker tickets inside the
+    // TRSV kernel were measured slower, 0.52 vs 0.43 ms at n=5000, k=16: their 200 MB
+    // stream competes with the helpers' latency-bound tile loads.)
     CUtensorMap tm2;
-    const bool pdl = GCM_PDL_APPLY && a.fuse && !a.fuse_apply && lay.NB > 1 && lay.CI == 1 && a.bulk_ok &&
+    const bool pdl = lay.NB > 1 && lay.CI == 1 && a.bulk_ok &&
                      encode_tmap(&tm2, L, n, ldl, (unsigned)kT2Rows, (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B);
-    a.publish = a.fuse_apply || pdl;
+    a.publish = pdl;
     a.G = reinterpret_cast<double *>(wsbase + lay.G);
     a.Ui = reinterpret_cast<double *>(wsbase + lay.U);
     a.sigma = sigma;
@@ -1865,7 +1708,6 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
                                       4 * kD * KB + kD) *
                              sizeof(double);
     size_t smem = std::max(std::max(smem_chain, smem_help), smem_diag);
-    if (a.fuse_apply) smem = std::max(smem, t2_smem_bytes(KB));
     st = check_cuda(cudaFuncSetAttribute(trsv_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (st != GCM_OK) return st;
     int per_sm = 0;
@@ -1876,9 +1718,9 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (grid <= a.NC + 1) return GCM_ECUDA;
     a.H = grid - a.NC - 1;
     void *args[] = {&a};
-    // hand-off slots start empty (all-ones); consumers re-arm what they read
-    st = check_cuda(cudaMemsetAsync(a.rchain, 0xff,
-                                    lay.pfast - lay.rchain + ((size_t)lay.NT * kDT * k + 1) * sizeof(double), stream));
+    // hand-off slots, pfast, the ticket counter, flags and progress words: all-ones (see
+    // make_layout; hand-off consumers also re-arm what they read)
+    st = check_cuda(cudaMemsetAsync(wsbase + lay.rchain, 0xff, lay.MX - lay.rchain, stream));
     if (st != GCM_OK) return st;
     double *U = reinterpret_cast<double *>(wsbase + lay.U);
     double *panels = reinterpret_cast<double *>(wsbase + lay.panels);
@@ -1913,31 +1755,11 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     }
     if (st != GCM_OK) return st;
 
-    if (!a.fuse) {  // else the diagonal sweeps ran inside trsv_kernel (worker mode)
-        st = check_cuda(
-            cudaFuncSetAttribute(bdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_diag));
-        if (st != GCM_OK) return st;
-        ProfScope ps("bdiag", stream);
-        bdiag_kernel<KB><<<lay.NB, kDiagThreads, smem_diag, stream>>>(L, n, ldl, V, k, sigma, a.P, U, a.G, panels,
-                                                                      key, ebase);
-    }
-    if (lay.NB > 1 && !a.fuse_apply) {
+    if (lay.NB > 1) {  // the Apply after the TRSV kernel (unaligned L or CI > 1)
         const size_t smem_apply = (size_t)(2 * kD * KB + kD + KB + KB * KB + 2 * kD * kLdC) * sizeof(double);
         st = check_cuda(
             cudaFuncSetAttribute(bapply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_apply));
         if (st != GCM_OK) return st;
-        if (lay.CI == 1 && a.bulk_ok &&
-            encode_tmap(&tm2, L, n, ldl, (unsigned)kT2Rows, (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B)) {
-            const size_t smem_t2 = t2_smem_bytes(KB);
-            st = check_cuda(cudaFuncSetAttribute(btma_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem_t2));
-            if (st != GCM_OK) return st;
-            const dim3 gridt(lay.NB - 1, (lay.NB - 1 + t2_strips(KB) - 1) / t2_strips(KB));
-            ProfScope ps("bapply", stream);
-            btma_kernel<KB><<<gridt, kT2Threads, smem_t2, stream>>>(tm2, n, k, a.chk, U, panels, lay.NB,
-                                                                    ApplyWait{nullptr, nullptr, nullptr, 0u, 1, 1});
-            return check_cuda(cudaGetLastError());
-        }
         if (lay.CI == 1) {
             const size_t smem_tile =
                 (size_t)(2 * kD * KB + kD + KB + KB * KB + 2 * kStripsPerCta * kD * kLdC) * sizeof(double);
@@ -1992,7 +1814,9 @@ gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_
             lay = make_layout(n, kc, budget);
         }
         if (lay.total > cap) return GCM_ENOMEM;
-        const unsigned epoch = ++ws->epoch;
+        // flags are armed to all-ones each pass: the epoch is never 0 or all-ones
+        if (++ws->epoch == 0xffffffffu) ws->epoch = 1;
+        const unsigned epoch = ws->epoch;
         double *Vc = V + e0 * n;
         if (kc <= 4) st = blocked_pass<4>(L, n, ldl, Vc, kc, sigma, key, e0, base, lay, epoch, stream);
         else if (kc <= 8) st = blocked_pass<8>(L, n, ldl, Vc, kc, sigma, key, e0, base, lay, epoch, stream);

@@ -41,6 +41,8 @@ struct Workspace {
 gcm_status_t get_workspace(cudaStream_t stream, size_t bytes, size_t nkeys, Workspace **ws);
 
 gcm_status_t check_cuda(cudaError_t e);
+// consume an error a previous failed call left behind (called at every ABI entry point)
+void clear_stale_error();
 
 // Profiling hook (gcm_profile_enable): bracket a launch with events on `stream`.
 // Usage: { ProfScope ps("trsv", stream); kernel<<<..., stream>>>(...); }

@@ -1,0 +1,186 @@
+"""GPU parity on the edges of the method, through the C-ABI, against the oracle.
+
+* the helper residual-spill branch of the blocked path (strip residuals beyond what a
+  TRSV helper keeps in shared memory round-trip through global memory): by default it is
+  only reached at n > ~50k (rank bucket 32) / ~107k (rank buckets <= 16), so
+  GCM_HELP_OWN_CAP lowers the shared-memory cap and drives it at oracle sizes;
+* near-singular but feasible downdates (sigma = -1, PAPER.md 20-21, the paper's downdate
+  experiment at line 111; no epsilon in the failure test, SPEC.md 184): the update vector
+  is (1 - delta) times a row of the factor, so the downdated matrix keeps a pivot of
+  relative size sqrt(2 delta).  The tolerance follows DESIGN.md reading R19: the
+  relative condition number of a downdate is 1/rho^2, rho^2 = lambda_min(I - P^T P),
+  P = L^{-T} V (Stewart 1979; SURVEY 8(c) P12 "downdate amplification"), so two correct
+  fp64 implementations may differ by O(eps / rho^2);
+* NaN inputs: the failure report must name the same lexicographically first (e, i) as
+  k sequential rank-1 oracle calls (R5, R6), whichever path runs.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gcm_testutil import col_scaled_max, rel_fro, row_scaled_max, upper
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(np.float64).eps
+
+
+@pytest.fixture(scope="module")
+def gcm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1011_1173_b200 as g
+    return g
+
+
+def _gpu(gcm, Lbuf, Vbuf, sigma, algo="auto"):
+    dev = torch.device("cuda")
+    L = torch.from_numpy(Lbuf).to(dev)
+    V = torch.from_numpy(Vbuf).to(dev)
+    info = gcm.new_info(dev)
+    gcm.modify(L, V, sigma, info=info, algo=algo)
+    torch.cuda.synchronize()
+    return L.cpu().numpy(), V.cpu().numpy(), gcm.read_info(info)[0]
+
+
+def _ora(Lbuf, Vbuf, sigma):
+    Lo, Vo = Lbuf.copy(), Vbuf.copy()
+    _, _, oi = oracle.modify_a(Lo, Vo, sigma)
+    return Lo, Vo, (oi.code, oi.col, oi.row)
+
+
+# ------------------------------------------------------------------ spill branch
+@pytest.mark.parametrize("cap", [0, 1])
+@pytest.mark.parametrize("n,k", [(1000, 4), (1000, 16), (2113, 32), (1300, 40)])
+@pytest.mark.parametrize("sigma", [1, -1])
+def test_helper_spill_path(gcm, monkeypatch, cap, n, k, sigma):
+    """cap = 0: every owned strip's residual lives in global memory (rcur); cap = 1: only
+    the first.  Rank buckets 4, 16 (KB <= 16) and 32 (KB = 32, and k = 40 = 32 + 8)."""
+    monkeypatch.setenv("GCM_HELP_OWN_CAP", str(cap))
+    Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=n + 31 * k + cap, lower_fill=np.nan)
+    Lg, Vg, ig = _gpu(gcm, Lbuf, Vbuf, sigma, algo="blocked")
+    Lo, Vo, io = _ora(Lbuf, Vbuf, sigma)
+    assert ig == io == (0, 0, 0)
+    assert rel_fro(upper(Lg), upper(Lo)) <= 1e-11
+    assert col_scaled_max(upper(Lg), upper(Lo)) <= 1e-12
+    assert row_scaled_max(Vg, Vo) <= 1e-11
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [16, 32])
+def test_helper_spill_path_headline_size(gcm, monkeypatch, k):
+    """n = 5000 (157 strips over ~139 helpers): with cap = 1 the helpers owning two strips
+    keep the first in shared memory and spill the second, as at n = 1e5 by default."""
+    monkeypatch.setenv("GCM_HELP_OWN_CAP", "1")
+    for sigma in (1, -1):
+        Lbuf, Vbuf, _ = synth.paper_instance(5000, k, sigma, seed=synth.SEED_ROOT + k, lower_fill=np.nan)
+        Lg, Vg, ig = _gpu(gcm, Lbuf, Vbuf, sigma)
+        Lo, Vo, io = _ora(Lbuf, Vbuf, sigma)
+        assert ig == io == (0, 0, 0)
+        assert rel_fro(upper(Lg), upper(Lo)) <= 1e-11
+        assert col_scaled_max(upper(Lg), upper(Lo)) <= 1e-12
+
+
+# ------------------------------------------------------------------ near-singular downdates
+def near_singular(n, k, m, delta, seed):
+    """A feasible downdate with relative pivot sqrt(2 delta - delta^2) at row m.  In
+    P = L^{-T} V^T coordinates: column 0 is (1 - delta) e_m (so update vector 0 is
+    (1 - delta) times row m of the upper factor), the other columns are U[0,1) draws
+    scaled by 1/(2 sqrt(nk)) with row m zeroed, so rho^2 = lambda_min(I - P^T P) =
+    1 - (1 - delta)^2 exactly and L~_mm = L_mm sqrt(1 - (1 - delta)^2)."""
+    Lbuf, _, _ = synth.paper_instance(n, k, -1, seed=seed)
+    U = upper(Lbuf)
+    P = synth.uniform(seed, synth.S_VDIRECT, n * k).reshape(n, k) / (2.0 * np.sqrt(n * k))
+    P[m, :] = 0.0
+    P[:, 0] = 0.0
+    P[m, 0] = 1.0 - delta
+    V = np.ascontiguousarray((U.T @ P).T)
+    return Lbuf, V
+
+
+def rho2(Lbuf, V):
+    """lambda_min(I - P^T P), P = L^{-T} V^T: the downdate's distance from indefiniteness."""
+    U = upper(Lbuf)
+    P = np.linalg.solve(U.T, V.T)
+    return float(np.linalg.eigvalsh(np.eye(V.shape[0]) - P.T @ P).min())
+
+
+@pytest.mark.parametrize("algo", ["sweep", "blocked"])
+@pytest.mark.parametrize("delta", [1e-2, 1e-4, 1e-6])
+@pytest.mark.parametrize("n,k,m", [(200, 1, 77), (700, 4, 300), (700, 16, 640)])
+def test_near_singular_downdate(gcm, algo, delta, n, k, m):
+    Lbuf, V = near_singular(n, k, m, delta, seed=n + m)
+    r2 = rho2(Lbuf, V)
+    assert 0 < r2 <= 2 * delta
+    Lg, Vg, ig = _gpu(gcm, Lbuf.copy(), V.copy(), -1, algo=algo)
+    Lo, Vo, io = _ora(Lbuf, V, -1)
+    assert ig == io == (0, 0, 0)
+    # DESIGN.md R19: GPU and oracle may each be O(eps/rho^2) from the exact factor
+    tol = max(1e-11, 64 * np.sqrt(n) * EPS / r2)
+    err = rel_fro(upper(Lg), upper(Lo))
+    assert err <= tol, f"rel-F {err:.3e} > {tol:.3e} (rho^2 = {r2:.2e})"
+    assert col_scaled_max(upper(Lg), upper(Lo)) <= tol
+    assert rel_fro(Vg, Vo) <= 10 * tol
+    # the downdated factor is genuinely near-singular at row m
+    assert abs(Lo[m, m] - np.sqrt(r2) * Lbuf[m, m]) <= 1e-6 * abs(Lo[m, m])
+
+
+@pytest.mark.parametrize("delta", [1e-2, 1e-4, 1e-6])
+def test_near_singular_downdate_batched(gcm, delta):
+    n, k, batch = 300, 8, 3
+    Ls, Vs = [], []
+    for f in range(batch):
+        Lb, V = near_singular(n, k, 50 + 90 * f, delta, seed=900 + f)
+        Ls.append(Lb)
+        Vs.append(V)
+    Ls, Vs = np.stack(Ls), np.stack(Vs)
+    L = torch.from_numpy(Ls).cuda()
+    V = torch.from_numpy(Vs).cuda()
+    info = gcm.new_info("cuda", batch)
+    gcm.modify_batched(L, V, -1, info=info)
+    torch.cuda.synchronize()
+    Lg, Vg, ig = L.cpu().numpy(), V.cpu().numpy(), gcm.read_info(info)
+    for f in range(batch):
+        Lo, Vo, io = _ora(Ls[f], Vs[f], -1)
+        assert ig[f] == io == (0, 0, 0)
+        tol = max(1e-11, 64 * np.sqrt(n) * EPS / rho2(Ls[f], Vs[f]))
+        assert rel_fro(upper(Lg[f]), upper(Lo)) <= tol
+        assert col_scaled_max(upper(Lg[f]), upper(Lo)) <= tol
+
+
+# ------------------------------------------------------------------ NaN inputs
+NAN_CASES = {
+    # where the NaN is put -> what the oracle (k sequential rank-1 sweeps) reports
+    "V entry": lambda L, V: V.__setitem__((2, 100), np.nan),
+    "off-diagonal L": lambda L, V: L.__setitem__((90, 40), np.nan),  # factor entry (40, 90)
+    "diagonal L": lambda L, V: L.__setitem__((70, 70), np.nan),
+}
+
+
+@pytest.mark.parametrize("algo", ["sweep", "blocked"])
+@pytest.mark.parametrize("case", sorted(NAN_CASES))
+@pytest.mark.parametrize("sigma", [1, -1])
+def test_nan_input_reported(gcm, algo, case, sigma):
+    n, k = 300, 4
+    Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=55)
+    NAN_CASES[case](Lbuf, Vbuf)
+    _, _, io = _ora(Lbuf, Vbuf, sigma)
+    assert io[0] in (1, 2)
+    _, _, ig = _gpu(gcm, Lbuf, Vbuf, sigma, algo=algo)
+    assert ig == io, f"{case}: gpu {ig} vs oracle {io}"
+
+
+@pytest.mark.parametrize("case", sorted(NAN_CASES))
+def test_nan_input_reported_batched(gcm, case):
+    n, k, batch = 300, 4, 3
+    Ls, Vs, _ = synth.batched_instances(batch, n, k, 1, seed=77)
+    NAN_CASES[case](Ls[1], Vs[1])  # only factor 1 is poisoned
+    ios = [_ora(Ls[f], Vs[f], 1)[2] for f in range(batch)]
+    L = torch.from_numpy(Ls).cuda()
+    V = torch.from_numpy(Vs).cuda()
+    info = gcm.new_info("cuda", batch)
+    gcm.modify_batched(L, V, 1, info=info)
+    assert gcm.read_info(info) == ios
+    assert ios[0] == ios[2] == (0, 0, 0) and ios[1][0] in (1, 2)

@@ -3,20 +3,25 @@ element on the same seeded inputs.
 
 Tolerances (DESIGN.md "tolerances"): L~ relative Frobenius <= 1e-11 (north_star);
 V_exit relative Frobenius <= 1e-10 (V_exit is the rotated residual, a secondary
-output whose error carries the downdate amplification).
+output whose error carries the downdate amplification).  Beside the
+Frobenius bounds every element is checked: |L~_gpu - L~_cpu|_ij <= 1e-12 ||L~_cpu(:, j)||
+(column-scaled) and |V_gpu - V_cpu|_ej <= 1e-11 max_j |V_cpu(e, j)| (row-scaled), so a
+single wrong tile cannot pass under a large norm.
 """
 import numpy as np
 import pytest
 
 import oracle
 import synth
-from gcm_testutil import rel_fro, upper
+from gcm_testutil import col_scaled_max, rel_fro, row_scaled_max, upper
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TOL_L = 1e-11
 TOL_V = 1e-10
+TOL_L_ELEM = 1e-12  # column-scaled, per element
+TOL_V_ELEM = 1e-11  # row-scaled, per element
 
 
 @pytest.fixture(scope="module")
@@ -47,8 +52,10 @@ def run_both(gcm, n, k, sigma, ldl=None, seed=1, algo="auto", instance="paper"):
 def check(Lg, Vg, ginfo, Lo, Vo, oinfo, n):
     assert ginfo == (oinfo.code, oinfo.col, oinfo.row)
     assert rel_fro(upper(Lg), upper(Lo)) <= TOL_L
+    assert col_scaled_max(upper(Lg), upper(Lo)) <= TOL_L_ELEM
     if Vo.size:
         assert rel_fro(Vg, Vo) <= TOL_V
+        assert row_scaled_max(Vg, Vo) <= TOL_V_ELEM
     # strictly lower part and padding rows are never written (NaN sentinel)
     bad = ~np.tril(np.ones(Lg.shape, bool))
     assert np.all(np.isnan(Lg[bad]))
@@ -219,8 +226,9 @@ def test_parity_checkpoint_interval(gcm, monkeypatch, budget, n, k, sigma):
 @pytest.mark.slow
 @pytest.mark.parametrize("n,k", [(24000, 16), (24000, 32)])
 def test_large_n_properties(gcm, n, k):
-    """Sizes where a strip owner holds more than a handful of strips (n/32/139 > 5) and the
-    oracle is too slow element-wise: full-size pins that hold at any size (SURVEY 8(c) P4,
+    """Sizes where each strip owner holds several strips (n/32/139 ~ 5, all kept in shared
+    memory by default; the spill path is driven by test_gpu_edge.py's GCM_HELP_OWN_CAP cases)
+    and the oracle is slow element-wise: full-size pins that hold at any size (SURVEY 8(c) P4,
     P5) -- the column-norm identity ||L~_{:,c}||^2 = ||L_{:,c}||^2 + sigma ||V_{c,:}||^2 on
     every column, and Freivalds' check L~^T L~ x = L^T L x + sigma V V^T x -- for an update
     and the downdate back (direct-L instance, R18, drawn on the device)."""

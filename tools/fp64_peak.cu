@@ -61,6 +61,7 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
+    double best_tf = 0.0;
     for (int bps = 1; bps <= 8; bps *= 2) {
         const int grid = nsm * bps;
         dfma_tput<<<grid, threads>>>(out, 16, 1.0000001, 1e-9);
@@ -71,18 +72,26 @@ int main() {
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         const double fmas = (double)grid * threads * iters * 16 * 8;
+        if (2 * fmas / ms / 1e9 > best_tf) best_tf = 2 * fmas / ms / 1e9;
         printf("dfma_tput grid=%d (%d CTA/SM x %d thr): %.3f ms  %.2f TFLOP/s (2 flop/FMA)  %.1f FMA/clk/SM at nominal %d MHz\n",
                grid, bps, threads, ms, 2 * fmas / ms / 1e9, fmas / (ms * 1e-3) / nsm / (clk * 1e3), clk / 1000);
     }
     long long h;
     dfma_lat<<<1, 32>>>(out, cyc, iters, 1.0000001, 1e-9);
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
-    printf("dfma dependent latency: %.2f cycles\n", (double)h / (iters * 16));
+    const double lat = (double)h / (iters * 16);
+    printf("dfma dependent latency: %.2f cycles\n", lat);
     const char *names[] = {"compute link (sqrt+div+mul)", "rcp link (add+div)", "rsqrt link (fma+rsqrt)"};
+    double links[3];
     for (int m = 0; m < 3; ++m) {
         link_lat<<<1, 32>>>(out, cyc, 1024, m);
         cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
-        printf("%s: %.1f cycles\n", names[m], (double)h / 1024);
+        links[m] = (double)h / 1024;
+        printf("%s: %.1f cycles\n", names[m], links[m]);
     }
+    // one machine-readable line (bench.py reads the committed copy: profiles/*fp64_peak*.json)
+    printf("{\"fp64_tflops\": %.3f, \"dfma_latency_cycles\": %.2f, \"t_link_compute_cycles\": %.1f, "
+           "\"t_link_rcp_cycles\": %.1f, \"t_link_rsqrt_cycles\": %.1f, \"sm_count\": %d, \"clock_attr_mhz\": %d}\n",
+           best_tf, lat, links[0], links[1], links[2], nsm, clk / 1000);
     return 0;
 }
