@@ -905,12 +905,23 @@ __device__ __forceinline__ void warp_chol_inv(double (&a)[KB], double *out) {
     for (int j = 0; j < KB; ++j) w[j] = (i == j) ? 1.0 : 0.0;
 #pragma unroll
     for (int c = 0; c < KB - 1; ++c) {
+        // rows above the pivot are left untouched (selected, not multiplied by f = 0): a NaN
+        // in a later row (a NaN update column, R5/R6) must not reach the rows of
+        // the earlier update columns through 0 * NaN, or the failure report would name
+        // the wrong (lexicographically smaller) column
+        const bool below = i > c;
         const double rp = 1.0 / __shfl_sync(kFull, a[c], c);
-        const double f = i > c ? a[c] * rp : 0.0;
+        const double f = a[c] * rp;
 #pragma unroll
-        for (int j = c + 1; j < KB; ++j) a[j] = fma(-f, __shfl_sync(kFull, a[j], c), a[j]);
+        for (int j = c + 1; j < KB; ++j) {
+            const double x = __shfl_sync(kFull, a[j], c);
+            if (below) a[j] = fma(-f, x, a[j]);
+        }
 #pragma unroll
-        for (int j = 0; j <= c; ++j) w[j] = fma(-f, __shfl_sync(kFull, w[j], c), w[j]);
+        for (int j = 0; j <= c; ++j) {
+            const double x = __shfl_sync(kFull, w[j], c);
+            if (below) w[j] = fma(-f, x, w[j]);
+        }
     }
     double di = 0.0;
 #pragma unroll
