@@ -115,7 +115,7 @@ def rho2(Lbuf, V):
 def test_near_singular_downdate(gcm, algo, delta, n, k, m):
     Lbuf, V = near_singular(n, k, m, delta, seed=n + m)
     r2 = rho2(Lbuf, V)
-    assert 0 < r2 <= 2 * delta
+    assert 0 < r2 <= 2.01 * delta  # (computed rho^2 carries its own rounding)
     Lg, Vg, ig = _gpu(gcm, Lbuf.copy(), V.copy(), -1, algo=algo)
     Lo, Vo, io = _ora(Lbuf, V, -1)
     assert ig == io == (0, 0, 0)
