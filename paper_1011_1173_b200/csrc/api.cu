@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "tma.cuh"
 
 namespace gcm {
 
@@ -114,6 +115,35 @@ gcm_status_t validate(const double *L, int64_t n, int64_t ldl, const double *V, 
 }
 
 }  // namespace
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool encode_tmap_f64(CUtensorMap *m, const void *base, int rank, int64_t rows, int64_t cols, int64_t ldl,
+                     int64_t batch, int64_t strideL, unsigned box_rows, unsigned box_cols, CUtensorMapSwizzle swz,
+                     CUtensorMapDataType dtype, int esize) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p) {
+            clear_stale_error();
+            return false;
+        }
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    if (rank != 2 && rank != 3) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)rows, (cuuint64_t)cols, (cuuint64_t)batch};
+    const cuuint64_t strides[2] = {(cuuint64_t)ldl * esize, (cuuint64_t)strideL * esize};
+    const cuuint32_t box[3] = {box_rows, box_cols, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, dtype, (cuuint32_t)rank, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     if (algo != GCM_ALGO_AUTO) return algo;

@@ -30,13 +30,13 @@
 //   btile_kernel / bapply_kernel: the Apply as a plain launch after the TRSV kernel
 //                 (unaligned L or odd ldl, or checkpoint interval CI > 1).
 #include <cooperative_groups.h>
-#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 
 #include <algorithm>
 #include <cstdlib>
 
 #include "internal.h"
 #include "rot.cuh"
+#include "tma.cuh"
 
 namespace gcm {
 
@@ -290,33 +290,6 @@ __device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred P;\n WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-        " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
-__device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, unsigned bytes, unsigned long long *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(smem_dst)),
-                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
 // Shared-memory plan of a chain CTA (doubles).  A "stage" holds block tb's
 // precomputed operands (N, M^T, X: one bulk copy of kMXStride doubles); three
 // stages rotate.
@@ -445,7 +418,10 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
 #pragma unroll
             for (int u = 0; u < kPerX; ++u) {
                 const int q = pw * kPerX + u;
-                if (q < kDT) {
+                // X = L_tb,tb^{-1} is upper triangular: X(q, j) = 0 for q > j is skipped, not
+                // multiplied -- a NaN residual of a later row must not reach row j (0 * NaN),
+                // or a NaN input would be reported at an earlier row (R5, R6)
+                if (q <= j) {
                     const double x = X[q * kDT + j];
                     const double2 hvv = *reinterpret_cast<const double2 *>(hand + q * kRPC);
                     acc0[0] = fma(x, hvv.x, acc0[0]);
@@ -566,7 +542,8 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
             for (int j = kDT - 1; j >= 0; --j) {
                 double s = (j == c) ? 1.0 : 0.0;
 #pragma unroll
-                for (int m = j + 1; m < kDT; ++m) s = fma(-Lb[m * kLdT + j], m <= c ? x[m] : 0.0, s);
+                for (int m = j + 1; m < kDT; ++m)
+                    if (m <= c) s = fma(-Lb[m * kLdT + j], x[m], s);  // skipped, not times 0 (NaN inputs)
                 x[j] = j <= c ? s / Lb[j * kLdT + j] : 0.0;
             }
 #pragma unroll
@@ -589,23 +566,23 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
         __syncthreads();
         double *mx = a.MX + (int64_t)tb * kMXStride;
         for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
-            const int m = idx / kDT, j = idx % kDT;  // M(j, m) = sum_q X(q, j) L(m, q)
+            const int m = idx / kDT, j = idx % kDT;  // M(j, m) = sum_{q <= j} X(q, j) L(m, q)
+            // X is upper triangular: the q > j terms are skipped, not multiplied by zero, so a
+            // NaN entry of a later column cannot reach row j (R5, R6)
             double s0 = 0.0, s1 = 0.0;
-#pragma unroll 8
-            for (int q = 0; q < kDT; q += 2) {
+            for (int q = 0; q <= j; q += 2) {
                 s0 = fma(Xs[q * kLdT + j], Lb[q * kLdT + m], s0);
-                s1 = fma(Xs[(q + 1) * kLdT + j], Lb[(q + 1) * kLdT + m], s1);
+                if (q + 1 <= j) s1 = fma(Xs[(q + 1) * kLdT + j], Lb[(q + 1) * kLdT + m], s1);
             }
             mx[kMXN + m * kDT + j] = s0 + s1;                        // M^T row-major: (m, j)
             mx[kMXN + kDT * kDT + m * kDT + j] = Xs[m * kLdT + j];   // X row-major: (q=m, j)
         }
         for (int idx = t; idx < kDT * kSeg; idx += kTrsvThreads) {
-            const int j = idx / kSeg, R = idx % kSeg;  // N(j, R) = sum_q X(q, j) L(rs + R, q)
+            const int j = idx / kSeg, R = idx % kSeg;  // N(j, R) = sum_{q <= j} X(q, j) L(rs + R, q)
             double s0 = 0.0, s1 = 0.0;
-#pragma unroll 8
-            for (int q = 0; q < kDT; q += 2) {
+            for (int q = 0; q <= j; q += 2) {
                 s0 = fma(Xs[q * kLdT + j], sg[q * kLdN + R], s0);
-                s1 = fma(Xs[(q + 1) * kLdT + j], sg[(q + 1) * kLdN + R], s1);
+                if (q + 1 <= j) s1 = fma(Xs[(q + 1) * kLdT + j], sg[(q + 1) * kLdN + R], s1);
             }
             mx[j * kLdN + R] = s0 + s1;
         }
@@ -1354,21 +1331,6 @@ __host__ __device__ constexpr size_t t2_smem_bytes(int KB) {
            ((size_t)panel_doubles(KB) + KB * KB) * 8 + 8 * (2 * kT2Stages + 1);
 }
 
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int c0, int c1,
-                                            unsigned long long *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, int c0, int c1, const void *src) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                     reinterpret_cast<uint64_t>(tm)),
-                 "r"(c0), "r"(c1), "r"(smem_u32(src))
-                 : "memory");
-}
-
 // Apply of panel b to the 64 x 256 tile at 64-column strip s0 by threads 0..kT2Threads-1
 // (a btma_kernel CTA, or a TRSV helper in worker mode: then `bar` is a named barrier id
 // for those threads only; tm must be a __grid_constant__ parameter).
@@ -1631,29 +1593,9 @@ __global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_cons
     }
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 bool encode_tmap(CUtensorMap *m, const double *L, int64_t n, int64_t ldl, unsigned box_rows, unsigned box_cols,
                  CUtensorMapSwizzle swz) {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void *p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !p)
-            return false;
-        fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
-    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
-    const cuuint64_t strides[1] = {(cuuint64_t)ldl * sizeof(double)};
-    const cuuint32_t box[2] = {box_rows, box_cols};
-    const cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(L), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return encode_tmap_f64(m, L, 2, n, n, ldl, 1, 0, box_rows, box_cols, swz);
 }
 
 template <int KB>

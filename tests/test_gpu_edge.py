@@ -158,6 +158,7 @@ NAN_CASES = {
     # where the NaN is put -> what the oracle (k sequential rank-1 sweeps) reports
     "V entry": lambda L, V: V.__setitem__((2, 100), np.nan),
     "off-diagonal L": lambda L, V: L.__setitem__((90, 40), np.nan),  # factor entry (40, 90)
+    "in-block L": lambda L, V: L.__setitem__((90, 70), np.nan),  # factor entry (70, 90): same 32/64-row block
     "diagonal L": lambda L, V: L.__setitem__((70, 70), np.nan),
 }
 
