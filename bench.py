@@ -378,6 +378,12 @@ def kernel_units(name, n, k, batch, per_step=1):
                 "flops": 6 * kp * n * (n - 1) / 2,
                 "what": f"one pass of {kp:g} update columns (TRSV + fused sweeps + overlapped Apply): upper "
                         "triangle read+write once + V; 6 flops per Apply"}
+    if name == "ptrsv":  # panel algorithm's right-looking solve: the triangle read once, k FMA per element
+        return {"bound": "alu" if kp >= 16 else "hbm", "bytes": tri + 16 * n * kp, "flops": n * n * kp,
+                "what": "column-block solve + residual updates: L triangle read once, n^2 k flops (2 per FMA)"}
+    if name == "papply":  # panel algorithm's Apply: every tile read+written once, 6 flops per Apply
+        return {"bound": "hbm" if kp < 16 else "alu", "bytes": 2 * tri, "flops": 6 * kp * n * (n - 1) / 2,
+                "what": "upper triangle read+write once (off-diagonal tiles); 6 flops per Apply"}
     if name == "trsv":  # reads the triangle once for P = L^-T V (k FMA per element)
         return {"bound": "hbm", "bytes": tri + 16 * n * kp, "flops": n * n * kp,
                 "what": "L triangle read once + V read + P write; n^2 k flops"}
@@ -494,7 +500,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="n5000_k16")
-    ap.add_argument("--algo", choices=["auto", "sweep", "blocked"], default="auto")
+    ap.add_argument("--algo", choices=["auto", "sweep", "blocked", "panel"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -73,8 +73,11 @@ typedef struct {
 typedef enum {
     GCM_ALGO_AUTO = 0,     /* library's choice for the shape          */
     GCM_ALGO_SWEEP = 1,    /* per-row-block launches: diagonal chain, then Apply panel */
-    GCM_ALGO_BLOCKED = 2   /* chain-shortened: block-parallel diagonal sweeps seeded by
+    GCM_ALGO_BLOCKED = 2,  /* chain-shortened: block-parallel diagonal sweeps seeded by
                               P = L^{-T} V             */
+    GCM_ALGO_PANEL = 3     /* the column-sharded algorithm of gcm_modify_dist on one GPU:
+                              right-looking column blocks of 512, separate Apply
+                              (large n)                   */
 } gcm_algo_t;
 
 /* In-place rank-k modification L~^T L~ = L^T L + sigma V V^T.
@@ -124,11 +127,16 @@ gcm_status_t gcm_modify_batched(double *L, int64_t n, int64_t ldl, int64_t strid
  * of columns this rank owns; V_local holds the V rows of those columns
  * (n_local x k, ld n_local), overwritten with their V_exit rows.  Every rank
  * calls gcm_modify_dist with identical (n, nb, k, sigma); it is collective.
- * nb must be a positive multiple of 64 (the panel height), else GCM_EINVAL.
- * Per 64-row block the owner of its columns runs the diagonal Compute chain and
- * one ncclBroadcast (root = owner) ships its coefficient panel; every rank then
- * applies it to its own columns.  d_info (device, nullable) receives the global
- * first failure on every rank.  Built without NCCL: GCM_ENOTSUP. */
+ * nb must be a positive multiple of 64 (a multiple of 256 lets the Apply use
+ * 256-column TMA tiles), nranks <= 8, n < 2^31, else GCM_EINVAL.
+ * Algorithm (PAPER.md 24-30/44-54 restated as in
+ * GCM_ALGO_BLOCKED): per column block the owner solves its rows of P = L^{-T} V,
+ * which reach every rank (ncclBroadcast here; device-initiated stores in the
+ * virtual-rank entry below), every rank updates its own residuals; then each
+ * rank sweeps its own diagonal blocks, the coefficient panels reach every rank,
+ * and every rank applies them to its own tiles.  d_info (device, nullable)
+ * receives the global first failure on every rank.  Built without NCCL:
+ * GCM_ENOTSUP. */
 typedef struct gcm_comm *gcm_comm_t;
 gcm_status_t gcm_comm_unique_id(void *host_id_out /* 128 bytes */);
 gcm_status_t gcm_comm_init(gcm_comm_t *comm, const void *host_id, int nranks, int rank);
@@ -140,6 +148,25 @@ int64_t gcm_dist_global_col(int64_t nb, int nranks, int rank, int64_t local_col)
 gcm_status_t gcm_modify_dist(gcm_comm_t comm, double *L_local, int64_t n, int64_t nb,
                              int64_t ldl_local, double *V_local, int64_t k, int sigma,
                              gcm_info_t *d_info, gcm_stream_t stream);
+/* Host only (no CUDA call): the work rank `rank` does in gcm_modify_dist.  what = 0:
+ * its Apply tiles as (row block b, global 64-column strip s) pairs, 2 entries each;
+ * what = 1: its 64-row diagonal blocks b; what = 2: the column blocks g whose rows of P
+ * it solves.  Writes min(count, cap) entries of out and returns count (-1 on bad
+ * arguments).  The union over ranks covers every tile (b < s), diagonal block and
+ * column block exactly once (tests/test_dist_host.py). */
+int64_t gcm_dist_plan(int64_t n, int64_t nb, int nranks, int rank, int what, int64_t *out, int64_t cap);
+
+/* Virtual ranks: the same column-sharded algorithm for `nranks` ranks whose shards all
+ * live on the CURRENT device, run by one call on one stream (the ranks' kernels are
+ * ordered by the stream, never waiting on each other).  L_local[r], ldl_local[r],
+ * V_local[r] are HOST arrays of nranks entries holding rank r's device pointers and
+ * leading dimension, laid out as for gcm_modify_dist.  The owner of each column block
+ * writes its P rows, and each rank its coefficient panels, straight into every other
+ * rank's buffers (device-initiated stores: the multi-GPU exchange with peer pointers).
+ * nranks in 1..8.  d_info: one gcm_info_t (device, nullable), the global first failure. */
+gcm_status_t gcm_modify_dist_virtual(int nranks, double *const *L_local, int64_t n, int64_t nb,
+                                     const int64_t *ldl_local, double *const *V_local, int64_t k,
+                                     int sigma, gcm_info_t *d_info, gcm_stream_t stream);
 
 /* ---- measurement hooks (used by bench.py; off by default, no cost when off) ----
  * When enabled, every kernel launch of the library on any stream is bracketed by

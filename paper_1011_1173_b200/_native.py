@@ -14,7 +14,7 @@ class GcmInfo(ctypes.Structure):
 
 
 STATUS = {0: "GCM_OK", 1: "GCM_EINVAL", 2: "GCM_ECUDA", 3: "GCM_ENOMEM", 4: "GCM_ENCCL", 5: "GCM_ENOTSUP"}
-ALGO = {"auto": 0, "sweep": 1, "blocked": 2}
+ALGO = {"auto": 0, "sweep": 1, "blocked": 2, "panel": 3}
 
 # every symbol include/gcm.h declares, with (restype, argtypes)
 _vp, _i64, _int, _dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
@@ -31,6 +31,8 @@ SIGNATURES = {
     "gcm_dist_local_cols": (_i64, [_i64, _i64, _int, _int]),
     "gcm_dist_global_col": (_i64, [_i64, _int, _int, _i64]),
     "gcm_modify_dist": (_int, [_vp, _dp, _i64, _i64, _i64, _dp, _i64, _int, _vp, _vp]),
+    "gcm_modify_dist_virtual": (_int, [_int, _vp, _i64, _i64, _vp, _vp, _i64, _int, _vp, _vp]),
+    "gcm_dist_plan": (_i64, [_i64, _i64, _int, _int, _int, _vp, _i64]),
     "gcm_profile_enable": (_int, [_int]),
     "gcm_profile_read": (_int, [ctypes.c_char_p, _vp, _vp, _int]),
     "gcm_status_string": (ctypes.c_char_p, [_int]),

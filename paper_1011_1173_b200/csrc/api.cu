@@ -150,9 +150,14 @@ gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     const char *env = std::getenv("GCM_ALGO");
     if (env && std::strcmp(env, "sweep") == 0) return GCM_ALGO_SWEEP;
     if (env && std::strcmp(env, "blocked") == 0) return GCM_ALGO_BLOCKED;
+    if (env && std::strcmp(env, "panel") == 0) return GCM_ALGO_PANEL;
     (void)k;
     // the chain-shortened path wins once there is more
-    // than a handful of row blocks; tiny factors keep the two-kernel sweep.
+    // than a handful of row blocks; tiny factors keep the two-kernel sweep; very large
+    // factors take the column-block (panel) algorithm, whose residual updates are plain
+    // block GEMMs instead of the blocked path's per-strip helpers (n = 1e5, k = 32:
+    // 107 vs 131 ms, profiles/r02t_*).
+    if (n >= 50000) return GCM_ALGO_PANEL;
     return n >= 256 ? GCM_ALGO_BLOCKED : GCM_ALGO_SWEEP;
 }
 
@@ -225,6 +230,7 @@ static gcm_status_t modify_impl(double *L, int64_t n, int64_t ldl, double *V, in
         return GCM_OK;
     }
     algo = pick_algo(n, k, algo);
+    if (algo == GCM_ALGO_PANEL) return modify_panel(L, n, ldl, V, k, sigma, d_info, stream);
     Workspace *ws = nullptr;
     st = get_workspace(stream, single_workspace_bytes(n, k, algo), 1, &ws);
     if (st != GCM_OK) return st;
@@ -250,7 +256,8 @@ gcm_status_t gcm_modify_info(double *L, int64_t n, int64_t ldl, double *V, int64
 
 gcm_status_t gcm_modify_ex(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma, gcm_info_t *d_info,
                            gcm_algo_t algo, gcm_stream_t stream) {
-    if (algo != GCM_ALGO_AUTO && algo != GCM_ALGO_SWEEP && algo != GCM_ALGO_BLOCKED) return GCM_EINVAL;
+    if (algo != GCM_ALGO_AUTO && algo != GCM_ALGO_SWEEP && algo != GCM_ALGO_BLOCKED && algo != GCM_ALGO_PANEL)
+        return GCM_EINVAL;
     return modify_impl(L, n, ldl, V, k, sigma, d_info, algo, (cudaStream_t)stream);
 }
 

@@ -461,7 +461,8 @@ gcm_status_t modify_batched(double *L, int64_t n, int64_t ldl, int64_t strideL, 
     }
     // larger factors: one single-factor call per factor on the same stream (each
     // already fills the GPU), each reporting into its own failure slot
-    const gcm_algo_t algo = pick_algo(n, k, GCM_ALGO_AUTO);
+    gcm_algo_t algo = pick_algo(n, k, GCM_ALGO_AUTO);
+    if (algo == GCM_ALGO_PANEL) algo = GCM_ALGO_BLOCKED;  // the per-factor loop runs on one workspace
     gcm_status_t st = get_workspace(stream, single_workspace_bytes(n, k, algo), (size_t)batch, &ws);
     if (st != GCM_OK) return st;
     for (int64_t f = 0; f < batch; ++f) {

@@ -83,6 +83,8 @@ size_t blocked_workspace_bytes(int64_t n, int64_t k);
 gcm_status_t modify_batched(double *L, int64_t n, int64_t ldl, int64_t strideL, double *V,
                             int64_t strideV, int64_t k, int sigma, int64_t batch,
                             gcm_info_t *d_info, cudaStream_t stream);
+gcm_status_t modify_panel(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma, gcm_info_t *d_info,
+                          cudaStream_t stream);
 gcm_status_t finalize_info(const unsigned long long *key, gcm_info_t *d_info, int64_t count,
                            cudaStream_t stream);
 

@@ -1,0 +1,1094 @@
+// panel.cu -- the column-sharded path (gcm_modify_dist, gcm_modify_dist_virtual) and its
+// one-rank instance GCM_ALGO_PANEL (large single factors).
+//
+// The blocked single-factor path (blocked.cu) keeps the whole triangular solve P = L^{-T} V
+// inside one persistent kernel whose helpers own every column strip; at n = 1e5 its helpers
+// are throughput-bound and it cannot be split over GPUs.  This path runs the same method
+// (P, prefix Grams G_b, U_b = chol_lower(I + sigma G_b), Apply tiles seeded
+// by the checkpointed residuals U_b^{-1} r) as a right-looking block algorithm over column
+// blocks of width nb, which shards by columns:
+//
+//   for every column block g (rows/columns [g nb, (g+1) nb)):
+//     owner (rank g mod R):  P rows of block g = L_gg^{-T} r_g  (dsolve_kernel: 64-row
+//                            sub-blocks, in-block residual updates + their checkpoints),
+//                            written straight into EVERY rank's replicated P buffer
+//                            (device-initiated puts; PEER mode adds a system-scope flag)
+//                            -- or one ncclBroadcast in NCCL mode;
+//     every rank:            residuals of its strips right of block g  -= L_{g,s}^T P_g,
+//                            writing the Apply checkpoint of each 64-row tile (pupdate_kernel);
+//   every rank: G_b prefix Grams from the replicated P (pgram/pscan), the diagonal sweeps of
+//     its own 64-row diagonal blocks (bdiag_body: PAPER.md 24-30 Compute/Apply on the block,
+//     seeded by U_b^{-1} L_bb^T P_b), then coefficient panels + U_b^{-1} to every rank;
+//   every rank: the Apply (PAPER.md 52-54) of every panel to its own tiles (btma_body over a
+//     tensor map of the LOCAL columns, 4 strips per CTA; ptile_kernel for the tiles of the
+//     diagonal column block).
+//
+// The only exchanges are P (n k doubles per call, every owner's rows once) and the panels
+// (~(2*64*k + 64 + k) doubles per 64-row block), both written by the producing kernel
+// itself.  Layout: 1-D block-cyclic over columns (gcm.h), V rows follow their columns.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <tuple>
+#include <vector>
+
+#include "bparts.cuh"
+#include "diag.cuh"
+#include "internal.h"
+#include "tma.cuh"
+
+#ifdef GCM_WITH_NCCL
+#include <nccl.h>
+#endif
+
+struct gcm_comm {
+#ifdef GCM_WITH_NCCL
+    ncclComm_t nc = nullptr;
+#endif
+    int rank = 0;
+    int nranks = 1;
+};
+
+namespace gcm {
+namespace {
+
+constexpr int kMaxRanks = 8;  // virtual ranks / peers a kernel writes to
+constexpr int kPT = 256;      // pupdate threads
+constexpr int kDsT = 1024;    // dsolve threads (warp e solves update column e)
+constexpr int kPassK = 32;    // update columns per pass (k > 32: sequential passes, R3)
+
+// -------------------------------------------------------------------------- layout (host)
+int64_t local_cols(int64_t n, int64_t nb, int R, int r) {
+    if (n < 0 || nb <= 0 || R <= 0 || r < 0 || r >= R) return -1;
+    const int64_t nblk = (n + nb - 1) / nb;
+    int64_t cols = 0;
+    for (int64_t g = r; g < nblk; g += R) cols += std::min<int64_t>(nb, n - g * nb);
+    return cols;
+}
+int64_t global_col(int64_t nb, int R, int r, int64_t lc) {
+    const int64_t lb = lc / nb;
+    return (lb * R + r) * nb + lc % nb;
+}
+
+// One rank's view: its factor columns, V rows, and workspace carve-up.
+struct Plan {
+    int64_t n, nb, nloc;
+    int R, r, k, KB;
+    int NB64, NBc, nsl;
+    std::vector<int> gstrip;                // global 64-column strip of local strip sl
+    std::vector<int64_t> chkoff;            // first checkpoint tile of local strip sl
+    int64_t nchk = 0;
+    std::vector<int> dl_b;                  // local diagonal 64-row blocks
+    std::vector<int64_t> dl_lc;             //   and their first local column
+    std::vector<int2> full;                 // TMA Apply items (b, first local strip of 4)
+    std::vector<int2> tiles;                // single-tile Apply items (b, local strip)
+    int64_t sb;                             // solve-block height (<= nb, dsolve's shared-memory cap)
+    int NSB;                                // solve blocks
+    std::vector<int> first_strip_after;     // per solve block: first local strip right of it
+};
+
+// rows of one dsolve launch: its residuals live in shared memory (kDsMaxRows x KB doubles)
+inline int64_t solve_block_rows(int64_t nb, int KB) {
+    const int64_t cap = KB <= 16 ? 512 : 256;
+    return std::min<int64_t>(nb, cap);
+}
+
+Plan make_plan(int64_t n, int64_t nb, int R, int r, int k, bool tma_groups) {
+    Plan p;
+    p.n = n;
+    p.nb = nb;
+    p.R = R;
+    p.r = r;
+    p.k = k;
+    p.KB = k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
+    p.nloc = local_cols(n, nb, R, r);
+    p.NB64 = (int)((n + kD - 1) / kD);
+    p.NBc = (int)((n + nb - 1) / nb);
+    p.nsl = (int)((p.nloc + kD - 1) / kD);
+    p.gstrip.resize(p.nsl);
+    p.chkoff.resize(p.nsl);
+    for (int sl = 0; sl < p.nsl; ++sl) {
+        p.gstrip[sl] = (int)(global_col(nb, R, r, (int64_t)sl * kD) / kD);
+        p.chkoff[sl] = p.nchk;
+        p.nchk += p.gstrip[sl];  // tiles (b, s), b < s
+    }
+    for (int sl = 0; sl < p.nsl; ++sl) {  // a strip's diagonal block b = its global strip
+        p.dl_b.push_back(p.gstrip[sl]);
+        p.dl_lc.push_back((int64_t)sl * kD);
+    }
+    p.sb = solve_block_rows(nb, p.KB);
+    p.NSB = (int)((n + p.sb - 1) / p.sb);
+    p.first_strip_after.resize(p.NSB);
+    for (int g = 0; g < p.NSB; ++g) {
+        const int64_t end = std::min<int64_t>(n, (int64_t)(g + 1) * p.sb);
+        int sl = 0;
+        while (sl < p.nsl && (int64_t)p.gstrip[sl] * kD < end) ++sl;
+        p.first_strip_after[g] = sl;
+    }
+    // Apply items: groups of 4 local strips inside one local column block (globally
+    // contiguous when nb is a multiple of 256): a TMA item while all 4 are right of row
+    // block b, else per-strip tiles for the strips that are
+    const int spb = (int)(nb / kD);  // strips per column block
+    const bool grp = tma_groups && nb % 256 == 0;
+    for (int lb0 = 0; lb0 < p.nsl; lb0 += spb) {
+        const int lb_end = std::min(p.nsl, lb0 + spb);
+        for (int sl0 = lb0; sl0 < lb_end; sl0 += 4) {
+            const int cnt = std::min(4, lb_end - sl0);
+            const int last = p.gstrip[sl0 + cnt - 1];
+            for (int b = 0; b < last; ++b) {
+                if (grp && p.gstrip[sl0] > b) {
+                    p.full.push_back(make_int2(b, sl0));
+                } else {
+                    for (int q = 0; q < cnt; ++q)
+                        if (p.gstrip[sl0 + q] > b) p.tiles.push_back(make_int2(b, sl0 + q));
+                }
+            }
+        }
+    }
+    return p;
+}
+
+// workspace carve-up of one rank (byte offsets)
+struct Carve {
+    size_t P, res, chk, Q, G, U, panels, key, flags, ctr, gstrip, chkoff, dlb, dllc, full, tiles, total;
+};
+Carve carve(const Plan &p) {
+    Carve c{};
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o += (bytes + 255) / 256 * 256;
+        return at;
+    };
+    const int KB = p.KB;
+    c.P = take((size_t)p.NBc * p.nb * p.k * 8);
+    c.res = take((size_t)std::max(p.nsl, 1) * kD * p.k * 8);
+    c.chk = take((size_t)std::max<int64_t>(p.nchk, 1) * kD * p.k * 8);
+    c.Q = take((size_t)p.NB64 * KB * KB * 8);
+    c.G = take((size_t)p.NB64 * KB * KB * 8);
+    c.U = take((size_t)p.NB64 * KB * KB * 8);
+    c.panels = take((size_t)p.NB64 * panel_doubles(KB) * 8);
+    c.key = take(8);
+    c.flags = take((size_t)(p.NSB + 1) * 4);
+    c.ctr = take(16);
+    c.gstrip = take((size_t)std::max(p.nsl, 1) * 4);
+    c.chkoff = take((size_t)std::max(p.nsl, 1) * 8);
+    c.dlb = take((size_t)std::max<size_t>(p.dl_b.size(), 1) * 4);
+    c.dllc = take((size_t)std::max<size_t>(p.dl_lc.size(), 1) * 8);
+    c.full = take((size_t)std::max<size_t>(p.full.size(), 1) * 8);
+    c.tiles = take((size_t)std::max<size_t>(p.tiles.size(), 1) * 8);
+    c.total = o;
+    return c;
+}
+
+// where a kernel writes replicated data: one pointer per rank (device-initiated puts)
+struct Peers {
+    double *dst[kMaxRanks];
+    double *dst2[kMaxRanks];
+    unsigned *flag[kMaxRanks];  // nullptr: no flag (stream order suffices)
+    int R;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_flag_sys(const unsigned *f, unsigned epoch) {
+    if (threadIdx.x == 0)
+        while (ld_acquire_sys(f) != epoch) __nanosleep(200);
+    __syncthreads();
+}
+
+// -------------------------------------------------------------------------- kernels
+// residual of every local strip = its V rows; checkpoint of tile (0, s) likewise
+__global__ void pinit_kernel(const double *__restrict__ V, int64_t ldv, int64_t nloc, int k, const int *gstrip,
+                             const int64_t *chkoff, double *res, double *chk) {
+    const int sl = blockIdx.x;
+    const int64_t lc0 = (int64_t)sl * kD;
+    double *r = res + (int64_t)sl * kD * k;
+    double *c0 = gstrip[sl] >= 1 ? chk + chkoff[sl] * kD * k : nullptr;
+    for (int o = threadIdx.x; o < kD * k; o += blockDim.x) {
+        const int c = o / k, e = o % k;
+        const double v = lc0 + c < nloc ? V[lc0 + c + (int64_t)e * ldv] : 0.0;
+        r[o] = v;
+        if (c0) c0[o] = v;
+    }
+}
+
+// The owner's diagonal solve of column block g: P rows [row0, row0 + nrows) = L_gg^{-T} r_g,
+// 64-row sub-block a after sub-block a: the pair-row substitution of diag.cuh (one warp per
+// update column), the rows written to every rank's P, then the residuals (and Apply
+// checkpoints) of the block's later strips updated with them.  One CTA; the block's
+// residuals stay in shared memory for the whole kernel (they are dead after it: the block's
+// strips have no tiles below it), and every L tile is prefetched one step ahead (cp.async
+// double buffer), so the only exposed latency is the first load.
+constexpr int kDsMaxRows = 512;  // solve-block height the kernel's shared memory is sized for (KB <= 16)
+__device__ __forceinline__ void cp8(double *dst, const double *src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(ok ? src : nullptr),
+                 "r"(ok ? 8 : 0)
+                 : "memory");
+}
+template <int KB>
+__global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restrict__ L, int64_t ldl, int64_t n, int k,
+                                                       int64_t row0, int nrows, int sl0, double *res, double *chk,
+                                                       const int64_t *chkoff, Peers peers, unsigned epoch) {
+    extern __shared__ double sm_ds[];
+    double(*Ls)[kD + 1] = reinterpret_cast<double(*)[kD + 1]>(sm_ds);
+    double *Lt = sm_ds + kD * (kD + 1);          // [2][kD][kD+1] off-diagonal tiles
+    double *qv = Lt + 2 * kD * (kD + 1);         // [kD][KB+1]
+    double *rinv = qv + kD * (KB + 1);           // [kD]
+    double *R = rinv + kD;                       // [kDsMaxRows][KB]: the block's residuals
+    const int t = threadIdx.x;
+    constexpr int LQ = KB + 1;
+    const int na = (nrows + kD - 1) / kD;
+    // the whole block's residuals (one round trip) and the first diagonal tile
+    for (int o = t; o < na * kD * KB; o += kDsT) {
+        const int row = o / KB, e = o % KB;
+        const int a = row / kD, m = row % kD;
+        cp8(R + o, res + (int64_t)(sl0 + a) * kD * k + m * k + e, e < k && row < nrows);
+    }
+    auto load_diag = [&](int a) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        const int Da = (int)imin64(kD, n - r0);
+        const int64_t lc = (int64_t)(sl0 + a) * kD;
+        for (int idx = t; idx < kD * kD; idx += kDsT) {
+            const int m = idx / kD, j = idx % kD;
+            cp8(&Ls[m][j], L + (r0 + j) + (lc + m) * ldl, m < Da && j <= m);
+        }
+    };
+    // tile (a, a2): rows of sub-block a, columns of sub-block a2, into Lt[buf]
+    auto load_tile = [&](int a, int a2, int buf) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        const int Da = (int)imin64(kD, n - r0);
+        const int64_t lc2 = (int64_t)(sl0 + a2) * kD;
+        const int D2 = (int)imin64(kD, n - (row0 + (int64_t)a2 * kD));
+        double *lt = Lt + buf * kD * (kD + 1);
+        for (int idx = t; idx < kD * kD; idx += kDsT) {
+            const int c = idx / kD, m = idx % kD;
+            cp8(lt + c * (kD + 1) + m, L + (r0 + m) + (lc2 + c) * ldl, c < D2 && m < Da);
+        }
+    };
+    load_diag(0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int a = 0; a < na; ++a) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        const int Da = (int)imin64(kD, n - r0);
+        if (a + 1 < na) load_tile(a, a + 1, 0);  // first update tile of this step, under the solve
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // R, Ls(a) landed
+        __syncthreads();
+        for (int o = t; o < kD * KB; o += kDsT) {
+            const int m = o / KB, e = o % KB;
+            qv[m * LQ + e] = m < Da ? R[(a * kD + m) * KB + e] : 0.0;
+        }
+        __syncthreads();
+        block_trsv<KB>(Ls, qv, LQ, Da, rinv);
+        for (int o = t; o < Da * k; o += kDsT) {
+            const int m = o / k, e = o % k;
+            const double v = qv[m * LQ + e];
+            for (int r = 0; r < peers.R; ++r) peers.dst[r][(r0 + m) * k + e] = v;
+        }
+        if (a + 1 < na) load_diag(a + 1);  // Ls is free (the solve and the P stores read qv)
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        for (int a2 = a + 1; a2 < na; ++a2) {
+            const int buf = (a2 - a - 1) & 1;
+            if (a2 + 1 < na) load_tile(a, a2 + 1, buf ^ 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            // tile (a, a2) landed: at a2 = a + 1 the diagonal tile of a + 1 and tile (a, a + 2)
+            // may still be in flight, later only the tile just issued
+            if (a2 == a + 1) asm volatile("cp.async.wait_group 2;" ::: "memory");
+            else asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
+            const int D2 = (int)imin64(kD, n - (row0 + (int64_t)a2 * kD));
+            const double *lt = Lt + buf * kD * (kD + 1);
+            double *ck = chk + (chkoff[sl0 + a2] + r0 / kD) * kD * k;  // tile (r0/64, strip a2)
+            for (int o = t; o < D2 * KB; o += kDsT) {
+                const int c = o / KB, e = o % KB;
+                double *rp = R + (a2 * kD + c) * KB + e;
+                const double old = *rp;
+                if (e < k) ck[c * k + e] = old;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                const double *l = lt + c * (kD + 1);
+                for (int m = 0; m < Da; m += 4) {
+                    s0 = fma(l[m], qv[m * LQ + e], s0);
+                    s1 = fma(l[m + 1], qv[(m + 1) * LQ + e], s1);
+                    s2 = fma(l[m + 2], qv[(m + 2) * LQ + e], s2);
+                    s3 = fma(l[m + 3], qv[(m + 3) * LQ + e], s3);
+                }
+                *rp = old - ((s0 + s1) + (s2 + s3));
+            }
+            __syncthreads();  // Lt[buf] is refilled two steps on
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+    }
+    if (peers.flag[0]) {  // PEER mode: the P rows are visible to every rank before the flag
+        __threadfence_system();
+        __syncthreads();
+        if (t == 0)
+            for (int r = 0; r < peers.R; ++r) st_release_sys(peers.flag[r], epoch);
+    }
+}
+
+// Every rank: residuals of its strips right of solve block g -= L_{rows of g, strip}^T P,
+// checkpointing the residual at the start of every 64-row tile.  Thread (column group, e
+// group) owns CPT adjacent columns x EPT update columns of the strip (a CPT x EPT register
+// block: per row one 16-byte load of the L pair and EPT/2 16-byte loads of P feed CPT*EPT
+// FMAs); the L tile (row-major in shared memory) and the P rows of the next 64-row
+// sub-block stream in (cp.async, double buffered) under the current one.
+template <int KB>
+struct PuShape {
+    static constexpr int CPT = KB >= 8 ? 2 : 1;
+    static constexpr int EPT = KB / (4 * CPT);
+    static constexpr int NCG = kD / CPT;  // column groups
+    static constexpr int LDT = kD + 2;    // row stride of the L tile (16-byte aligned)
+};
+template <int KB>
+__global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restrict__ L, int64_t ldl, int64_t n,
+                                                        int64_t nloc, int k, int64_t row0, int nrows, int sl_first,
+                                                        double *res, double *chk, const int64_t *chkoff,
+                                                        const double *__restrict__ P, const unsigned *flag,
+                                                        unsigned epoch) {
+    using S = PuShape<KB>;
+    constexpr int CPT = S::CPT, EPT = S::EPT, LDT = S::LDT;
+    extern __shared__ __align__(16) double sm_pu[];
+    double *Lt = sm_pu;                // [2][kD rows m][LDT]: Lt[m][c] = L(r0 + m, strip column c)
+    double *Ps = sm_pu + 2 * kD * LDT;  // [2][kD][KB]
+    const int t = threadIdx.x, cg = t % S::NCG, eg = t / S::NCG;
+    const int c0 = cg * CPT, e0 = eg * EPT;
+    const int sl = sl_first + blockIdx.x;
+    const int64_t lc = (int64_t)sl * kD;
+    const int nc = (int)imin64(kD, nloc - lc);
+    const int na = (nrows + kD - 1) / kD;
+    if (flag) wait_flag_sys(flag, epoch);
+    double *rs = res + (int64_t)sl * kD * k;
+    double acc[CPT][EPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) acc[u][i] = (c0 + u < nc && e0 + i < k) ? rs[(c0 + u) * k + e0 + i] : 0.0;
+    auto issue = [&](int a) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        const int Da = (int)imin64(kD, n - r0);
+        double *lt = Lt + (a & 1) * kD * LDT;
+        double *ps = Ps + (a & 1) * kD * KB;
+        for (int idx = t; idx < kD * kD; idx += kPT) {
+            const int cc = idx / kD, m = idx % kD;  // consecutive threads: consecutive rows (coalesced)
+            const bool ok = cc < nc && m < Da;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(lt + m * LDT + cc)),
+                         "l"(ok ? L + (r0 + m) + (lc + cc) * ldl : L), "r"(ok ? 8 : 0)
+                         : "memory");
+        }
+        for (int idx = t; idx < kD * KB; idx += kPT) {
+            const int m = idx / KB, e = idx % KB;
+            const bool ok = m < Da && e < k;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(ps + idx)),
+                         "l"(ok ? P + (r0 + m) * k + e : P), "r"(ok ? 8 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0);
+    for (int a = 0; a < na; ++a) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        if (a + 1 < na) {
+            issue(a + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        {
+            double *ck = chk + (chkoff[sl] + r0 / kD) * kD * k;
+#pragma unroll
+            for (int u = 0; u < CPT; ++u)
+#pragma unroll
+                for (int i = 0; i < EPT; ++i)
+                    if (c0 + u < nc && e0 + i < k) ck[(c0 + u) * k + e0 + i] = acc[u][i];
+        }
+        const double *lt = Lt + (a & 1) * kD * LDT + c0;
+        const double *ps = Ps + (a & 1) * kD * KB + e0;
+#pragma unroll 4
+        for (int m = 0; m < kD; ++m) {
+            double l[CPT], pv[EPT];
+            if constexpr (CPT == 2) {
+                const double2 l2 = *reinterpret_cast<const double2 *>(lt + m * LDT);
+                l[0] = l2.x;
+                l[1] = l2.y;
+            } else {
+                l[0] = lt[m * LDT];
+            }
+            if constexpr (EPT % 2 == 0) {
+#pragma unroll
+                for (int i = 0; i < EPT; i += 2) {
+                    const double2 p2 = *reinterpret_cast<const double2 *>(ps + m * KB + i);
+                    pv[i] = p2.x;
+                    pv[i + 1] = p2.y;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < EPT; ++i) pv[i] = ps[m * KB + i];
+            }
+#pragma unroll
+            for (int u = 0; u < CPT; ++u)
+#pragma unroll
+                for (int i = 0; i < EPT; ++i) acc[u][i] = fma(-l[u], pv[i], acc[u][i]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < CPT; ++u)
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (c0 + u < nc && e0 + i < k) rs[(c0 + u) * k + e0 + i] = acc[u][i];
+}
+
+// Q_b = P_b^T P_b per 64-row block (KB x KB, zero padded)
+template <int KB>
+__global__ void pgram_kernel(const double *__restrict__ P, int64_t n, int k, double *Q) {
+    const int b = blockIdx.x;
+    for (int o = threadIdx.x; o < KB * KB; o += blockDim.x) {
+        const int i = o / KB, j = o % KB;
+        double s = 0.0;
+        if (i < k && j < k)
+            for (int64_t m = (int64_t)b * kD; m < n && m < (int64_t)(b + 1) * kD; ++m) s = fma(P[m * k + i], P[m * k + j], s);
+        Q[(int64_t)b * KB * KB + o] = s;
+    }
+}
+// G_b = sum_{b' < b} Q_b' (exclusive prefix; one thread per entry)
+template <int KB>
+__global__ void pscan_kernel(const double *__restrict__ Q, int NB, double *G) {
+    const int o = threadIdx.x;
+    if (o >= KB * KB) return;
+    double run = 0.0;
+    for (int b = 0; b < NB; ++b) {
+        const double q = Q[(int64_t)b * KB * KB + o];
+        G[(int64_t)b * KB * KB + o] = run;
+        run += q;
+    }
+}
+
+// the diagonal sweeps of this rank's 64-row diagonal blocks (bdiag_body, global indexing of
+// L and V shifted onto the local columns)
+template <int KB>
+__global__ void __launch_bounds__(kDiagThreads) pdiag_kernel(double *L, int64_t ldl, int64_t n, double *V, int64_t ldv,
+                                                           int k, int sigma, const double *P, double *Ui,
+                                                           const double *G, double *panels, unsigned long long *key,
+                                                           int64_t ebase, const int *dl_b, const int64_t *dl_lc) {
+    extern __shared__ double smem_pd[];
+    const int b = dl_b[blockIdx.x];
+    const int64_t shift = dl_lc[blockIdx.x] - (int64_t)b * kD;  // local column - global column
+    bdiag_body<KB>(L + shift * ldl, n, ldl, V + shift, ldv, k, sigma, P, false, Ui, G, panels, key, ebase, b, smem_pd);
+}
+
+// this rank's panels and U_b^{-1} to every other rank (device-initiated puts), then the
+// flags of PEER mode
+template <int KB>
+__global__ void pbcast_kernel(const int *dl_b, int ndl, const double *panels, const double *Ui, Peers peers, int self,
+                              unsigned epoch) {
+    constexpr int PD = panel_doubles(KB), UD = KB * KB;
+    for (int i = blockIdx.x; i < ndl; i += gridDim.x) {
+        const int b = dl_b[i];
+        for (int r = 0; r < peers.R; ++r) {
+            if (r == self) continue;
+            for (int o = threadIdx.x; o < PD; o += blockDim.x)
+                peers.dst[r][(int64_t)b * PD + o] = panels[(int64_t)b * PD + o];
+            for (int o = threadIdx.x; o < UD; o += blockDim.x)
+                peers.dst2[r][(int64_t)b * UD + o] = Ui[(int64_t)b * UD + o];
+        }
+    }
+    if (peers.flag[0]) {  // PEER mode: count this rank in on every peer's panel barrier
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int r = 0; r < peers.R; ++r) atomicAdd_system(peers.flag[r], 1u);
+    }
+}
+// PEER mode: wait until all R ranks have published their panels for this call
+__global__ void pwait_kernel(const unsigned *ctr, unsigned target) {
+    if (threadIdx.x == 0)
+        while ((int)(ld_acquire_sys(ctr) - target) < 0) __nanosleep(200);
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kT2Threads, 2) papply_kernel(const __grid_constant__ CUtensorMap tm, int64_t n,
+                                                              int k, const double *__restrict__ chk,
+                                                              const double *__restrict__ Ui,
+                                                              const double *__restrict__ panels, int NB,
+                                                              const int2 *items, ApplyMap map) {
+    extern __shared__ __align__(16) unsigned char smem_pa[];
+    const int2 it = items[blockIdx.x];
+    btma_body<KB>(tm, n, k, chk, Ui, panels, NB, it.x, it.y, smem_pa, 0, map);
+}
+
+// one 64 x 64 tile (b, local strip sl) of the diagonal column block (or any tile when L is
+// not TMA-addressable): thread = column, V state U_b^{-1} r from the checkpoint, 8-row chunks
+// through registers; only the tile's own columns are read and written.
+template <int KB>
+__global__ void __launch_bounds__(kD) ptile_kernel(double *L, int64_t ldl, int64_t nloc, int k,
+                                                  const double *__restrict__ chk, const double *__restrict__ Ui,
+                                                  const double *__restrict__ panels, const int2 *items,
+                                                  const int64_t *chkoff) {
+    __shared__ double2 cs[kD * KB];
+    __shared__ double rho[kD], nu[KB], Us[KB * KB];
+    const int2 it = items[blockIdx.x];
+    const int b = it.x, sl = it.y, c = threadIdx.x;
+    const double *pan = panels + (int64_t)b * panel_doubles(KB);
+    for (int i = c; i < kD * KB; i += kD) cs[i] = make_double2(pan[2 * i], pan[2 * i + 1]);
+    for (int i = c; i < kD; i += kD) rho[i] = pan[2 * kD * KB + i];
+    for (int i = c; i < KB; i += kD) nu[i] = pan[2 * kD * KB + kD + i];
+    for (int i = c; i < KB * KB; i += kD) Us[i] = Ui[(int64_t)b * KB * KB + i];
+    __syncthreads();
+    const int64_t lc = (int64_t)sl * kD + c;
+    if (lc >= nloc) return;
+    const double *r = chk + (chkoff[sl] + b) * kD * k + (int64_t)c * k;
+    double rr[KB], v[KB];
+#pragma unroll
+    for (int e = 0; e < KB; ++e) rr[e] = e < k ? r[e] : 0.0;
+#pragma unroll
+    for (int e = 0; e < KB; ++e) {
+        double acc = 0.0;
+#pragma unroll
+        for (int ep = 0; ep <= e; ++ep) acc = fma(Us[e * KB + ep], rr[ep], acc);
+        v[e] = acc;
+    }
+    double *col = L + (int64_t)b * kD + lc * ldl;
+    for (int j0 = 0; j0 < kD; j0 += 8) {
+        double l[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) l[u] = col[j0 + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) l[u] = apply_row<KB>(l[u], v, cs + (j0 + u) * KB, rho[j0 + u], KB);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) col[j0 + u] = l[u];
+    }
+}
+
+// min over the virtual ranks' failure keys into key[0]
+struct KeyList {
+    unsigned long long *k[kMaxRanks];
+    int R;
+};
+__global__ void keymin_kernel(unsigned long long *key0, KeyList keys) {
+    unsigned long long m = ~0ull;
+    for (int r = 0; r < keys.R; ++r) m = min(m, *keys.k[r]);
+    *key0 = m;
+}
+
+// -------------------------------------------------------------------------- host driver
+enum class Mode { Virtual, Nccl, Peer };
+
+struct Rank {
+    double *L;
+    int64_t ldl;
+    double *V;  // local V rows (ld nloc)
+    Plan plan;
+    Carve cv;
+    char *ws;
+    CUtensorMap tm;
+    bool tma;
+    template <typename T>
+    T *at(size_t off) const {
+        return reinterpret_cast<T *>(ws + off);
+    }
+};
+
+template <int KB>
+size_t dsolve_smem() {
+    return (size_t)(3 * kD * (kD + 1) + kD * (KB + 1) + kD + (KB <= 16 ? 512 : 256) * KB) * 8;
+}
+template <int KB>
+size_t pupdate_smem() {
+    return (size_t)(2 * kD * PuShape<KB>::LDT + 2 * kD * KB) * 8;
+}
+template <int KB>
+size_t pdiag_smem() {
+    return (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 + 4 * kD * KB + kD) *
+           sizeof(double);
+}
+
+struct Exchange {
+    Mode mode;
+    void *nccl;        // ncclComm_t (Nccl / Peer modes)
+    int self;          // this process's rank (Nccl / Peer); 0 in Virtual mode
+    double **peerP;    // Peer mode: every rank's P, panels, Ui buffers and flag words (IPC-mapped)
+    double **peerPan;
+    double **peerU;
+    unsigned **peerFlag;
+    unsigned **peerCtr;
+};
+
+// The library's auxiliary stream on the current device (the residual updates that overlap the
+// next diagonal solve) and two event pairs for the hand-offs between it and the call's stream.
+std::mutex g_aux_mutex;
+struct Aux {
+    cudaStream_t s = nullptr;
+    cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+};
+std::map<int, Aux> g_aux;
+gcm_status_t aux_stream(cudaStream_t *s, cudaEvent_t **ready, cudaEvent_t **done) {
+    int dev = 0;
+    gcm_status_t st = check_cuda(cudaGetDevice(&dev));
+    if (st != GCM_OK) return st;
+    std::lock_guard<std::mutex> lock(g_aux_mutex);
+    Aux &a = g_aux[dev];
+    if (!a.s) {
+        st = check_cuda(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
+        for (int i = 0; i < 2 && st == GCM_OK; ++i) {
+            st = check_cuda(cudaEventCreateWithFlags(&a.ready[i], cudaEventDisableTiming));
+            if (st == GCM_OK) st = check_cuda(cudaEventCreateWithFlags(&a.done[i], cudaEventDisableTiming));
+        }
+        if (st != GCM_OK) return st;
+    }
+    *s = a.s;
+    *ready = a.ready;
+    *done = a.done;
+    return GCM_OK;
+}
+
+// one pass (<= 32 update columns) over all ranks of `rk` (Virtual: all R; else rk has one entry)
+template <int KB>
+gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int k, int sigma, int64_t ebase,
+                        unsigned epoch, const Exchange &x, cudaStream_t stream) {
+    gcm_status_t st = GCM_OK;
+    const int nloc_ranks = (int)rk.size();
+    const int NBc = (int)((n + nb - 1) / nb), NB64 = (int)((n + kD - 1) / kD);
+    auto peers_P = [&](int owner_local) {
+        Peers p{};
+        if (x.mode == Mode::Virtual) {
+            p.R = R;
+            for (int r = 0; r < R; ++r) p.dst[r] = rk[r].at<double>(rk[r].cv.P);
+        } else if (x.mode == Mode::Nccl) {
+            p.R = 1;
+            p.dst[0] = rk[owner_local].at<double>(rk[owner_local].cv.P);
+        } else {
+            p.R = R;
+            for (int r = 0; r < R; ++r) p.dst[r] = x.peerP[r];
+        }
+        return p;
+    };
+    st = check_cuda(cudaFuncSetAttribute(dsolve_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dsolve_smem<KB>()));
+    if (st == GCM_OK)
+        st = check_cuda(cudaFuncSetAttribute(pupdate_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)pupdate_smem<KB>()));
+    if (st == GCM_OK)
+        st = check_cuda(cudaFuncSetAttribute(pdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)pdiag_smem<KB>()));
+    if (st != GCM_OK) return st;
+    // 1. residuals = V, tile (0, s) checkpoints
+    for (auto &q : rk) {
+        if (q.plan.nsl == 0) continue;
+        pinit_kernel<<<q.plan.nsl, kPT, 0, stream>>>(q.V, std::max<int64_t>(q.plan.nloc, 1), q.plan.nloc, k,
+                                                      q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff),
+                                                      q.at<double>(q.cv.res), q.at<double>(q.cv.chk));
+    }
+    // 2. the right-looking solve over column blocks
+    {
+        ProfScope ps("ptrsv", stream);
+        cudaStream_t aux = nullptr;
+        cudaEvent_t *p_ready = nullptr, *rest_done = nullptr;
+        st = aux_stream(&aux, &p_ready, &rest_done);
+        if (st != GCM_OK) return st;
+        st = check_cuda(cudaEventRecord(p_ready[1], stream));  // the aux stream starts after this call's prologue
+        if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(aux, p_ready[1], 0));
+        if (st != GCM_OK) return st;
+        const int64_t sb = rk[0].plan.sb;
+        const int NSB = rk[0].plan.NSB;
+        for (int g = 0; g < NSB; ++g) {  // solve blocks of sb rows (sb divides nb)
+            const int64_t row0 = (int64_t)g * sb;
+            const int owner = (int)((row0 / nb) % R);
+            const int nrows = (int)std::min<int64_t>(sb, n - row0);
+            const int ol = x.mode == Mode::Virtual ? owner : (owner == x.self ? 0 : -1);
+            if (ol >= 0) {
+                Rank &q = rk[ol];
+                // owner's local strip of row0's column: local block (row0/nb)/R, offset row0 % nb
+                const int sl0 = (int)((((row0 / nb) / R) * nb + row0 % nb) / kD);
+                Peers p = peers_P(ol);
+                if (x.mode == Mode::Peer)
+                    for (int r = 0; r < R; ++r) p.flag[r] = x.peerFlag[r] + g;
+                dsolve_kernel<KB><<<1, kDsT, dsolve_smem<KB>(), stream>>>(
+                    q.L, q.ldl, n, k, row0, nrows, sl0, q.at<double>(q.cv.res), q.at<double>(q.cv.chk),
+                    q.at<int64_t>(q.cv.chkoff), p, epoch);
+            }
+#ifdef GCM_WITH_NCCL
+            if (x.mode == Mode::Nccl) {
+                double *Pg = rk[0].at<double>(rk[0].cv.P) + row0 * k;
+                st = ncclBroadcast(Pg, Pg, (size_t)nrows * k, ncclDouble, owner, (ncclComm_t)x.nccl, stream) ==
+                             ncclSuccess
+                         ? GCM_OK
+                         : GCM_ENCCL;
+                if (st != GCM_OK) return st;
+            }
+#endif
+            // lookahead: the strips of the NEXT solve block first, on the call's stream (after the
+            // rest of block g-1, which touched the same residuals); the rest on the aux stream,
+            // where it overlaps the next diagonal solve
+            if (g >= 1) {
+                st = check_cuda(cudaStreamWaitEvent(stream, rest_done[(g - 1) & 1], 0));
+                if (st != GCM_OK) return st;
+            }
+            for (int pass = 0; pass < 2; ++pass) {
+                cudaStream_t sp = pass == 0 ? stream : aux;
+                if (pass == 1) {
+                    st = check_cuda(cudaEventRecord(p_ready[g & 1], stream));
+                    if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(aux, p_ready[g & 1], 0));
+                    if (st != GCM_OK) return st;
+                }
+                for (int ri = 0; ri < nloc_ranks; ++ri) {
+                    Rank &q = rk[ri];
+                    const int slf = q.plan.first_strip_after[g];
+                    const int sla = g + 1 < NSB ? q.plan.first_strip_after[g + 1] : q.plan.nsl;
+                    const int s_lo = pass == 0 ? slf : sla, s_hi = pass == 0 ? sla : q.plan.nsl;
+                    if (s_lo >= s_hi) continue;
+                    const int rank_id = x.mode == Mode::Virtual ? ri : x.self;
+                    const unsigned *flag =
+                        (x.mode == Mode::Peer && rank_id != owner) ? x.peerFlag[x.self] + g : nullptr;
+                    pupdate_kernel<KB><<<s_hi - s_lo, kPT, pupdate_smem<KB>(), sp>>>(
+                        q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                        q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.at<double>(q.cv.P), flag, epoch);
+                }
+            }
+            st = check_cuda(cudaEventRecord(rest_done[g & 1], aux));
+            if (st != GCM_OK) return st;
+        }
+        st = check_cuda(cudaStreamWaitEvent(stream, rest_done[(NSB - 1) & 1], 0));  // join the aux stream
+        if (st == GCM_OK) st = check_cuda(cudaGetLastError());
+        if (st != GCM_OK) return st;
+    }
+    // 3. prefix Grams (replicated), 4. diagonal sweeps of the local diagonal blocks
+    {
+        ProfScope ps("psweep", stream);
+        for (auto &q : rk) {
+            pgram_kernel<KB><<<NB64, KB * KB <= 1024 ? KB * KB : 1024, 0, stream>>>(q.at<double>(q.cv.P), n, k,
+                                                                                  q.at<double>(q.cv.Q));
+            pscan_kernel<KB><<<1, KB * KB, 0, stream>>>(q.at<double>(q.cv.Q), NB64, q.at<double>(q.cv.G));
+            if (!q.plan.dl_b.empty())
+                pdiag_kernel<KB><<<(unsigned)q.plan.dl_b.size(), kDiagThreads, pdiag_smem<KB>(), stream>>>(
+                    q.L, q.ldl, n, q.V, std::max<int64_t>(q.plan.nloc, 1), k, sigma, q.at<double>(q.cv.P),
+                    q.at<double>(q.cv.U), q.at<double>(q.cv.G), q.at<double>(q.cv.panels),
+                    q.at<unsigned long long>(q.cv.key), ebase, q.at<int>(q.cv.dlb), q.at<int64_t>(q.cv.dllc));
+        }
+        // 5. panels and U_b^{-1} to every rank
+        if (x.mode == Mode::Virtual || x.mode == Mode::Peer) {
+            for (int ri = 0; ri < nloc_ranks; ++ri) {
+                Rank &q = rk[ri];
+                Peers p{};
+                p.R = R;
+                for (int r = 0; r < R; ++r) {
+                    p.dst[r] = x.mode == Mode::Virtual ? rk[r].at<double>(rk[r].cv.panels) : x.peerPan[r];
+                    p.dst2[r] = x.mode == Mode::Virtual ? rk[r].at<double>(rk[r].cv.U) : x.peerU[r];
+                    p.flag[r] = x.mode == Mode::Peer ? x.peerCtr[r] : nullptr;
+                }
+                const int self = x.mode == Mode::Virtual ? ri : x.self;
+                pbcast_kernel<KB><<<std::max<int>(1, std::min<int>(1024, (int)q.plan.dl_b.size())), 256, 0, stream>>>(
+                    q.at<int>(q.cv.dlb), (int)q.plan.dl_b.size(), q.at<double>(q.cv.panels), q.at<double>(q.cv.U),
+                    p, self, epoch);
+            }
+            if (x.mode == Mode::Peer) pwait_kernel<<<1, 32, 0, stream>>>(x.peerCtr[x.self], epoch * (unsigned)R);
+        }
+#ifdef GCM_WITH_NCCL
+        if (x.mode == Mode::Nccl) {
+            ncclGroupStart();
+            for (int g = 0; g < NBc; ++g) {
+                const int owner = g % R;
+                const int b0 = (int)((int64_t)g * nb / kD), b1 = (int)std::min<int64_t>(NB64, ((int64_t)g + 1) * nb / kD);
+                double *pan = rk[0].at<double>(rk[0].cv.panels) + (int64_t)b0 * panel_doubles(KB);
+                double *U = rk[0].at<double>(rk[0].cv.U) + (int64_t)b0 * KB * KB;
+                ncclBroadcast(pan, pan, (size_t)(b1 - b0) * panel_doubles(KB), ncclDouble, owner,
+                              (ncclComm_t)x.nccl, stream);
+                ncclBroadcast(U, U, (size_t)(b1 - b0) * KB * KB, ncclDouble, owner, (ncclComm_t)x.nccl, stream);
+            }
+            if (ncclGroupEnd() != ncclSuccess) return GCM_ENCCL;
+        }
+#endif
+        st = check_cuda(cudaGetLastError());
+        if (st != GCM_OK) return st;
+    }
+    // 6. the Apply of every panel to this rank's tiles
+    {
+        ProfScope ps("papply", stream);
+        const size_t smem_t2 = t2_smem_bytes(KB);
+        st = check_cuda(
+            cudaFuncSetAttribute(papply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t2));
+        if (st != GCM_OK) return st;
+        for (auto &q : rk) {
+            ApplyMap map{q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff), q.plan.nloc};
+            if (q.tma && !q.plan.full.empty())
+                papply_kernel<KB><<<(unsigned)q.plan.full.size(), kT2Threads, smem_t2, stream>>>(
+                    q.tm, n, k, q.at<double>(q.cv.chk), q.at<double>(q.cv.U), q.at<double>(q.cv.panels), NB64,
+                    q.at<int2>(q.cv.full), map);
+            if (!q.plan.tiles.empty())
+                ptile_kernel<KB><<<(unsigned)q.plan.tiles.size(), kD, 0, stream>>>(
+                    q.L, q.ldl, q.plan.nloc, k, q.at<double>(q.cv.chk), q.at<double>(q.cv.U),
+                    q.at<double>(q.cv.panels), q.at<int2>(q.cv.tiles), q.at<int64_t>(q.cv.chkoff));
+        }
+        st = check_cuda(cudaGetLastError());
+    }
+    return st;
+}
+
+// The host layout arrays live as long as the process (keyed by layout), so the
+// asynchronous uploads below never read freed memory.
+std::mutex g_plan_mutex;
+std::map<std::tuple<int64_t, int64_t, int, int, int, bool>, Plan> g_plans;
+const Plan &get_plan(int64_t n, int64_t nb, int R, int r, int k, bool tma) {
+    std::lock_guard<std::mutex> lock(g_plan_mutex);
+    auto key = std::make_tuple(n, nb, R, r, k, tma);
+    auto it = g_plans.find(key);
+    if (it == g_plans.end()) it = g_plans.emplace(key, make_plan(n, nb, R, r, k, tma)).first;
+    return it->second;
+}
+
+gcm_status_t upload(const Rank &q, cudaStream_t stream) {
+    auto up = [&](size_t off, const void *src, size_t bytes) {
+        return bytes ? check_cuda(cudaMemcpyAsync(q.ws + off, src, bytes, cudaMemcpyHostToDevice, stream)) : GCM_OK;
+    };
+    gcm_status_t st = up(q.cv.gstrip, q.plan.gstrip.data(), q.plan.gstrip.size() * 4);
+    if (st == GCM_OK) st = up(q.cv.chkoff, q.plan.chkoff.data(), q.plan.chkoff.size() * 8);
+    if (st == GCM_OK) st = up(q.cv.dlb, q.plan.dl_b.data(), q.plan.dl_b.size() * 4);
+    if (st == GCM_OK) st = up(q.cv.dllc, q.plan.dl_lc.data(), q.plan.dl_lc.size() * 8);
+    if (st == GCM_OK) st = up(q.cv.full, q.plan.full.data(), q.plan.full.size() * 8);
+    if (st == GCM_OK) st = up(q.cv.tiles, q.plan.tiles.data(), q.plan.tiles.size() * 8);
+    return st;
+}
+
+// Runs the whole modification for the ranks in `rk` (each with L, ldl, V set).  Virtual
+// mode: all R ranks of the job, in this process, on one stream; Nccl / Peer: this process's
+// one rank.  d_info receives the global first failure.
+gcm_status_t panel_modify(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int64_t k, int sigma,
+                          gcm_info_t *d_info, Exchange x, cudaStream_t stream) {
+    gcm_status_t st = GCM_OK;
+    const int kc0 = (int)std::min<int64_t>(k, kPassK);
+    // workspace: one carve per rank, back to back (sized for the widest pass)
+    size_t total = 0;
+    std::vector<size_t> base(rk.size());
+    for (size_t i = 0; i < rk.size(); ++i) {
+        const int r = x.mode == Mode::Virtual ? (int)i : x.self;
+        const int64_t nloc = local_cols(n, nb, R, r);
+        // the Apply's TMA path needs a tensor map over the local columns (16-byte aligned L,
+        // even ldl); otherwise every tile goes through ptile_kernel
+        rk[i].tma = nloc > 0 && encode_tmap_f64(&rk[i].tm, rk[i].L, 2, n, nloc, rk[i].ldl, 1, 0, (unsigned)kT2Rows,
+                                                 (unsigned)kT2Box, CU_TENSOR_MAP_SWIZZLE_64B);
+        rk[i].plan = get_plan(n, nb, R, r, kc0, rk[i].tma);
+        rk[i].cv = carve(rk[i].plan);
+        base[i] = total;
+        total += rk[i].cv.total;
+    }
+    Workspace *ws = nullptr;
+    st = get_workspace(stream, total, 1, &ws);
+    if (st != GCM_OK) return st;
+    char *wsb = reinterpret_cast<char *>(ws->panels);
+    if (x.mode == Mode::Virtual) {  // one key per rank + the min
+        for (size_t i = 0; i < rk.size(); ++i) rk[i].ws = wsb + base[i];
+    } else {
+        rk[0].ws = wsb;
+    }
+    for (auto &q : rk) {
+        st = upload(q, stream);
+        if (st != GCM_OK) return st;
+        st = check_cuda(cudaMemsetAsync(q.ws + q.cv.key, 0xff, 8, stream));
+        if (st != GCM_OK) return st;
+    }
+    for (int64_t e0 = 0; e0 < k; e0 += kPassK) {
+        const int kc = (int)std::min<int64_t>(kPassK, k - e0);
+        if (++ws->epoch == 0xffffffffu || ws->epoch == 0) ws->epoch = 1;
+        const unsigned epoch = ws->epoch;
+        std::vector<Rank> pass = rk;
+        for (auto &q : pass) {
+            q.V = q.V + e0 * std::max<int64_t>(q.plan.nloc, 1);
+            if (kc != kc0) {  // a narrower last pass: same carve (it is sized for kc0 >= kc)
+                Plan p = get_plan(n, nb, R, x.mode == Mode::Virtual ? (int)(&q - pass.data()) : x.self, kc, q.tma);
+                p.k = kc;
+                q.plan = p;  // identical layout arrays; only k / KB change
+            }
+        }
+        const int KBp = pass[0].plan.KB;
+        if (KBp <= 4) st = panel_pass<4>(pass, R, n, nb, kc, sigma, e0, epoch, x, stream);
+        else if (KBp <= 8) st = panel_pass<8>(pass, R, n, nb, kc, sigma, e0, epoch, x, stream);
+        else if (KBp <= 16) st = panel_pass<16>(pass, R, n, nb, kc, sigma, e0, epoch, x, stream);
+        else st = panel_pass<32>(pass, R, n, nb, kc, sigma, e0, epoch, x, stream);
+        if (st != GCM_OK) return st;
+    }
+    // global first failure
+    unsigned long long *key0 = rk[0].at<unsigned long long>(rk[0].cv.key);
+    if (x.mode == Mode::Virtual && rk.size() > 1) {
+        KeyList keys{};
+        keys.R = (int)rk.size();
+        for (size_t i = 0; i < rk.size(); ++i) keys.k[i] = rk[i].at<unsigned long long>(rk[i].cv.key);
+        keymin_kernel<<<1, 1, 0, stream>>>(ws->key, keys);
+        st = check_cuda(cudaGetLastError());
+        if (st != GCM_OK) return st;
+        return finalize_info(ws->key, d_info, 1, stream);
+    }
+#ifdef GCM_WITH_NCCL
+    if (x.mode != Mode::Virtual) {
+        if (ncclAllReduce(key0, key0, 1, ncclUint64, ncclMin, (ncclComm_t)x.nccl, stream) != ncclSuccess)
+            return GCM_ENCCL;
+    }
+#endif
+    return finalize_info(key0, d_info, 1, stream);
+}
+
+}  // namespace
+
+// GCM_ALGO_PANEL on one GPU: the sharded algorithm with one rank (nb = 512).
+gcm_status_t modify_panel(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma, gcm_info_t *d_info,
+                          cudaStream_t stream) {
+    std::vector<Rank> rk(1);
+    rk[0].L = L;
+    rk[0].ldl = ldl;
+    rk[0].V = V;
+    Exchange x{Mode::Virtual, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
+    return panel_modify(rk, 1, n, 512, k, sigma, d_info, x, stream);
+}
+
+}  // namespace gcm
+
+using namespace gcm;
+
+extern "C" {
+
+int64_t gcm_dist_local_cols(int64_t n, int64_t nb, int nranks, int rank) { return local_cols(n, nb, nranks, rank); }
+
+int64_t gcm_dist_global_col(int64_t nb, int nranks, int rank, int64_t local_col) {
+    if (nb <= 0 || nranks <= 0 || rank < 0 || rank >= nranks || local_col < 0) return -1;
+    return global_col(nb, nranks, rank, local_col);
+}
+
+int64_t gcm_dist_plan(int64_t n, int64_t nb, int nranks, int rank, int what, int64_t *out, int64_t cap) {
+    if (n < 0 || nb <= 0 || nb % kD != 0 || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) return -1;
+    if (what < 0 || what > 2 || cap < 0 || (cap > 0 && !out)) return -1;
+    const Plan &p = get_plan(n, nb, nranks, rank, 1, true);
+    int64_t cnt = 0;
+    auto put = [&](int64_t v) {
+        if (cnt < cap) out[cnt] = v;
+        ++cnt;
+    };
+    if (what == 0) {  // Apply tiles (b, global strip), TMA groups expanded
+        for (const int2 &it : p.full)
+            for (int q = 0; q < 4 && it.y + q < p.nsl; ++q) {
+                const int sl = it.y + q;
+                if ((sl * kD) / nb != (it.y * kD) / nb) break;  // groups never leave a column block
+                put(it.x);
+                put(p.gstrip[sl]);
+            }
+        for (const int2 &it : p.tiles) {
+            put(it.x);
+            put(p.gstrip[it.y]);
+        }
+    } else if (what == 1) {
+        for (int b : p.dl_b) put(b);
+    } else {
+        for (int g = 0; g < p.NBc; ++g)
+            if (g % nranks == rank) put(g);
+    }
+    return cnt;
+}
+
+static gcm_status_t dist_args(int64_t n, int64_t nb, int64_t k, int sigma) {
+    if (n < 0 || k < 0 || nb <= 0 || nb % kD != 0 || (sigma != 1 && sigma != -1)) return GCM_EINVAL;
+    if (n >= (1ll << 31) || k >= (1ll << 22)) return GCM_EINVAL;
+    return GCM_OK;
+}
+
+gcm_status_t gcm_modify_dist_virtual(int nranks, double *const *L_local, int64_t n, int64_t nb,
+                                     const int64_t *ldl_local, double *const *V_local, int64_t k, int sigma,
+                                     gcm_info_t *d_info, gcm_stream_t stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (nranks < 1 || nranks > kMaxRanks || !L_local || !ldl_local || !V_local) return GCM_EINVAL;
+    gcm_status_t st = dist_args(n, nb, k, sigma);
+    if (st != GCM_OK) return st;
+    std::vector<Rank> rk(nranks);
+    for (int r = 0; r < nranks; ++r) {
+        const int64_t nloc = local_cols(n, nb, nranks, r);
+        if (ldl_local[r] < std::max<int64_t>(1, n)) return GCM_EINVAL;
+        if (n > 0 && k > 0 && nloc > 0 && (!L_local[r] || !V_local[r])) return GCM_EINVAL;
+        rk[r].L = L_local[r];
+        rk[r].ldl = ldl_local[r];
+        rk[r].V = V_local[r];
+    }
+    clear_stale_error();
+    if (n == 0 || k == 0) return d_info ? check_cuda(cudaMemsetAsync(d_info, 0, sizeof(gcm_info_t), stream)) : GCM_OK;
+    Exchange x{Mode::Virtual, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
+    return panel_modify(rk, nranks, n, nb, k, sigma, d_info, x, stream);
+}
+
+#ifdef GCM_WITH_NCCL
+
+static gcm_status_t check_nccl(ncclResult_t r) { return r == ncclSuccess ? GCM_OK : GCM_ENCCL; }
+
+gcm_status_t gcm_comm_unique_id(void *host_id_out) {
+    if (!host_id_out) return GCM_EINVAL;
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    ncclUniqueId id;
+    gcm_status_t st = check_nccl(ncclGetUniqueId(&id));
+    if (st == GCM_OK) std::memcpy(host_id_out, &id, sizeof(id));
+    return st;
+}
+
+gcm_status_t gcm_comm_init(gcm_comm_t *comm, const void *host_id, int nranks, int rank) {
+    if (!comm || !host_id || nranks <= 0 || nranks > kMaxRanks || rank < 0 || rank >= nranks) return GCM_EINVAL;
+    clear_stale_error();
+    gcm_comm *c = new (std::nothrow) gcm_comm;
+    if (!c) return GCM_ENOMEM;
+    ncclUniqueId id;
+    std::memcpy(&id, host_id, sizeof(id));
+    gcm_status_t st = check_nccl(ncclCommInitRank(&c->nc, nranks, id, rank));
+    if (st != GCM_OK) {
+        delete c;
+        return st;
+    }
+    c->rank = rank;
+    c->nranks = nranks;
+    *comm = c;
+    return GCM_OK;
+}
+
+gcm_status_t gcm_comm_destroy(gcm_comm_t comm) {
+    if (!comm) return GCM_EINVAL;
+    gcm_status_t st = check_nccl(ncclCommDestroy(comm->nc));
+    delete comm;
+    return st;
+}
+
+gcm_status_t gcm_modify_dist(gcm_comm_t comm, double *L_local, int64_t n, int64_t nb, int64_t ldl_local,
+                             double *V_local, int64_t k, int sigma, gcm_info_t *d_info, gcm_stream_t stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (!comm) return GCM_EINVAL;
+    gcm_status_t st = dist_args(n, nb, k, sigma);
+    if (st != GCM_OK) return st;
+    if (ldl_local < std::max<int64_t>(1, n)) return GCM_EINVAL;
+    const int R = comm->nranks, r = comm->rank;
+    const int64_t nloc = local_cols(n, nb, R, r);
+    if (n > 0 && k > 0 && nloc > 0 && (L_local == nullptr || V_local == nullptr)) return GCM_EINVAL;
+    clear_stale_error();
+    if (n == 0 || k == 0) return d_info ? check_cuda(cudaMemsetAsync(d_info, 0, sizeof(gcm_info_t), stream)) : GCM_OK;
+    std::vector<Rank> rk(1);
+    rk[0].L = L_local;
+    rk[0].ldl = ldl_local;
+    rk[0].V = V_local;
+    Exchange x{Mode::Nccl, comm->nc, r, nullptr, nullptr, nullptr, nullptr, nullptr};
+    return panel_modify(rk, R, n, nb, k, sigma, d_info, x, stream);
+}
+
+#else  // built without NCCL
+
+gcm_status_t gcm_comm_unique_id(void *) { return GCM_ENOTSUP; }
+gcm_status_t gcm_comm_init(gcm_comm_t *, const void *, int, int) { return GCM_ENOTSUP; }
+gcm_status_t gcm_comm_destroy(gcm_comm_t) { return GCM_ENOTSUP; }
+gcm_status_t gcm_modify_dist(gcm_comm_t, double *, int64_t, int64_t, int64_t, double *, int64_t, int, gcm_info_t *,
+                             gcm_stream_t) {
+    return GCM_ENOTSUP;
+}
+
+#endif
+
+}  // extern "C"

@@ -83,4 +83,66 @@ def modify_dist(comm: Comm, L_local, V_local, n: int, nb: int, sigma: int, info=
     _native.check("gcm_modify_dist", st)
 
 
-__all__ = ["Comm", "modify_dist", "local_cols", "global_cols", "GcmError"]
+def plan(n: int, nb: int, world: int, rank: int, what: str) -> np.ndarray:
+    """The work `rank` does in modify_dist (gcm_dist_plan): what = "tiles" -> (b, s) pairs of
+    its Apply tiles, "diag" -> its 64-row diagonal blocks, "solve" -> the column blocks whose
+    rows of P it solves.  Host only."""
+    code = {"tiles": 0, "diag": 1, "solve": 2}[what]
+    lib = _native.lib()
+    cnt = lib.gcm_dist_plan(n, nb, world, rank, code, None, 0)
+    if cnt < 0:
+        raise ValueError("invalid block-cyclic layout arguments")
+    out = np.zeros(max(cnt, 1), dtype=np.int64)
+    lib.gcm_dist_plan(n, nb, world, rank, code, ctypes.c_void_p(out.ctypes.data), cnt)
+    out = out[:cnt]
+    return out.reshape(-1, 2) if code == 0 else out
+
+
+def modify_dist_virtual(L_locals, V_locals, n: int, nb: int, sigma: int, info=None, stream=None) -> None:
+    """All ranks of a column-sharded job on the current device, in one call (gcm_modify_dist_virtual):
+    L_locals[r] (n_local_r, ldl_r) and V_locals[r] (k, n_local_r) as for modify_dist with
+    world = len(L_locals), rank = r.  The owner of each column block writes its rows of P, and
+    each rank its panels, straight into the other ranks' buffers (device-initiated stores)."""
+    import torch
+    R = len(L_locals)
+    if R != len(V_locals) or not 1 <= R <= 8:
+        raise ValueError("1..8 ranks, one L and one V per rank")
+    k = V_locals[0].shape[0]
+    dev = L_locals[0].device
+    for r in range(R):
+        L, V = L_locals[r], V_locals[r]
+        if L.dtype != torch.float64 or V.dtype != torch.float64 or not (L.is_cuda and V.is_cuda):
+            raise ValueError("L_local and V_local must be float64 CUDA tensors")
+        if L.device != dev or V.device != dev:
+            raise ValueError("virtual ranks share one device")
+        if not (L.is_contiguous() and V.is_contiguous()) or L.dim() != 2 or V.dim() != 2:
+            raise ValueError("L_local (n_local, ldl) and V_local (k, n_local) must be contiguous")
+        nloc = local_cols(n, nb, R, r)
+        if L.shape[0] != nloc or V.shape[0] != k or (V.numel() and V.shape[1] != nloc) or L.shape[1] < max(1, n):
+            raise ValueError(f"rank {r} owns {nloc} columns")
+    Lp = (ctypes.c_void_p * R)(*[L.data_ptr() for L in L_locals])
+    Vp = (ctypes.c_void_p * R)(*[V.data_ptr() for V in V_locals])
+    ld = (ctypes.c_int64 * R)(*[L.shape[1] for L in L_locals])
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    ip = ctypes.c_void_p(info.data_ptr()) if info is not None else None
+    with torch.cuda.device(dev):
+        st = _native.lib().gcm_modify_dist_virtual(R, Lp, n, nb, ld, Vp, k, int(sigma), ip,
+                                                   ctypes.c_void_p(stream.cuda_stream))
+    _native.check("gcm_modify_dist_virtual", st)
+
+
+def shard(L_full, V_full, nb: int, world: int):
+    """Split a (n, ldl) factor buffer and (k, n) V into the block-cyclic shards of `world` ranks
+    (row c of a shard = global column global_cols()[c]).  Torch ops; a test/bench helper."""
+    n = L_full.shape[0]
+    out = []
+    for r in range(world):
+        g = global_cols(n, nb, world, r)
+        import torch
+        idx = torch.from_numpy(g).to(L_full.device)
+        out.append((L_full.index_select(0, idx).contiguous(), V_full.index_select(1, idx).contiguous(), g))
+    return out
+
+
+__all__ = ["Comm", "modify_dist", "modify_dist_virtual", "plan", "shard", "local_cols", "global_cols", "GcmError"]

@@ -2,12 +2,13 @@
 
 * the block-cyclic ownership functions exported by libgcm (gcm_dist_local_cols,
   gcm_dist_global_col) partition the columns correctly;
-* a world_size-2 gloo run of the SAME schedule dist.cu executes (owner of the
-  columns of each 64-row block computes its rotations, one broadcast per block from
-  that owner, every rank applies them to its own columns to the right; V rows follow
-  their columns), with the oracle as the per-rank arithmetic, reproduces the
-  single-process oracle result.  This pins the ownership/broadcast choreography;
-  the GPU kernels themselves are covered by the -m gpu tests.
+* a world_size-2 (and 3) gloo job in which every rank asks the library for ITS share of
+  gcm_modify_dist's work (gcm_dist_plan: the Apply tiles, the 64-row diagonal blocks it
+  sweeps, the column blocks whose rows of P it solves) and the ranks all-gather them: the
+  union must cover every tile (b < s), diagonal block and column block exactly once, every
+  tile must lie in the rank's own columns, and the owner of column block g must be rank
+  g mod R.  This pins the C++ planner the GPU path runs (panel.cu make_plan); the GPU
+  kernels themselves are covered by tests/test_gpu_dist.py (virtual ranks on one GPU).
 """
 import os
 import socket
@@ -40,6 +41,8 @@ def test_invalid_layout():
         gdist.local_cols(10, 0, 2, 0)
     with pytest.raises(ValueError):
         gdist.local_cols(10, 64, 2, 2)
+    with pytest.raises(ValueError):
+        gdist.plan(100, 48, 2, 0, "tiles")  # nb must be a multiple of 64
 
 
 def _free_port():
@@ -50,71 +53,51 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, n, k, nb, sigma, outdir):
+def _rank_main(rank, world, port, cases, outdir):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    import torch
     import torch.distributed as dist
 
-    import oracle
-    import synth
+    from paper_1011_1173_b200 import dist as gd
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=123)
-    gcols = gdist.global_cols(n, nb, world, rank)
-    Lloc = Lbuf[gcols].copy()       # local columns, all rows (row c of Lloc = column gcols[c])
-    Vloc = Vbuf[:, gcols].copy()    # V entries of the local columns
-    for b in range((n + D - 1) // D):
-        r0 = b * D
-        Db = min(D, n - r0)
-        owner = (r0 // nb) % world
-        cs = torch.zeros(2, Db, k, dtype=torch.float64)
-        if owner == rank:
-            lc = np.searchsorted(gcols, np.arange(r0, r0 + Db))
-            assert np.array_equal(gcols[lc], np.arange(r0, r0 + Db))
-            Lbb = np.zeros((Db, Db))
-            Lbb[:, :] = Lloc[lc][:, r0:r0 + Db]  # rows of Lbb = block columns
-            Vb = np.ascontiguousarray(Vloc[:, lc])
-            c, s, _ = oracle.modify_a(Lbb, Vb, sigma)  # the diagonal chain of block b
-            Lloc[lc, r0:r0 + Db] = Lbb
-            Vloc[:, lc] = Vb
-            cs[0] = torch.from_numpy(c)
-            cs[1] = torch.from_numpy(s)
-        dist.broadcast(cs, src=owner)  # the one exchange step per block
-        c, s = cs[0].numpy(), cs[1].numpy()
-        right = np.nonzero(gcols >= r0 + D)[0]
-        for j in range(Db):  # Apply (PAPER.md 52-54) to the rank's columns right of the block
-            for e in range(k):
-                Lr = Lloc[right, r0 + j]
-                Vr = Vloc[e, right]
-                lnew = (Lr + sigma * s[j, e] * Vr) / c[j, e]
-                Lloc[right, r0 + j] = lnew
-                Vloc[e, right] = c[j, e] * Vr - s[j, e] * lnew
-    np.save(os.path.join(outdir, f"L{rank}.npy"), Lloc)
-    np.save(os.path.join(outdir, f"V{rank}.npy"), Vloc)
+    for ci, (n, nb) in enumerate(cases):
+        mine = {w: gd.plan(n, nb, world, rank, w).tolist() for w in ("tiles", "diag", "solve")}
+        mine["cols"] = gd.global_cols(n, nb, world, rank).tolist()
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine)
+        if rank == 0:
+            import json
+            with open(os.path.join(outdir, f"case{ci}.json"), "w") as f:
+                json.dump(everyone, f)
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("sigma", [1, -1])
-def test_gloo_world2_schedule_matches_oracle(tmp_path, sigma):
-    import torch.multiprocessing as mp
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_plan_covers_the_factor_once(tmp_path, world):
+    import json
 
-    import oracle
-    import synth
-    from gcm_testutil import rel_fro, upper
-    n, k, nb, world = 300, 3, 64, 2
-    port = _free_port()
-    mp.spawn(_rank_main, args=(world, port, n, k, nb, sigma, str(tmp_path)), nprocs=world, join=True)
-    Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=123)
-    Lo, Vo = Lbuf.copy(), Vbuf.copy()
-    oracle.modify_a(Lo, Vo, sigma)
-    Lg = np.zeros_like(Lbuf)
-    Vg = np.zeros_like(Vbuf)
-    for r in range(world):
-        g = gdist.global_cols(n, nb, world, r)
-        Lg[g] = np.load(tmp_path / f"L{r}.npy")
-        Vg[:, g] = np.load(tmp_path / f"V{r}.npy")
-    assert rel_fro(upper(Lg), upper(Lo)) < 1e-13
-    assert rel_fro(Vg, Vo) < 1e-12
+    import torch.multiprocessing as mp
+    cases = [(300, 64), (1000, 256), (2113, 512), (777, 128)]
+    mp.spawn(_rank_main, args=(world, _free_port(), cases, str(tmp_path)), nprocs=world, join=True)
+    for ci, (n, nb) in enumerate(cases):
+        everyone = json.load(open(tmp_path / f"case{ci}.json"))
+        NB = (n + D - 1) // D
+        NBc = (n + nb - 1) // nb
+        tiles, diag, solve = [], [], []
+        for r, w in enumerate(everyone):
+            cols = set(w["cols"])
+            for b, s in w["tiles"]:
+                assert b < s and s * D in cols, (r, b, s)  # the rank's own columns, above the diagonal
+                tiles.append((b, s))
+            for b in w["diag"]:
+                assert b * D in cols
+                diag.append(b)
+            for g in w["solve"]:
+                assert g % world == r
+                solve.append(g)
+        assert sorted(tiles) == sorted((b, s) for s in range(NB) for b in range(s))
+        assert sorted(diag) == list(range(NB))
+        assert sorted(solve) == list(range(NBc))

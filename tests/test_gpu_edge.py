@@ -109,7 +109,7 @@ def rho2(Lbuf, V):
     return float(np.linalg.eigvalsh(np.eye(V.shape[0]) - P.T @ P).min())
 
 
-@pytest.mark.parametrize("algo", ["sweep", "blocked"])
+@pytest.mark.parametrize("algo", ["sweep", "blocked", "panel"])
 @pytest.mark.parametrize("delta", [1e-2, 1e-4, 1e-6, 1e-8])
 @pytest.mark.parametrize("n,k,m", [(200, 1, 77), (700, 4, 300), (700, 16, 640), (2000, 16, 1500)])
 def test_near_singular_downdate(gcm, algo, delta, n, k, m):
@@ -163,7 +163,7 @@ NAN_CASES = {
 }
 
 
-@pytest.mark.parametrize("algo", ["sweep", "blocked"])
+@pytest.mark.parametrize("algo", ["sweep", "blocked", "panel"])
 @pytest.mark.parametrize("case", sorted(NAN_CASES))
 @pytest.mark.parametrize("sigma", [1, -1])
 def test_nan_input_reported(gcm, algo, case, sigma):

@@ -66,7 +66,7 @@ SIZES = [1, 2, 3, 31, 63, 64, 65, 127, 128, 129, 200]
 RANKS = [1, 2, 3, 8, 15, 16, 17, 33, 64, 65]
 
 
-ALGOS = ["sweep", "blocked", "auto"]
+ALGOS = ["sweep", "blocked", "panel", "auto"]
 
 
 @pytest.mark.parametrize("algo", ALGOS)
