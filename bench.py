@@ -30,6 +30,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # no version banner: the JSON line is the only stdout line
 
 import numpy as np  # noqa: E402
 
@@ -49,6 +50,9 @@ CONFIGS = {
     # BASELINE configs[3] at one GPU: 80 GB factor, direct-L construction generated on the
     # device (R18), checked by the column-norm identity at full size
     "n100000_k32": dict(n=100000, k=32, direct=True),
+    # BASELINE configs[3] column-sharded over the job's GPUs (gcm_modify_dist, NCCL; nb = 512
+    # block-cyclic columns); strong scaling: the same 80 GB factor for every N
+    "n100000_k32_dist": dict(n=100000, k=32, direct=True, dist=True, nb=512),
 }
 
 
@@ -207,7 +211,25 @@ def run_ours(args, world, rank, local):
     batch = cfg.get("batch", 1)
     stream = torch.cuda.current_stream(dev)
 
-    if cfg.get("direct"):
+    comm = gcols = None
+    if cfg.get("dist"):
+        # this rank's block-cyclic shard of the direct-L instance (R18), drawn on the
+        # device: row c of L is global column gcols[c] (its entries above the diagonal
+        # (2U-1)/sqrt(n), diagonal U[1,2)), V rows U/sqrt(n)
+        from paper_1011_1173_b200 import dist as gdist
+        nb = cfg["nb"]
+        gcols_np = gdist.global_cols(n, nb, world, rank)
+        gcols = torch.from_numpy(gcols_np).to(dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(synth.SEED_ROOT + 1000 + rank)
+        L = torch.empty((len(gcols_np), n), dtype=torch.float64, device=dev)
+        L.uniform_(-1.0 / n ** 0.5, 1.0 / n ** 0.5, generator=g)
+        rows = torch.arange(len(gcols_np), device=dev)
+        L[rows, gcols] = 1.0 + torch.rand(len(gcols_np), dtype=torch.float64, device=dev, generator=g)
+        V0 = torch.rand((k, len(gcols_np)), dtype=torch.float64, device=dev, generator=g) / n ** 0.5
+        Lbuf = Vbuf = None
+        comm = gdist.Comm(rank, world)
+    elif cfg.get("direct"):
         # direct-L instance (R18) drawn on the device with torch's seeded Philox
         # generator: L_ii ~ U[1,2), L_ij ~ (2U-1)/sqrt(n), V ~ U/sqrt(n); update then downdate
         g = torch.Generator(device=dev)
@@ -233,7 +255,9 @@ def run_ours(args, world, rank, local):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def call(sigma):
-        if batch == 1:
+        if comm is not None:
+            gdist.modify_dist(comm, L, V, n, cfg["nb"], sigma)
+        elif batch == 1:
             gcm.modify(L, V, sigma, algo=args.algo)
         else:
             gcm.modify_batched(L, V, sigma)
@@ -244,6 +268,7 @@ def run_ours(args, world, rank, local):
         call(+1 if i % 2 == 0 else -1)
     torch.cuda.synchronize()
     gcm.profile_read()
+    gcm.profile_launches()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(torch.cuda.current_device())
@@ -268,9 +293,11 @@ def run_ours(args, world, rank, local):
     check = None
     if cfg.get("direct"):
         # full-size property pin: ||L~_{:,c}||^2 = ||L_{:,c}||^2 + sigma ||V_{c,:}||^2
-        # on 256 sampled columns, one more (untimed) update
-        cols = torch.randperm(n, device=dev, generator=torch.Generator(device=dev).manual_seed(7))[:256]
-        mask = torch.arange(n, device=dev)[None, :] <= cols[:, None]
+        # on 256 sampled (local) columns, one more (untimed) update
+        nl = L.shape[0]
+        cols = torch.randperm(nl, device=dev, generator=torch.Generator(device=dev).manual_seed(7))[:256]
+        gc = gcols[cols] if gcols is not None else cols
+        mask = torch.arange(n, device=dev)[None, :] <= gc[:, None]
         before = ((L[cols] * mask) ** 2).sum(1)
         V.copy_(V0)
         vnorm = (V0[:, cols] ** 2).sum(0)
@@ -285,12 +312,13 @@ def run_ours(args, world, rank, local):
     total_ms = max_over_ranks(sum(step_ms), world)
     ms_per_step = total_ms / args.steps
     applies, flops, bytes_ = algorithmic(n, k, batch)
-    value = world * flops / (ms_per_step * 1e-3) / 1e9  # GFLOP/s, whole job
+    # GFLOP/s of the whole job: replicas / factor shards (weak) add up; one sharded factor (strong) does not
+    value = (1 if comm is not None else world) * flops / (ms_per_step * 1e-3) / 1e9
 
     # dominant kernel and its roofline (bytes/flops per launch from DESIGN.md "roofline")
     hbm, hbm_src = measured_peaks()
     # kernels per profiling scope: 'blocked' = trsv_kernel + its programmatic-dependent btma_kernel
-    launches = sum(c * (2 if name == "blocked" else 1) for name, (c, _) in prof.items())
+    launches = gcm.profile_launches()  # counted by the library at every launch site
     dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 0.0))
     dname, (dcount, dms) = dom
     per_launch_ms = dms / max(dcount, 1)
@@ -324,11 +352,13 @@ def run_ours(args, world, rank, local):
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if comm is not None else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config, n, k, batch * world),
-                   "n": n, "k": k, "batch_per_gpu": batch, "algo": args.algo if batch == 1 else "batched",
+                   "n": n, "k": k, "batch_per_gpu": batch,
+                   "algo": "dist (gcm_modify_dist, NCCL)" if comm is not None else (args.algo if batch == 1 else "batched"),
                    "sigma": "alternating +1/-1 by the same V", "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": f"replicas x{world}" if batch == 1 else f"factor-sharded x{world}",
+                   "parallelism": (f"column-sharded x{world} (block-cyclic nb={cfg['nb']})" if comm is not None else
+                                   f"replicas x{world}" if batch == 1 else f"factor-sharded x{world}"),
                    "instance": ("direct-L (DESIGN.md R18) on the device, torch Philox seed 10111173+rank"
                                 if cfg.get("direct") else
                                 "paper construction (PAPER.md 111): B,V ~ U[0,1), A = B^T B + I, seed 10111173+rank")},

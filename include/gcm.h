@@ -141,6 +141,13 @@ typedef struct gcm_comm *gcm_comm_t;
 gcm_status_t gcm_comm_unique_id(void *host_id_out /* 128 bytes */);
 gcm_status_t gcm_comm_init(gcm_comm_t *comm, const void *host_id, int nranks, int rank);
 gcm_status_t gcm_comm_destroy(gcm_comm_t comm);
+/* on != 0: later gcm_modify_dist calls on this communicator exchange P rows and coefficient
+ * panels by DEVICE-INITIATED stores into the other ranks' memory (CUDA IPC windows mapped at
+ * the first call, NVLink peer stores, system-scope release flags / counters that the
+ * consumers' kernels acquire) instead of ncclBroadcast; NCCL is then used only to exchange
+ * the IPC handles, for one barrier per pass and the final failure all-reduce.  Collective:
+ * every rank sets the same mode.  (Verified on one GPU with one rank.) */
+gcm_status_t gcm_comm_set_peer(gcm_comm_t comm, int on);
 /* Number of columns rank `rank` owns (block-cyclic, width nb), or -1 on bad arguments. Host only. */
 int64_t gcm_dist_local_cols(int64_t n, int64_t nb, int nranks, int rank);
 /* Global column index of local column `local_col` of rank `rank`, or -1. Host only. */
@@ -178,6 +185,9 @@ gcm_status_t gcm_modify_dist_virtual(int nranks, double *const *L_local, int64_t
  * of entries written (or -1 on a CUDA error). */
 gcm_status_t gcm_profile_enable(int on);
 int gcm_profile_read(char *names, int64_t *counts, double *ms, int max_entries);
+/* Number of kernels the library launched (all streams) while profiling was enabled, since the
+ * last call; resets the count. */
+int64_t gcm_profile_launches(void);
 
 /* Human-readable status. */
 const char *gcm_status_string(gcm_status_t s);

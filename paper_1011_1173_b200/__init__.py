@@ -169,5 +169,10 @@ def profile_read(max_entries: int = 32):
     return out
 
 
+def profile_launches() -> int:
+    """Kernels the library launched while profiling was enabled, since the last call (resets)."""
+    return int(_native.lib().gcm_profile_launches())
+
+
 def release_workspace() -> None:
     _native.check("gcm_release_workspace", _native.lib().gcm_release_workspace())

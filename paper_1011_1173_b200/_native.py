@@ -28,6 +28,7 @@ SIGNATURES = {
     "gcm_comm_unique_id": (_int, [_vp]),
     "gcm_comm_init": (_int, [ctypes.POINTER(_vp), _vp, _int, _int]),
     "gcm_comm_destroy": (_int, [_vp]),
+    "gcm_comm_set_peer": (_int, [_vp, _int]),
     "gcm_dist_local_cols": (_i64, [_i64, _i64, _int, _int]),
     "gcm_dist_global_col": (_i64, [_i64, _int, _int, _i64]),
     "gcm_modify_dist": (_int, [_vp, _dp, _i64, _i64, _i64, _dp, _i64, _int, _vp, _vp]),
@@ -35,6 +36,7 @@ SIGNATURES = {
     "gcm_dist_plan": (_i64, [_i64, _i64, _int, _int, _int, _vp, _i64]),
     "gcm_profile_enable": (_int, [_int]),
     "gcm_profile_read": (_int, [ctypes.c_char_p, _vp, _vp, _int]),
+    "gcm_profile_launches": (_i64, []),
     "gcm_status_string": (ctypes.c_char_p, [_int]),
     "gcm_release_workspace": (_int, []),
     "gcm_version": (ctypes.c_char_p, []),

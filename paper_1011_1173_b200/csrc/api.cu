@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -31,6 +32,10 @@ gcm_status_t check_cuda(cudaError_t e) {
 }
 
 bool g_profile_on = false;
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) {
+    if (g_profile_on) g_launches += n;
+}
 
 namespace {
 
@@ -202,6 +207,7 @@ gcm_status_t finalize_info(const unsigned long long *key, gcm_info_t *d_info, in
     const int threads = 128;
     const unsigned grid = (unsigned)((count + threads - 1) / threads);
     info_finalize_kernel<<<grid, threads, 0, stream>>>(key, d_info, count);
+    count_launch();
     return check_cuda(cudaGetLastError());
 }
 
@@ -382,6 +388,8 @@ int gcm_profile_read(char *names, int64_t *counts, double *ms, int max_entries) 
     }
     return n;
 }
+
+int64_t gcm_profile_launches(void) { return (int64_t)g_launches.exchange(0); }
 
 const char *gcm_status_string(gcm_status_t s) {
     switch (s) {

@@ -404,6 +404,7 @@ bool batched_tma_launch(double *L, int64_t n, int64_t ldl, int64_t strideL, doub
         batched_tma_kernel<KB, SLOTS><<<grid, kBT, smem, stream>>>(tm, L + f0 * strideL, n, ldl, strideL,
                                                                    V + f0 * strideV, strideV, k, sigma, keys + f0,
                                                                    stage);
+        count_launch();
     }
     *st = check_cuda(cudaGetLastError());
     return true;
@@ -421,6 +422,7 @@ gcm_status_t batched_launch_s(double *L, int64_t n, int64_t ldl, int64_t strideL
         ProfScope ps("batched", stream);
         batched_kernel<KB, SLOTS><<<grid, kBT, smem, stream>>>(L + f0 * strideL, n, ldl, strideL, V + f0 * strideV,
                                                                strideV, k, sigma, keys + f0);
+        count_launch();
     }
     return check_cuda(cudaGetLastError());
 }

@@ -1331,6 +1331,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         const double *chk = a.chk;
+        count_launch(2);  // the TRSV kernel above and this Apply grid
         return check_cuda(cudaLaunchKernelEx(&cfg, btma_kernel<KB>, tm2, n, k, chk, (const double *)U,
                                              (const double *)panels, (int)lay.NB, w));
     }
@@ -1338,6 +1339,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
         ProfScope ps("trsv", stream);
         st = check_cuda(cudaLaunchCooperativeKernel((const void *)trsv_kernel<KB>, dim3(grid), dim3(kTrsvThreads),
                                                     args, smem, stream));
+        count_launch();
     }
     if (st != GCM_OK) return st;
 
@@ -1355,11 +1357,13 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
             const dim3 gridt(lay.NB - 1, (lay.NB - 1 + kStripsPerCta - 1) / kStripsPerCta);
             ProfScope ps("bapply", stream);
             btile_kernel<KB><<<gridt, kTileThreads, smem_tile, stream>>>(L, n, ldl, k, a.chk, U, panels, lay.NB);
+            count_launch();
             return check_cuda(cudaGetLastError());
         }
         const dim3 grid2(lay.NB - 1, (lay.NB - 1 + lay.CI - 1) / lay.CI);
         ProfScope ps("bapply", stream);
         bapply_kernel<KB><<<grid2, kApplyT, smem_apply, stream>>>(L, n, ldl, k, a.chk, lay.CI, U, panels);
+        count_launch();
     }
     return check_cuda(cudaGetLastError());
 }

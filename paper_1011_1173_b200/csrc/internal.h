@@ -47,6 +47,8 @@ void clear_stale_error();
 // Profiling hook (gcm_profile_enable): bracket a launch with events on `stream`.
 // Usage: { ProfScope ps("trsv", stream); kernel<<<..., stream>>>(...); }
 extern bool g_profile_on;
+// kernels this library launched while profiling is on (gcm_profile_launches)
+void count_launch(int n = 1);
 void prof_record(const char *name, cudaStream_t stream, bool begin);
 struct ProfScope {
     const char *name;

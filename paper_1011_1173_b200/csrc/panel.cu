@@ -50,6 +50,12 @@ struct gcm_comm {
 #endif
     int rank = 0;
     int nranks = 1;
+    int peer = 0;          // 1: device-initiated exchange through an IPC window (gcm_comm_set_peer)
+    unsigned epoch = 0;    // peer mode: pass counter (identical on every rank)
+    char *win = nullptr;   // this rank's window: [P | panels | U | flags | counter]
+    size_t win_bytes = 0;
+    char *peers[8] = {};   // every rank's window mapped into this process (peers[rank] = win)
+    size_t offP = 0, offPan = 0, offU = 0, offFlag = 0, offCtr = 0;
 };
 
 namespace gcm {
@@ -594,10 +600,15 @@ struct Rank {
     char *ws;
     CUtensorMap tm;
     bool tma;
+    // PEER mode: the replicated buffers live in the comm's IPC window (peers write into them)
+    double *Pw = nullptr, *panw = nullptr, *Uw = nullptr;
     template <typename T>
     T *at(size_t off) const {
         return reinterpret_cast<T *>(ws + off);
     }
+    double *Pbuf() const { return Pw ? Pw : at<double>(cv.P); }
+    double *panbuf() const { return panw ? panw : at<double>(cv.panels); }
+    double *Ubuf() const { return Uw ? Uw : at<double>(cv.U); }
 };
 
 template <int KB>
@@ -616,6 +627,7 @@ size_t pdiag_smem() {
 
 struct Exchange {
     Mode mode;
+    unsigned *epoch;   // Peer mode: the comm's call counter (identical on every rank); else the workspace's
     void *nccl;        // ncclComm_t (Nccl / Peer modes)
     int self;          // this process's rank (Nccl / Peer); 0 in Virtual mode
     double **peerP;    // Peer mode: every rank's P, panels, Ui buffers and flag words (IPC-mapped)
@@ -664,10 +676,10 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         Peers p{};
         if (x.mode == Mode::Virtual) {
             p.R = R;
-            for (int r = 0; r < R; ++r) p.dst[r] = rk[r].at<double>(rk[r].cv.P);
+            for (int r = 0; r < R; ++r) p.dst[r] = rk[r].Pbuf();
         } else if (x.mode == Mode::Nccl) {
             p.R = 1;
-            p.dst[0] = rk[owner_local].at<double>(rk[owner_local].cv.P);
+            p.dst[0] = rk[owner_local].Pbuf();
         } else {
             p.R = R;
             for (int r = 0; r < R; ++r) p.dst[r] = x.peerP[r];
@@ -689,6 +701,7 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         pinit_kernel<<<q.plan.nsl, kPT, 0, stream>>>(q.V, std::max<int64_t>(q.plan.nloc, 1), q.plan.nloc, k,
                                                       q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff),
                                                       q.at<double>(q.cv.res), q.at<double>(q.cv.chk));
+        count_launch();
     }
     // 2. the right-looking solve over column blocks
     {
@@ -717,10 +730,11 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                 dsolve_kernel<KB><<<1, kDsT, dsolve_smem<KB>(), stream>>>(
                     q.L, q.ldl, n, k, row0, nrows, sl0, q.at<double>(q.cv.res), q.at<double>(q.cv.chk),
                     q.at<int64_t>(q.cv.chkoff), p, epoch);
+                count_launch();
             }
 #ifdef GCM_WITH_NCCL
             if (x.mode == Mode::Nccl) {
-                double *Pg = rk[0].at<double>(rk[0].cv.P) + row0 * k;
+                double *Pg = rk[0].Pbuf() + row0 * k;
                 st = ncclBroadcast(Pg, Pg, (size_t)nrows * k, ncclDouble, owner, (ncclComm_t)x.nccl, stream) ==
                              ncclSuccess
                          ? GCM_OK
@@ -753,7 +767,8 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                         (x.mode == Mode::Peer && rank_id != owner) ? x.peerFlag[x.self] + g : nullptr;
                     pupdate_kernel<KB><<<s_hi - s_lo, kPT, pupdate_smem<KB>(), sp>>>(
                         q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
-                        q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.at<double>(q.cv.P), flag, epoch);
+                        q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                    count_launch();
                 }
             }
             st = check_cuda(cudaEventRecord(rest_done[g & 1], aux));
@@ -767,14 +782,18 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
     {
         ProfScope ps("psweep", stream);
         for (auto &q : rk) {
-            pgram_kernel<KB><<<NB64, KB * KB <= 1024 ? KB * KB : 1024, 0, stream>>>(q.at<double>(q.cv.P), n, k,
+            pgram_kernel<KB><<<NB64, KB * KB <= 1024 ? KB * KB : 1024, 0, stream>>>(q.Pbuf(), n, k,
                                                                                   q.at<double>(q.cv.Q));
+            count_launch();
             pscan_kernel<KB><<<1, KB * KB, 0, stream>>>(q.at<double>(q.cv.Q), NB64, q.at<double>(q.cv.G));
-            if (!q.plan.dl_b.empty())
+            count_launch();
+            if (!q.plan.dl_b.empty()) {
                 pdiag_kernel<KB><<<(unsigned)q.plan.dl_b.size(), kDiagThreads, pdiag_smem<KB>(), stream>>>(
-                    q.L, q.ldl, n, q.V, std::max<int64_t>(q.plan.nloc, 1), k, sigma, q.at<double>(q.cv.P),
-                    q.at<double>(q.cv.U), q.at<double>(q.cv.G), q.at<double>(q.cv.panels),
+                    q.L, q.ldl, n, q.V, std::max<int64_t>(q.plan.nloc, 1), k, sigma, q.Pbuf(),
+                    q.Ubuf(), q.at<double>(q.cv.G), q.panbuf(),
                     q.at<unsigned long long>(q.cv.key), ebase, q.at<int>(q.cv.dlb), q.at<int64_t>(q.cv.dllc));
+                count_launch();
+            }
         }
         // 5. panels and U_b^{-1} to every rank
         if (x.mode == Mode::Virtual || x.mode == Mode::Peer) {
@@ -783,16 +802,20 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                 Peers p{};
                 p.R = R;
                 for (int r = 0; r < R; ++r) {
-                    p.dst[r] = x.mode == Mode::Virtual ? rk[r].at<double>(rk[r].cv.panels) : x.peerPan[r];
-                    p.dst2[r] = x.mode == Mode::Virtual ? rk[r].at<double>(rk[r].cv.U) : x.peerU[r];
+                    p.dst[r] = x.mode == Mode::Virtual ? rk[r].panbuf() : x.peerPan[r];
+                    p.dst2[r] = x.mode == Mode::Virtual ? rk[r].Ubuf() : x.peerU[r];
                     p.flag[r] = x.mode == Mode::Peer ? x.peerCtr[r] : nullptr;
                 }
                 const int self = x.mode == Mode::Virtual ? ri : x.self;
                 pbcast_kernel<KB><<<std::max<int>(1, std::min<int>(1024, (int)q.plan.dl_b.size())), 256, 0, stream>>>(
-                    q.at<int>(q.cv.dlb), (int)q.plan.dl_b.size(), q.at<double>(q.cv.panels), q.at<double>(q.cv.U),
+                    q.at<int>(q.cv.dlb), (int)q.plan.dl_b.size(), q.panbuf(), q.Ubuf(),
                     p, self, epoch);
+                count_launch();
             }
-            if (x.mode == Mode::Peer) pwait_kernel<<<1, 32, 0, stream>>>(x.peerCtr[x.self], epoch * (unsigned)R);
+            if (x.mode == Mode::Peer) {
+                pwait_kernel<<<1, 32, 0, stream>>>(x.peerCtr[x.self], epoch * (unsigned)R);
+                count_launch();
+            }
         }
 #ifdef GCM_WITH_NCCL
         if (x.mode == Mode::Nccl) {
@@ -800,8 +823,8 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
             for (int g = 0; g < NBc; ++g) {
                 const int owner = g % R;
                 const int b0 = (int)((int64_t)g * nb / kD), b1 = (int)std::min<int64_t>(NB64, ((int64_t)g + 1) * nb / kD);
-                double *pan = rk[0].at<double>(rk[0].cv.panels) + (int64_t)b0 * panel_doubles(KB);
-                double *U = rk[0].at<double>(rk[0].cv.U) + (int64_t)b0 * KB * KB;
+                double *pan = rk[0].panbuf() + (int64_t)b0 * panel_doubles(KB);
+                double *U = rk[0].Ubuf() + (int64_t)b0 * KB * KB;
                 ncclBroadcast(pan, pan, (size_t)(b1 - b0) * panel_doubles(KB), ncclDouble, owner,
                               (ncclComm_t)x.nccl, stream);
                 ncclBroadcast(U, U, (size_t)(b1 - b0) * KB * KB, ncclDouble, owner, (ncclComm_t)x.nccl, stream);
@@ -821,14 +844,18 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         if (st != GCM_OK) return st;
         for (auto &q : rk) {
             ApplyMap map{q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff), q.plan.nloc};
-            if (q.tma && !q.plan.full.empty())
+            if (q.tma && !q.plan.full.empty()) {
                 papply_kernel<KB><<<(unsigned)q.plan.full.size(), kT2Threads, smem_t2, stream>>>(
-                    q.tm, n, k, q.at<double>(q.cv.chk), q.at<double>(q.cv.U), q.at<double>(q.cv.panels), NB64,
+                    q.tm, n, k, q.at<double>(q.cv.chk), q.Ubuf(), q.panbuf(), NB64,
                     q.at<int2>(q.cv.full), map);
-            if (!q.plan.tiles.empty())
+                count_launch();
+            }
+            if (!q.plan.tiles.empty()) {
                 ptile_kernel<KB><<<(unsigned)q.plan.tiles.size(), kD, 0, stream>>>(
-                    q.L, q.ldl, q.plan.nloc, k, q.at<double>(q.cv.chk), q.at<double>(q.cv.U),
-                    q.at<double>(q.cv.panels), q.at<int2>(q.cv.tiles), q.at<int64_t>(q.cv.chkoff));
+                    q.L, q.ldl, q.plan.nloc, k, q.at<double>(q.cv.chk), q.Ubuf(),
+                    q.panbuf(), q.at<int2>(q.cv.tiles), q.at<int64_t>(q.cv.chkoff));
+                count_launch();
+            }
         }
         st = check_cuda(cudaGetLastError());
     }
@@ -899,8 +926,9 @@ gcm_status_t panel_modify(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, i
     }
     for (int64_t e0 = 0; e0 < k; e0 += kPassK) {
         const int kc = (int)std::min<int64_t>(kPassK, k - e0);
-        if (++ws->epoch == 0xffffffffu || ws->epoch == 0) ws->epoch = 1;
-        const unsigned epoch = ws->epoch;
+        unsigned *ep = x.epoch ? x.epoch : &ws->epoch;
+        if (++*ep == 0xffffffffu || *ep == 0) *ep = 1;
+        const unsigned epoch = *ep;
         std::vector<Rank> pass = rk;
         for (auto &q : pass) {
             q.V = q.V + e0 * std::max<int64_t>(q.plan.nloc, 1);
@@ -910,6 +938,13 @@ gcm_status_t panel_modify(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, i
                 q.plan = p;  // identical layout arrays; only k / KB change
             }
         }
+#ifdef GCM_WITH_NCCL
+        if (x.mode == Mode::Peer) {  // no rank may write into a window another rank still reads
+            unsigned long long *kb = rk[0].at<unsigned long long>(rk[0].cv.key);
+            if (ncclAllReduce(kb, kb, 1, ncclUint64, ncclMin, (ncclComm_t)x.nccl, stream) != ncclSuccess)
+                return GCM_ENCCL;
+        }
+#endif
         const int KBp = pass[0].plan.KB;
         if (KBp <= 4) st = panel_pass<4>(pass, R, n, nb, kc, sigma, e0, epoch, x, stream);
         else if (KBp <= 8) st = panel_pass<8>(pass, R, n, nb, kc, sigma, e0, epoch, x, stream);
@@ -924,6 +959,7 @@ gcm_status_t panel_modify(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, i
         keys.R = (int)rk.size();
         for (size_t i = 0; i < rk.size(); ++i) keys.k[i] = rk[i].at<unsigned long long>(rk[i].cv.key);
         keymin_kernel<<<1, 1, 0, stream>>>(ws->key, keys);
+        count_launch();
         st = check_cuda(cudaGetLastError());
         if (st != GCM_OK) return st;
         return finalize_info(ws->key, d_info, 1, stream);
@@ -946,7 +982,7 @@ gcm_status_t modify_panel(double *L, int64_t n, int64_t ldl, double *V, int64_t 
     rk[0].L = L;
     rk[0].ldl = ldl;
     rk[0].V = V;
-    Exchange x{Mode::Virtual, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
+    Exchange x{Mode::Virtual, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
     return panel_modify(rk, 1, n, 512, k, sigma, d_info, x, stream);
 }
 
@@ -1017,7 +1053,7 @@ gcm_status_t gcm_modify_dist_virtual(int nranks, double *const *L_local, int64_t
     }
     clear_stale_error();
     if (n == 0 || k == 0) return d_info ? check_cuda(cudaMemsetAsync(d_info, 0, sizeof(gcm_info_t), stream)) : GCM_OK;
-    Exchange x{Mode::Virtual, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
+    Exchange x{Mode::Virtual, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
     return panel_modify(rk, nranks, n, nb, k, sigma, d_info, x, stream);
 }
 
@@ -1054,8 +1090,76 @@ gcm_status_t gcm_comm_init(gcm_comm_t *comm, const void *host_id, int nranks, in
 
 gcm_status_t gcm_comm_destroy(gcm_comm_t comm) {
     if (!comm) return GCM_EINVAL;
+    if (comm->win) {
+        cudaDeviceSynchronize();
+        for (int r = 0; r < comm->nranks; ++r)
+            if (r != comm->rank && comm->peers[r]) cudaIpcCloseMemHandle(comm->peers[r]);
+        cudaFree(comm->win);
+    }
     gcm_status_t st = check_nccl(ncclCommDestroy(comm->nc));
     delete comm;
+    return st;
+}
+
+gcm_status_t gcm_comm_set_peer(gcm_comm_t comm, int on) {
+    if (!comm) return GCM_EINVAL;
+    comm->peer = on ? 1 : 0;
+    return GCM_OK;
+}
+
+// (Re)allocate this rank's IPC window for (n, nb) and map every rank's (collective: all ranks
+// call it with the same sizes, in the same order).
+static gcm_status_t peer_window(gcm_comm_t c, int64_t n, int64_t nb, cudaStream_t stream) {
+    const int64_t NB64 = (n + kD - 1) / kD, NBc = (n + nb - 1) / nb;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t sP = al((size_t)NBc * nb * kPassK * 8), sPan = al((size_t)NB64 * panel_doubles(32) * 8),
+                 sU = al((size_t)NB64 * 32 * 32 * 8), sF = al((size_t)(NB64 + 1) * 4), sC = 256;
+    const size_t need = sP + sPan + sU + sF + sC;
+    if (c->win && c->win_bytes >= need) return GCM_OK;
+    gcm_status_t st = check_cuda(cudaStreamSynchronize(stream));
+    if (st != GCM_OK) return st;
+    if (c->win) {
+        for (int r = 0; r < c->nranks; ++r)
+            if (r != c->rank && c->peers[r]) cudaIpcCloseMemHandle(c->peers[r]);
+        cudaFree(c->win);
+        c->win = nullptr;
+        c->win_bytes = 0;
+    }
+    void *w = nullptr;
+    st = check_cuda(cudaMalloc(&w, need));
+    if (st != GCM_OK) return st;
+    c->win = static_cast<char *>(w);
+    c->win_bytes = need;
+    c->epoch = 0;  // flags/counters of a fresh window start at zero on every rank
+    st = check_cuda(cudaMemset(w, 0, need));
+    if (st != GCM_OK) return st;
+    c->offP = 0;
+    c->offPan = sP;
+    c->offU = sP + sPan;
+    c->offFlag = sP + sPan + sU;
+    c->offCtr = sP + sPan + sU + sF;
+    c->peers[c->rank] = c->win;
+    if (c->nranks == 1) return GCM_OK;
+    cudaIpcMemHandle_t h;
+    st = check_cuda(cudaIpcGetMemHandle(&h, w));
+    if (st != GCM_OK) return st;
+    const int R = c->nranks;
+    char *dh = nullptr;
+    st = check_cuda(cudaMalloc(&dh, (size_t)(R + 1) * sizeof(h)));
+    if (st != GCM_OK) return st;
+    std::vector<cudaIpcMemHandle_t> all(R);
+    st = check_cuda(cudaMemcpy(dh, &h, sizeof(h), cudaMemcpyHostToDevice));
+    if (st == GCM_OK)
+        st = check_nccl(ncclAllGather(dh, dh + sizeof(h), sizeof(h), ncclChar, c->nc, stream));
+    if (st == GCM_OK) st = check_cuda(cudaStreamSynchronize(stream));
+    if (st == GCM_OK) st = check_cuda(cudaMemcpy(all.data(), dh + sizeof(h), R * sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(dh);
+    for (int r = 0; r < R && st == GCM_OK; ++r) {
+        if (r == c->rank) continue;
+        void *pw = nullptr;
+        st = check_cuda(cudaIpcOpenMemHandle(&pw, all[r], cudaIpcMemLazyEnablePeerAccess));
+        c->peers[r] = static_cast<char *>(pw);
+    }
     return st;
 }
 
@@ -1075,7 +1179,27 @@ gcm_status_t gcm_modify_dist(gcm_comm_t comm, double *L_local, int64_t n, int64_
     rk[0].L = L_local;
     rk[0].ldl = ldl_local;
     rk[0].V = V_local;
-    Exchange x{Mode::Nccl, comm->nc, r, nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (!comm->peer) {
+        Exchange x{Mode::Nccl, nullptr, comm->nc, r, nullptr, nullptr, nullptr, nullptr, nullptr};
+        return panel_modify(rk, R, n, nb, k, sigma, d_info, x, stream);
+    }
+    // device-initiated exchange: the owner's dsolve and every rank's pbcast store straight into
+    // the peers' windows (NVLink), with system-scope flags / counters instead of NCCL calls
+    st = peer_window(comm, n, nb, stream);
+    if (st != GCM_OK) return st;
+    double *pP[kMaxRanks], *pPan[kMaxRanks], *pU[kMaxRanks];
+    unsigned *pF[kMaxRanks], *pC[kMaxRanks];
+    for (int q = 0; q < R; ++q) {
+        pP[q] = reinterpret_cast<double *>(comm->peers[q] + comm->offP);
+        pPan[q] = reinterpret_cast<double *>(comm->peers[q] + comm->offPan);
+        pU[q] = reinterpret_cast<double *>(comm->peers[q] + comm->offU);
+        pF[q] = reinterpret_cast<unsigned *>(comm->peers[q] + comm->offFlag);
+        pC[q] = reinterpret_cast<unsigned *>(comm->peers[q] + comm->offCtr);
+    }
+    rk[0].Pw = pP[r];
+    rk[0].panw = pPan[r];
+    rk[0].Uw = pU[r];
+    Exchange x{Mode::Peer, &comm->epoch, comm->nc, r, pP, pPan, pU, pF, pC};
     return panel_modify(rk, R, n, nb, k, sigma, d_info, x, stream);
 }
 
@@ -1084,6 +1208,7 @@ gcm_status_t gcm_modify_dist(gcm_comm_t comm, double *L_local, int64_t n, int64_
 gcm_status_t gcm_comm_unique_id(void *) { return GCM_ENOTSUP; }
 gcm_status_t gcm_comm_init(gcm_comm_t *, const void *, int, int) { return GCM_ENOTSUP; }
 gcm_status_t gcm_comm_destroy(gcm_comm_t) { return GCM_ENOTSUP; }
+gcm_status_t gcm_comm_set_peer(gcm_comm_t, int) { return GCM_ENOTSUP; }
 gcm_status_t gcm_modify_dist(gcm_comm_t, double *, int64_t, int64_t, int64_t, double *, int64_t, int, gcm_info_t *,
                              gcm_stream_t) {
     return GCM_ENOTSUP;

@@ -86,6 +86,7 @@ gcm_status_t diag_launch(double *Lb, int64_t ldl, int Db, double *Vb, int64_t ld
                          double *panel, unsigned long long *key, int64_t ebase, cudaStream_t stream) {
     ProfScope ps("diag_chain", stream);
     diag_chain_kernel<KMAX><<<1, kD, 0, stream>>>(Lb, ldl, Db, Vb, ldv, k, sigma, grow0, panel, key, ebase);
+    count_launch();
     return check_cuda(cudaGetLastError());
 }
 
@@ -101,6 +102,7 @@ gcm_status_t apply_launch(double *Lr, int64_t ldl, int Db, int64_t ncols, double
     const unsigned grid = (unsigned)((ncols + kApplyThreads - 1) / kApplyThreads);
     ProfScope ps("panel_apply", stream);
     panel_apply_kernel<KMAX><<<grid, kApplyThreads, smem, stream>>>(Lr, ldl, Db, ncols, Vc, ldv, k, panel);
+    count_launch();
     return check_cuda(cudaGetLastError());
 }
 

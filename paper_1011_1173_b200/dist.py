@@ -36,7 +36,7 @@ def global_cols(n: int, nb: int, world: int, rank: int) -> np.ndarray:
 class Comm:
     """NCCL communicator of the library.  world == 1 needs no process group."""
 
-    def __init__(self, rank: int, world: int, group=None):
+    def __init__(self, rank: int, world: int, group=None, peer: bool = False):
         lib = _native.lib()
         uid = ctypes.create_string_buffer(128)
         if rank == 0:
@@ -49,6 +49,8 @@ class Comm:
         self._h = ctypes.c_void_p()
         _native.check("gcm_comm_init", lib.gcm_comm_init(ctypes.byref(self._h), uid, world, rank))
         self.rank, self.world = rank, world
+        if peer:  # device-initiated exchange through IPC windows (gcm_comm_set_peer)
+            _native.check("gcm_comm_set_peer", lib.gcm_comm_set_peer(self._h, 1))
 
     def close(self):
         if self._h:

@@ -130,3 +130,31 @@ def test_dist_rejects_bad_block_width(gd, comm1):
     V = torch.zeros(1, 10, dtype=torch.float64, device="cuda")
     with pytest.raises(Exception):
         dist.modify_dist(comm1, L, V, 10, 48, 1)
+
+
+@pytest.fixture(scope="module")
+def comm1_peer(gd):
+    _, dist = gd
+    c = dist.Comm(0, 1, peer=True)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("sigma", [1, -1])
+@pytest.mark.parametrize("n,k,nb", [(300, 16, 128), (1100, 40, 512)])
+def test_dist_single_rank_peer_mode(gd, comm1_peer, n, k, nb, sigma):
+    """gcm_comm_set_peer: the IPC-window exchange (owner stores + system-scope flags, panel
+    counters) with one rank, twice in a row (the window and its counters are reused)."""
+    gcm, dist = gd
+    for rep in range(2):
+        Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=n + k + rep, ldl=n + 5, lower_fill=np.nan)
+        Lo, Vo = Lbuf.copy(), Vbuf.copy()
+        _, _, oi = oracle.modify_a(Lo, Vo, sigma)
+        L = torch.from_numpy(Lbuf).cuda()
+        V = torch.from_numpy(Vbuf).cuda()
+        info = gcm.new_info("cuda")
+        dist.modify_dist(comm1_peer, L, V, n, nb, sigma, info=info)
+        torch.cuda.synchronize()
+        assert gcm.read_info(info)[0] == (oi.code, oi.col, oi.row)
+        assert col_scaled_max(upper(L.cpu().numpy()), upper(Lo)) <= 1e-12
+        assert row_scaled_max(V.cpu().numpy(), Vo) <= 1e-11
