@@ -96,6 +96,13 @@ gcm_status_t gcm_modify_info(double *L, int64_t n, int64_t ldl, double *V, int64
 gcm_status_t gcm_modify_ex(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
                            gcm_info_t *d_info, gcm_algo_t algo, gcm_stream_t stream);
 
+/* Single precision: as gcm_modify_info with L, V in fp32 (float, same layouts).  The paper's
+ * experiments ran both precisions (PAPER.md 111, Figs. 2-3); this is the paper's panel-order
+ * sweep (diagonal Compute chain kernel, then the panel Apply kernel, per 64-row block)
+ * instantiated for float.  Failure semantics as in fp64 (the tests are in fp32). */
+gcm_status_t gcm_modify_f32(float *L, int64_t n, int64_t ldl, float *V, int64_t k, int sigma,
+                            gcm_info_t *d_info, gcm_stream_t stream);
+
 /* End-to-end convenience: L_host (n x n, ldl) and V_host (n x k) are HOST
  * pointers (pinned memory gives full PCIe bandwidth); the call copies the upper
  * triangle's columns and V to the device, runs gcm_modify_info on an internal

@@ -67,6 +67,9 @@ def _load():
             f = getattr(lib, name)
             f.argtypes = [dp, i64, i64, dp, i64, ctypes.c_int, dp, dp, ctypes.POINTER(_Info)]
             f.restype = ctypes.c_int
+        fp = ctypes.POINTER(ctypes.c_float)
+        lib.gcmo_modify_a_f32.argtypes = [fp, i64, i64, fp, i64, ctypes.c_int, fp, fp, ctypes.POINTER(_Info)]
+        lib.gcmo_modify_a_f32.restype = ctypes.c_int
         lib.gcmo_chol_upper.argtypes = [dp, i64, i64, dp, i64]
         lib.gcmo_chol_upper.restype = i64
         lib.gcmo_compute.argtypes = [dp, dp, dp, ctypes.c_double, ctypes.c_int]
@@ -113,6 +116,28 @@ def modify_a(Lbuf: np.ndarray, Vbuf: np.ndarray, sigma: int):
     ``Vbuf[e, i]`` holds the value Compute(i, e) consumed (PAPER.md 105).
     """
     return _modify("gcmo_modify_a", Lbuf, Vbuf, sigma)
+
+
+def modify_a_f32(Lbuf: np.ndarray, Vbuf: np.ndarray, sigma: int):
+    """CholeskyModifyA in single precision (gcmo_modify_a_f32; PAPER.md 111 ran fp32 too).
+    Lbuf (n, ldl) and Vbuf (k, n) float32, C-contiguous; same conventions as modify_a."""
+    if sigma not in (1, -1):
+        raise ValueError("sigma must be +1 or -1 (PAPER.md line 20)")
+    if Lbuf.dtype != np.float32 or Vbuf.dtype != np.float32:
+        raise TypeError("modify_a_f32 works in float32")
+    if not (Lbuf.flags.c_contiguous and Vbuf.flags.c_contiguous):
+        raise ValueError("Lbuf and Vbuf must be C-contiguous")
+    n, ldl = Lbuf.shape
+    k = Vbuf.shape[0]
+    if ldl < max(1, n) or (Vbuf.shape[1] != n and Vbuf.size):
+        raise ValueError("Lbuf (n, ldl >= n), Vbuf (k, n)")
+    c = np.zeros((max(n, 1), max(k, 1)), dtype=np.float32)
+    s = np.zeros_like(c)
+    info = _Info()
+    fp = ctypes.POINTER(ctypes.c_float)
+    _load().gcmo_modify_a_f32(Lbuf.ctypes.data_as(fp), n, ldl, Vbuf.ctypes.data_as(fp), k, sigma,
+                              c.ctypes.data_as(fp), s.ctypes.data_as(fp), ctypes.byref(info))
+    return c[:n, :k], s[:n, :k], Info(info.code, info.col, info.row)
 
 
 def modify_b(Lbuf: np.ndarray, Vbuf: np.ndarray, sigma: int):

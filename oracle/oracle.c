@@ -18,7 +18,8 @@
  * strictly lower part is never read or written.  V is n x k column-major with
  * leading dimension n (update vector e is V[e*n .. e*n+n-1]).
  *
- * Everything is fp64.  Indices below are 0-based; the paper's are 1-based.
+ * Everything is fp64 except gcmo_modify_a_f32 (the paper's single-precision runs).
+ * Indices below are 0-based; the paper's are 1-based.
  *
  * Functions and the passages they follow:
  *   gcmo_compute        PAPER.md lines 44-49, function Compute
@@ -135,6 +136,44 @@ int gcmo_modify_b(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int s
             cs_s[i * k + e] = s;
             for (int64_t j = i + 1; j < n; ++j)
                 gcmo_apply(c, s, &LIJ(i, j), &VIE(j, e), sigma);
+        }
+    }
+    return info ? info->code : 0;
+}
+
+/* Single precision (the paper's Figs. 2-3 ran fp32 and fp64, PAPER.md 111): the same
+ * CholeskyModifyA (PAPER.md 24-30 with the inner loop before Compute, R1), Compute
+ * (44-49) and Apply (52-54) with every quantity a float.  Separate functions, written out,
+ * so the fp64 oracle above stays exactly as pinned. */
+static int compute_f32(float *c, float *s, float *Lii, float Vi, int sigma) {
+    float d = *Lii;
+    float x = d * d + (float)sigma * (Vi * Vi);
+    int bad = !(x > 0.0f);
+    float w = bad ? NAN : sqrtf(x);
+    *c = w / d;
+    *s = Vi / d;
+    *Lii = w;
+    return bad;
+}
+static void apply_f32(float c, float s, float *Lij, float *Vj, int sigma) {
+    float l = (*Lij + (float)sigma * s * (*Vj)) / c;
+    *Lij = l;
+    *Vj = c * (*Vj) - s * l;
+}
+int gcmo_modify_a_f32(float *L, int64_t n, int64_t ldl, float *V, int64_t k, int sigma, float *cs_c, float *cs_s,
+                      gcmo_info_t *info) {
+    if (info) { info->code = 0; info->col = 0; info->row = 0; }
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t j = 0; j < i; ++j)
+            for (int64_t e = 0; e < k; ++e)
+                apply_f32(cs_c[j * k + e], cs_s[j * k + e], &LIJ(j, i), &VIE(i, e), sigma);
+        if (!(LIJ(i, i) > 0.0f)) {
+            info_record(info, 2, 0, i);
+            LIJ(i, i) = NAN;
+        }
+        for (int64_t e = 0; e < k; ++e) {
+            if (compute_f32(&cs_c[i * k + e], &cs_s[i * k + e], &LIJ(i, i), VIE(i, e), sigma))
+                info_record(info, 1, e, i);
         }
     }
     return info ? info->code : 0;

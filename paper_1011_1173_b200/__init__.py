@@ -20,7 +20,7 @@ import ctypes
 from . import _native
 from ._native import GcmError, GcmInfo
 
-__all__ = ["modify", "modify_batched", "modify_host", "modify_host_bytes", "new_info", "read_info", "GcmError", "lib_path",
+__all__ = ["modify", "modify_f32", "modify_batched", "modify_host", "modify_host_bytes", "new_info", "read_info", "GcmError", "lib_path",
            "release_workspace", "version"]
 
 
@@ -93,6 +93,30 @@ def modify(L, V, sigma: int, info=None, algo: str = "auto", stream=None) -> None
         st = _native.lib().gcm_modify_ex(ctypes.c_void_p(L.data_ptr()), n, ldl, ctypes.c_void_p(V.data_ptr()), k,
                                          int(sigma), ip, _native.ALGO[algo], _stream_ptr(stream, L.device))
     _native.check("gcm_modify_ex", st)
+
+
+def modify_f32(L, V, sigma: int, info=None, stream=None) -> None:
+    """Single-precision in-place modification (gcm_modify_f32): L (n, ldl), V (k, n), float32 CUDA."""
+    import torch
+    if not (isinstance(L, torch.Tensor) and isinstance(V, torch.Tensor)):
+        raise TypeError("L and V must be torch tensors")
+    if L.dtype != torch.float32 or V.dtype != torch.float32:
+        raise TypeError("modify_f32 takes torch.float32 tensors")
+    if not (L.is_cuda and V.is_cuda) or L.device != V.device:
+        raise ValueError("L and V must be CUDA tensors on one device (no CPU fallback)")
+    if not (L.is_contiguous() and V.is_contiguous()) or L.dim() != 2 or V.dim() != 2:
+        raise ValueError("L (n, ldl) and V (k, n) must be contiguous")
+    n, ldl = L.shape
+    if ldl < max(1, n):
+        raise ValueError("L must be (n, ldl) with ldl >= n")
+    k = V.shape[0]
+    if V.shape[1] != n and V.numel():
+        raise ValueError("V must have shape (k, n)")
+    ip = _info_ptr(info, L.device, 1)
+    with torch.cuda.device(L.device):
+        st = _native.lib().gcm_modify_f32(ctypes.c_void_p(L.data_ptr()), n, ldl, ctypes.c_void_p(V.data_ptr()), k,
+                                          int(sigma), ip, _stream_ptr(stream, L.device))
+    _native.check("gcm_modify_f32", st)
 
 
 def modify_host(L, V, sigma: int):

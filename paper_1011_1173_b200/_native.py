@@ -23,6 +23,7 @@ SIGNATURES = {
     "gcm_modify_info": (_int, [_dp, _i64, _i64, _dp, _i64, _int, _vp, _vp]),
     "gcm_modify_ex": (_int, [_dp, _i64, _i64, _dp, _i64, _int, _vp, _int, _vp]),
     "gcm_modify_host": (_int, [_dp, _i64, _i64, _dp, _i64, _int, _vp]),
+    "gcm_modify_f32": (_int, [_vp, _i64, _i64, _vp, _i64, _int, _vp, _vp]),
     "gcm_modify_host_bytes": (_i64, [_i64, _i64]),
     "gcm_modify_batched": (_int, [_dp, _i64, _i64, _i64, _dp, _i64, _i64, _int, _i64, _vp, _vp]),
     "gcm_comm_unique_id": (_int, [_vp]),

@@ -267,6 +267,28 @@ gcm_status_t gcm_modify_ex(double *L, int64_t n, int64_t ldl, double *V, int64_t
     return modify_impl(L, n, ldl, V, k, sigma, d_info, algo, (cudaStream_t)stream);
 }
 
+// Single precision (PAPER.md 111: the paper's experiments ran fp32 and fp64): the panel-order
+// sweep (GCM_ALGO_SWEEP, the paper's own kernel structure) instantiated for float.
+gcm_status_t gcm_modify_f32(float *L, int64_t n, int64_t ldl, float *V, int64_t k, int sigma, gcm_info_t *d_info,
+                            gcm_stream_t stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (n < 0 || k < 0 || ldl < std::max<int64_t>(1, n) || (sigma != 1 && sigma != -1)) return GCM_EINVAL;
+    if (n > 0 && k > 0 && (L == nullptr || V == nullptr)) return GCM_EINVAL;
+    if (n >= (1ll << 40) || k >= (1ll << 22)) return GCM_EINVAL;
+    clear_stale_error();
+    if (n == 0 || k == 0) return d_info ? check_cuda(cudaMemsetAsync(d_info, 0, sizeof(gcm_info_t), stream)) : GCM_OK;
+    const int64_t nblk = (n + kD - 1) / kD;
+    Workspace *ws = nullptr;
+    gcm_status_t st = get_workspace(
+        stream, (size_t)nblk * panel_doubles((int)std::min<int64_t>(k, kKMax)) * sizeof(float), 1, &ws);
+    if (st != GCM_OK) return st;
+    st = check_cuda(cudaMemsetAsync(ws->key, 0xff, sizeof(unsigned long long), stream));
+    if (st == GCM_OK)
+        st = modify_sweep_f32(L, n, ldl, V, k, sigma, ws->key, reinterpret_cast<float *>(ws->panels), stream);
+    if (st != GCM_OK) return st;
+    return finalize_info(ws->key, d_info, 1, stream);
+}
+
 static constexpr int64_t kHostCB = 256;
 
 int64_t gcm_modify_host_bytes(int64_t n, int64_t k) {

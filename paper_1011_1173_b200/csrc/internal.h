@@ -73,6 +73,8 @@ gcm_status_t sweep_apply(double *Lr, int64_t ldl, int Db, int64_t ncols, double 
                          const double *panel, cudaStream_t stream);
 gcm_status_t modify_sweep(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
                           unsigned long long *key, double *panels, cudaStream_t stream);
+gcm_status_t modify_sweep_f32(float *L, int64_t n, int64_t ldl, float *V, int64_t k, int sigma,
+                              unsigned long long *key, float *panels, cudaStream_t stream);
 gcm_status_t modify_blocked(double *L, int64_t n, int64_t ldl, double *V, int64_t k, int sigma,
                             unsigned long long *key, Workspace *ws, cudaStream_t stream);
 // Bytes of scratch one single-factor call needs (either algorithm), and the

@@ -46,6 +46,32 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
     return y * fma(-h * y, y, 1.5);
 }
 
+// fp32 counterparts (the single-precision path, GCM fp32 entry points; PAPER.md 111 ran
+// both precisions): IEEE round-to-nearest reciprocal, rsqrt + one Newton step
+__device__ __forceinline__ float fast_rcp(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ float fast_rsqrt(float x) {
+    const float y = rsqrtf(x);
+    return y * fmaf(-0.5f * x * y, y, 1.5f);
+}
+template <typename T>
+struct V2;
+template <>
+struct V2<double> {
+    using type = double2;
+    static __device__ __forceinline__ double2 make(double a, double b) { return make_double2(a, b); }
+};
+template <>
+struct V2<float> {
+    using type = float2;
+    static __device__ __forceinline__ float2 make(float a, float b) { return make_float2(a, b); }
+};
+template <typename T>
+__device__ __forceinline__ T qnan();
+template <>
+__device__ __forceinline__ double qnan<double>() { return __longlong_as_double(0x7ff8000000000000ll); }
+template <>
+__device__ __forceinline__ float qnan<float>() { return __int_as_float(0x7fc00000); }
+
 __device__ __forceinline__ void record_failure(unsigned long long *key, int64_t e, int64_t row, int code) {
     atomicMin(key, info_key(e, row, code));
 }
@@ -58,47 +84,47 @@ __device__ __forceinline__ void record_failure(unsigned long long *key, int64_t 
 // (true residual, PAPER.md 105) if vexit != nullptr.  Returns w = L~_jj on all
 // lanes.  grow = global row index, ebase = index of update column 0 of this
 // pass (for failure reports).
-__device__ __forceinline__ double compute_row_warp(int lane, double d0, const double *vrow, double *IM,
-                                                   double2 *cs, double *gpanel, double *vexit, int64_t ldv,
-                                                   int k, int sigma, int64_t grow, int64_t ebase,
-                                                   unsigned long long *key) {
-    double d = d0;
-    if (!(d > 0.0)) {  // non-positive pivot on entry (R5)
+template <typename T>
+__device__ __forceinline__ T compute_row_warp(int lane, T d0, const T *vrow, T *IM, typename V2<T>::type *cs,
+                                              T *gpanel, T *vexit, int64_t ldv, int k, int sigma, int64_t grow,
+                                              int64_t ebase, unsigned long long *key) {
+    T d = d0;
+    if (!(d > T(0))) {  // non-positive pivot on entry (R5)
         if (lane == 0) record_failure(key, ebase, grow, 2);
-        d = __longlong_as_double(0x7ff8000000000000ll);
+        d = qnan<T>();
     }
-    const double invd = fast_rcp(d);
-    double base = d * d;       // x_{j,-1}
-    double rbase = invd * invd;
+    const T invd = fast_rcp(d);
+    T base = d * d;  // x_{j,-1}
+    T rbase = invd * invd;
     for (int c0 = 0; c0 < k; c0 += 32) {
         const int e = c0 + lane;
         const bool valid = e < k;
-        const double vt = valid ? vrow[e] : 0.0;
-        const double im = valid ? IM[e] : 1.0;
-        const double a = sigma > 0 ? vt * im : -(vt * im);  // sigma vt IM
+        const T vt = valid ? vrow[e] : T(0);
+        const T im = valid ? IM[e] : T(1);
+        const T a = sigma > 0 ? vt * im : -(vt * im);  // sigma vt IM
         // inclusive scan over lanes of a*vt  ->  x_{j,e} = x_{j,c0-1} + scan
-        double s = a * vt;
+        T s = a * vt;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const double y = __shfl_up_sync(kFull, s, off);
+            const T y = __shfl_up_sync(kFull, s, off);
             if (lane >= off) s += y;
         }
-        double x = base + s;
-        const bool bad = valid && !(x > 0.0);
+        T x = base + s;
+        const bool bad = valid && !(x > T(0));
         const unsigned badmask = __ballot_sync(kFull, bad);
         if (badmask) {
             const int first = __ffs(badmask) - 1;
             if (lane == first) record_failure(key, ebase + e, grow, 1);
-            if (lane >= first) x = __longlong_as_double(0x7ff8000000000000ll);
+            if (lane >= first) x = qnan<T>();
         }
-        const double rx = fast_rcp(x);
-        double rxp = __shfl_up_sync(kFull, rx, 1);
+        const T rx = fast_rcp(x);
+        T rxp = __shfl_up_sync(kFull, rx, 1);
         if (lane == 0) rxp = rbase;
         if (valid) {
-            const double gam = a * invd;
-            const double del = vt * d * rx;
+            const T gam = a * invd;
+            const T del = vt * d * rx;
             IM[e] = im * x * rxp;
-            cs[e] = make_double2(gam, del);
+            cs[e] = V2<T>::make(gam, del);
             if (gpanel) {
                 gpanel[2 * e] = gam;
                 gpanel[2 * e + 1] = del;
@@ -113,12 +139,12 @@ __device__ __forceinline__ double compute_row_warp(int lane, double d0, const do
 
 // Apply the k rotations of one row (coefficients cs[0..k-1] in shared memory)
 // to one (L element, V state) pair held by this thread; returns the final L.
-template <int KMAX>
-__device__ __forceinline__ double apply_row(double l, double (&v)[KMAX], const double2 *cs, double rho, int k) {
+template <int KMAX, typename T>
+__device__ __forceinline__ T apply_row(T l, T (&v)[KMAX], const typename V2<T>::type *cs, T rho, int k) {
 #pragma unroll
     for (int e = 0; e < KMAX; ++e) {
         if (e < k) {
-            const double2 gd = cs[e];
+            const auto gd = cs[e];
             l = fma(gd.x, v[e], l);
             v[e] = fma(-gd.y, l, v[e]);
         }
@@ -135,16 +161,15 @@ __device__ __forceinline__ double apply_row(double l, double (&v)[KMAX], const d
 // Emits the block's coefficient panel (gamma/delta, rho, nu; layout in
 // internal.h, panel may be shared or global memory), V_exit rows r0..
 // (vexit + e*ldv), and leaves L~ in Ls.  Must be called by ALL threads of the CTA.
-template <int KMAX, int LD>
-__device__ __forceinline__ void block_sweep(double (*Ls)[LD], double (&v)[KMAX], int Db, int k, int sigma,
-                                            int64_t r0, double *panel, double *vexit, int64_t ldv,
-                                            unsigned long long *key, int64_t ebase, double *vrow, double *IM,
-                                            double2 *cs, double *rho_s, int tbase = 0) {
+template <int KMAX, int LD, typename T>
+__device__ __forceinline__ void block_sweep(T (*Ls)[LD], T (&v)[KMAX], int Db, int k, int sigma, int64_t r0,
+                                            T *panel, T *vexit, int64_t ldv, unsigned long long *key, int64_t ebase,
+                                            T *vrow, T *IM, typename V2<T>::type *cs, T *rho_s, int tbase = 0) {
     const int t = threadIdx.x;
     const int m = t - tbase;  // own column within the block (valid if 0 <= m < Db)
     const int lane = t & 31;
-    for (int e = t; e < k; e += blockDim.x) IM[e] = 1.0;
-    double *rho_g = panel + 2ll * kD * k;
+    for (int e = t; e < k; e += blockDim.x) IM[e] = T(1);
+    T *rho_g = panel + 2ll * kD * k;
     for (int j = 0; j < Db; ++j) {
         if (m == j) {
 #pragma unroll
@@ -153,11 +178,11 @@ __device__ __forceinline__ void block_sweep(double (*Ls)[LD], double (&v)[KMAX],
         }
         __syncthreads();
         if (m >= 0 && m < 32) {
-            const double d0 = Ls[j][j];
-            const double w = compute_row_warp(lane, d0, vrow, IM, cs, panel + 2ll * j * k, vexit + j, ldv, k,
-                                              sigma, r0 + j, ebase, key);
+            const T d0 = Ls[j][j];
+            const T w = compute_row_warp<T>(lane, d0, vrow, IM, cs, panel + 2ll * j * k, vexit + j, ldv, k, sigma,
+                                            r0 + j, ebase, key);
             if (lane == 0) {
-                const double rho = d0 / w;
+                const T rho = d0 / w;
                 *rho_s = rho;
                 rho_g[j] = rho;
                 Ls[j][j] = w;
@@ -167,7 +192,7 @@ __device__ __forceinline__ void block_sweep(double (*Ls)[LD], double (&v)[KMAX],
         if (m > j && m < Db) Ls[m][j] = apply_row<KMAX>(Ls[m][j], v, cs, *rho_s, k);
     }
     __syncthreads();
-    double *nu_g = panel + 2ll * kD * k + kD;
+    T *nu_g = panel + 2ll * kD * k + kD;
     for (int e = t; e < k; e += blockDim.x) nu_g[e] = sqrt(IM[e]);
 }
 

@@ -308,3 +308,44 @@ def test_strictly_lower_and_padding_untouched():
     oracle.modify_a(Lbuf, Vbuf, 1)
     assert np.all(np.isnan(Lbuf[mask]))
     assert np.all(np.isfinite(Lbuf[~mask]))
+
+
+# ------------------------------------------------------------------ single precision oracle
+EPS32 = float(np.finfo(np.float32).eps)
+
+
+def test_f32_worked_example_exact():
+    """3-4-5 Compute (SPEC.md 125-128) is exact in fp32: L = [3], V = [4] -> L~ = 5, V_exit = 4."""
+    L = np.array([[3.0]], dtype=np.float32)
+    V = np.array([[4.0]], dtype=np.float32)
+    c, s, info = oracle.modify_a_f32(L, V, 1)
+    assert info.code == 0 and L[0, 0] == 5.0 and V[0, 0] == 4.0
+    assert c[0, 0] == np.float32(5.0) / np.float32(3.0) and s[0, 0] == np.float32(4.0) / np.float32(3.0)
+
+
+@pytest.mark.parametrize("n,k,sigma", [(64, 1, 1), (64, 1, -1), (200, 16, 1), (200, 16, -1)])
+def test_f32_oracle_matches_f64_oracle_and_brute_force(n, k, sigma):
+    """The fp32 oracle is the fp64 one rounded to single precision: column-scaled element error
+    <= 64 eps32 against the fp64 oracle (measured <= 9 eps32), and the paper's error metric
+    max|A~ - L~^T L~| (PAPER.md 111) <= 16 sqrt(n) eps32 max|A~| (measured <= 2 sqrt(n) eps32)."""
+    Lbuf, Vbuf, A = synth.paper_instance(n, k, sigma, seed=n + k)
+    L64, V64 = Lbuf.copy(), Vbuf.copy()
+    oracle.modify_a(L64, V64, sigma)
+    L32, V32 = Lbuf.astype(np.float32), Vbuf.astype(np.float32)
+    _, _, info = oracle.modify_a_f32(L32, V32, sigma)
+    assert info.code == 0
+    U64, U32 = upper(L64), upper(L32).astype(np.float64)
+    cn = np.linalg.norm(U64, axis=0)
+    assert np.max(np.abs(U32 - U64) / cn[None, :]) <= 64 * EPS32
+    At = A + sigma * (Vbuf.T @ Vbuf)
+    assert np.abs(At - U32.T @ U32).max() <= 16 * np.sqrt(n) * EPS32 * np.abs(At).max()
+    assert np.max(np.abs(V32 - V64)) <= 64 * EPS32 * np.abs(V64).max() * np.sqrt(n)
+
+
+def test_f32_failure_report_matches_f64():
+    n, m = 120, 77
+    Lbuf, _, _ = synth.paper_instance(n, 1, 1, seed=4)
+    V = np.stack([np.zeros(n), 1.01 * upper(Lbuf)[m, :]])
+    _, _, i64 = oracle.modify_a(Lbuf.copy(), V.copy(), -1)
+    _, _, i32 = oracle.modify_a_f32(Lbuf.astype(np.float32), V.astype(np.float32), -1)
+    assert (i32.code, i32.col, i32.row) == (i64.code, i64.col, i64.row) == (1, 1, m)
