@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "gcm.h")
 def header_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(gcm_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(gcm_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
