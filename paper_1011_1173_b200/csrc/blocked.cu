@@ -164,6 +164,7 @@ size_t chk_budget(int64_t n, int kc) {
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    chaos_delay();
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
@@ -180,9 +181,11 @@ __device__ __forceinline__ double handoff_value(double v) {
     return v == v ? v : __longlong_as_double(0x7ff8000000000000ll);  // NaNs canonicalised
 }
 __device__ __forceinline__ void st_handoff(double *p, double v) {
+    chaos_delay();
     asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(handoff_value(v)) : "memory");
 }
 __device__ __forceinline__ double ld_handoff(double *p) {
+    chaos_delay();
     unsigned long long u;
     do {
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(u) : "l"(p) : "memory");
@@ -191,13 +194,16 @@ __device__ __forceinline__ double ld_handoff(double *p) {
     return __longlong_as_double((long long)u);
 }
 __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
+    chaos_delay();
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+    chaos_delay();
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 // CTA-wide publish: every thread's prior global stores, then *f = epoch.
 __device__ __forceinline__ void cta_publish(unsigned *f, unsigned epoch) {
+    chaos_delay();
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -1290,9 +1296,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     const size_t smem_help = (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + help_max_own(KB) * kDT * KB +
                                       kHelpRing * (kDT * kLdT + kDT * (KB + 1)) + 3 * kHelpRing) *
                              sizeof(double);
-    const size_t smem_diag = (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 +
-                                      4 * kD * KB + kD) *
-                             sizeof(double);
+    const size_t smem_diag = (size_t)bdiag_smem_doubles(KB) * sizeof(double);
     size_t smem = std::max(std::max(smem_chain, smem_help), smem_diag);
     st = check_cuda(cudaFuncSetAttribute(trsv_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (st != GCM_OK) return st;

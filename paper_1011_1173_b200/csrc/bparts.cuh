@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include "diag.cuh"
 #include "internal.h"
 #include "rot.cuh"
 #include "tma.cuh"
@@ -33,6 +34,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const double *p) {
 }
 // same, for values several consumers read (no re-arm; the pass's memset arms them)
 __device__ __forceinline__ double ld_value(const double *p) {
+    chaos_delay();
     unsigned long long u;
     do {
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(u) : "l"(p) : "memory");
@@ -93,6 +95,17 @@ __device__ __forceinline__ void warp_chol_inv(double (&a)[KB], double *out) {
 constexpr int kDiagNQ = GCM_DIAG_NQ;  // threads per column in the diagonal sweep
 constexpr int kDiagThreads = 4 * kD + 32;  // up to 4 column parts + the coefficient warp
 static_assert(kDiagNQ == 1 || kDiagNQ == 2 || kDiagNQ == 4, "kDiagNQ * kD + 32 <= kDiagThreads");
+
+// the diagonal sweep's form: the closed form (diag.cuh) for rank buckets <= 16 (its KB x KB
+// per-row eliminations fit the worker's shared memory), the wave for 32
+#ifndef GCM_DIAG_CLOSED
+#define GCM_DIAG_CLOSED 1
+#endif
+__host__ __device__ constexpr bool bdiag_closed(int KB) { return GCM_DIAG_CLOSED && KB <= 16; }
+__host__ __device__ constexpr int bdiag_smem_doubles(int KB) {
+    return kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 + 4 * kD * KB + kD +
+           (bdiag_closed(KB) ? kD * (KB + 1) + diag_closed_scratch(KB) : 0);
+}
 
 // The sweep of diagonal block b by one CTA of kDiagThreads threads (a TRSV helper in
 // worker mode; P is read from the self-validating copy when p_poll).
@@ -199,24 +212,42 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
 #ifdef GCM_SWEEP_TRACE
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1006] = clock64();
 #endif
-    if (t < kDiagNQ * kD) {  // V state y = U^{-1} w
+    // closed-form block (diag.cuh, R20) for KB <= 16: q_m = U_b^{-1} p_m (the block's
+    // L^{-T} of the V states, no solve needed), every row's rotations in parallel
+    constexpr bool kClosed = bdiag_closed(KB);
+    double *qv = Vs + kD * KB;  // [kD][KB+1] (closed form only), then diag_closed's scratch
+    if (t < kDiagNQ * kD) {  // V state y = U^{-1} w (and q = U^{-1} p)
         const int cm = t % kD, cq = t / kD;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             const int e = cq * EPT + i;
-            double acc = 0.0;
+            double acc = 0.0, aq = 0.0;
 #pragma unroll
-            for (int ep = 0; ep < KB; ++ep)  // U^{-1} lower triangular; vt past column k is scratch
+            for (int ep = 0; ep < KB; ++ep) {  // U^{-1} lower triangular; vt past column k is scratch
                 if (ep <= e) acc = fma(Uis[e * KB + ep], vt[cm * KB + ep], acc);
+                if (kClosed && ep <= e && ep < k) aq = fma(Uis[e * KB + ep], Ps[cm][ep], aq);
+            }
             Vs[cm * KB + e] = (cm < Db && e < k) ? acc : 0.0;
+            if (kClosed) qv[cm * (KB + 1) + e] = (cm < Db && e < k) ? aq : 0.0;
         }
     }
-    __syncthreads();  // wave_sweep reads Vs from other threads before its own first barrier
+    __syncthreads();  // the sweep reads Vs from other threads before its own first barrier
 #ifdef GCM_SWEEP_TRACE
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1001] = clock64();
 #endif
-    wave_sweep<KB, kDiagNQ, kD + 1>(Ls, Vs, Db, k, sigma, r0, pan, V + r0, ldv, key, ebase, vx, dinv, vt, imx, 0,
-                                    kDiagNQ * kD / 32);
+    if constexpr (kClosed) {
+        diag_closed<KB>(Ls, qv, KB + 1, Db, k, sigma, r0, pan, V + r0, ldv, key, ebase, qv + kD * (KB + 1));
+        if (t < Db && t > 0) {  // the block's own triangle, column t from its block-start state
+            double y[KB];
+#pragma unroll
+            for (int e = 0; e < KB; ++e) y[e] = Vs[t * KB + e];
+            diag_triangle<KB>(Ls, t, y, pan);
+        }
+        __syncthreads();
+    } else {
+        wave_sweep<KB, kDiagNQ, kD + 1>(Ls, Vs, Db, k, sigma, r0, pan, V + r0, ldv, key, ebase, vx, dinv, vt, imx,
+                                        0, kDiagNQ * kD / 32);
+    }
 #ifdef GCM_SWEEP_TRACE
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1002] = clock64();
 #endif

@@ -199,6 +199,7 @@ struct Peers {
 };
 
 __device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
+    chaos_delay();
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
@@ -207,6 +208,7 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
     return v;
 }
 __device__ __forceinline__ void wait_flag_sys(const unsigned *f, unsigned epoch) {
+    chaos_delay();
     if (threadIdx.x == 0)
         while (ld_acquire_sys(f) != epoch) __nanosleep(200);
     __syncthreads();
@@ -621,8 +623,7 @@ size_t pupdate_smem() {
 }
 template <int KB>
 size_t pdiag_smem() {
-    return (size_t)(kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 + 4 * kD * KB + kD) *
-           sizeof(double);
+    return (size_t)bdiag_smem_doubles(KB) * sizeof(double);
 }
 
 struct Exchange {

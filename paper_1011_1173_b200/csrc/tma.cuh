@@ -8,6 +8,21 @@
 
 namespace gcm {
 
+// Chaos build (-DGCM_CHAOS, tools/chaos.sh): a pseudo-random pause of up to ~4 us before one in
+// eight publishes, polls and barrier waits, so the GPU suite runs under perturbed inter-CTA
+// timing (compute-sanitizer is closed on this pool: profiles/r02_sanitizer_closed.txt).
+#ifdef GCM_CHAOS
+__device__ __forceinline__ void chaos_delay() {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    unsigned h = ((unsigned)(c ^ (c >> 17)) * 0x9E3779B1u) ^ (threadIdx.x * 0x85ebca6bu) ^ (blockIdx.x * 0xc2b2ae35u);
+    h ^= h >> 15;
+    if ((h & 7u) == 0u) __nanosleep(h % 4096u);
+}
+#else
+__device__ __forceinline__ void chaos_delay() {}
+#endif
+
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -20,6 +35,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    chaos_delay();
     asm volatile(
         "{\n .reg .pred P;\n WAIT_%=:\n"
         " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
