@@ -1386,6 +1386,9 @@ extern "C" int gcm_debug_sweep_trace(long long *host, int count) {
 extern "C" int gcm_debug_htrace(long long *host, int count) {
     return (int)cudaMemcpyFromSymbol(host, g_htrace, sizeof(long long) * count);
 }
+extern "C" int gcm_debug_dtrace(long long *host, int count) {
+    return (int)cudaMemcpyFromSymbol(host, g_dtrace, sizeof(long long) * count);
+}
 #endif
 
 size_t blocked_workspace_bytes(int64_t n, int64_t k) {

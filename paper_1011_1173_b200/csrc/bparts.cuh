@@ -96,6 +96,20 @@ constexpr int kDiagNQ = GCM_DIAG_NQ;  // threads per column in the diagonal swee
 constexpr int kDiagThreads = 4 * kD + 32;  // up to 4 column parts + the coefficient warp
 static_assert(kDiagNQ == 1 || kDiagNQ == 2 || kDiagNQ == 4, "kDiagNQ * kD + 32 <= kDiagThreads");
 
+#ifdef GCM_TRACE  // per-block phase times of the diagonal sweep (globaltimer ns; tools/trace_chain.py)
+__device__ long long g_dtrace[256 * 8];
+#define DT_MARK(b, slot)                                                                        \
+    do {                                                                                        \
+        if (threadIdx.x == 0 && (b) < 256) {                                                    \
+            long long v_;                                                                       \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v_));                             \
+            g_dtrace[(b) * 8 + (slot)] = v_;                                                    \
+        }                                                                                       \
+    } while (0)
+#else
+#define DT_MARK(b, slot) ((void)0)
+#endif
+
 // the diagonal sweep's form: the closed form (diag.cuh) for rank buckets <= 16 (its KB x KB
 // per-row eliminations fit the worker's shared memory), the wave for 32
 #ifndef GCM_DIAG_CLOSED
@@ -103,7 +117,7 @@ static_assert(kDiagNQ == 1 || kDiagNQ == 2 || kDiagNQ == 4, "kDiagNQ * kD + 32 <
 #endif
 __host__ __device__ constexpr bool bdiag_closed(int KB) { return GCM_DIAG_CLOSED && KB <= 16; }
 __host__ __device__ constexpr int bdiag_smem_doubles(int KB) {
-    return kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 + 4 * kD * KB + kD +
+    return kD * (kD + 1) + kD * (KB + 1) + KB * (KB + 1) + 2 + wave_panel_doubles(KB) + 1 + 4 * kD * KB + 2 * kD +
            (bdiag_closed(KB) ? kD * (KB + 1) + diag_closed_scratch(KB) : 0);
 }
 
@@ -123,11 +137,12 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
     double *vx = pan + wave_panel_doubles(KB) + 1;
     double *dinv = vx + kD * KB;
     double *vt = dinv + kD;
-    double *imx = vt + kD * KB;
+    double *imx = vt + kD * (KB + 1);
     double *Vs = imx + kD * KB;
     const int t = threadIdx.x;
     const int64_t r0 = (int64_t)b * kD;
     const int Db = (int)imin64(kD, n - r0);
+    DT_MARK(b, 0);
 #ifdef GCM_SWEEP_TRACE
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1000] = clock64();
 #endif
@@ -169,6 +184,7 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
         }
     }
     __syncthreads();
+    DT_MARK(b, 1);
 #ifdef GCM_SWEEP_TRACE
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1003] = clock64();
 #endif
@@ -187,7 +203,7 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
             }
         }
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) vt[cm * KB + cq * EPT + i] = w[i];
+        for (int i = 0; i < EPT; ++i) vt[cm * (KB + 1) + cq * EPT + i] = w[i];  // odd stride: no bank conflicts
 #ifdef GCM_SWEEP_TRACE
         if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1005] = clock64();
 #endif
@@ -209,6 +225,7 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
         for (int o = lane; o < KB * KB; o += 32) Ui[(int64_t)b * KB * KB + o] = Uis[o];
     }
     __syncthreads();
+    DT_MARK(b, 2);
 #ifdef GCM_SWEEP_TRACE
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1006] = clock64();
 #endif
@@ -224,7 +241,7 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
             double acc = 0.0, aq = 0.0;
 #pragma unroll
             for (int ep = 0; ep < KB; ++ep) {  // U^{-1} lower triangular; vt past column k is scratch
-                if (ep <= e) acc = fma(Uis[e * KB + ep], vt[cm * KB + ep], acc);
+                if (ep <= e) acc = fma(Uis[e * KB + ep], vt[cm * (KB + 1) + ep], acc);
                 if (kClosed && ep <= e && ep < k) aq = fma(Uis[e * KB + ep], Ps[cm][ep], aq);
             }
             Vs[cm * KB + e] = (cm < Db && e < k) ? acc : 0.0;
@@ -235,8 +252,10 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
 #ifdef GCM_SWEEP_TRACE
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1001] = clock64();
 #endif
+    DT_MARK(b, 3);
     if constexpr (kClosed) {
         diag_closed<KB>(Ls, qv, KB + 1, Db, k, sigma, r0, pan, V + r0, ldv, key, ebase, qv + kD * (KB + 1));
+        DT_MARK(b, 4);
         if (t < Db && t > 0) {  // the block's own triangle, column t from its block-start state
             double y[KB];
 #pragma unroll
@@ -251,6 +270,7 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
 #ifdef GCM_SWEEP_TRACE
     if (blockIdx.x == 0 && t == 0) gcm_sweep_trace[1002] = clock64();
 #endif
+    DT_MARK(b, 5);
     // panel out in the blocked path's stride-KB layout (padding rotations are identities)
     double *panel = panels + (int64_t)b * panel_doubles(KB);
     for (int i = t; i < (int)panel_doubles(KB); i += kDiagThreads) panel[i] = pan[i];

@@ -43,7 +43,7 @@ __device__ long long g_dc_trace[16 * 8];
 #endif
 
 // shared-memory scratch of diag_closed (doubles)
-__host__ __device__ constexpr int diag_closed_scratch(int KB) { return 8 * KB * KB + 2 * kD * (KB + 1) + 3 * kD; }
+__host__ __device__ constexpr int diag_closed_scratch(int KB) { return 8 * KB * (KB + 1) + 2 * kD * (KB + 1) + 3 * kD; }
 
 // q = L_bb^{-T} Y for the block's Db rows (k right-hand sides padded to KB; padding
 // columns of Y are zero), IN PLACE: on entry Y[m*ldy + e], on exit q there.  Ls[m][i] =
@@ -106,8 +106,8 @@ __device__ void diag_closed(double (*Ls)[LD], const double *q, int ldq, int Db, 
                             double *scratch) {
     static_assert(KB == 4 || KB == 8 || KB == 16 || KB == 32, "rank bucket");
     constexpr int LY = KB + 1;
-    double *S8 = scratch;              // [8][KB][KB]: exclusive prefix Grams at rows 0, 8, .., 56
-    double *yv = S8 + 8 * KB * KB;     // [kD][LY]: y_{j,e}
+    double *S8 = scratch;                 // [8][KB][KB+1]: exclusive prefix Grams at rows 0, 8, .., 56
+    double *yv = S8 + 8 * KB * (KB + 1);  // [kD][LY]: y_{j,e}
     double *mu = yv + kD * LY;         // [kD][LY]: w_{j,e-1}/w_{j,e}, then mu_{j-1,e}
     double *dj = mu + kD * LY;         // [kD]: L_jj (original)
     double *rj = dj + kD;              // [kD]: 1/L_jj
@@ -118,11 +118,12 @@ __device__ void diag_closed(double (*Ls)[LD], const double *q, int ldq, int Db, 
     DC_MARK(0);
 
     // A. Grams of 8-row groups, then their exclusive prefix
+    // (row stride KB + 1: a row problem's KB lanes read one column of S8 without bank conflicts)
     for (int o = t; o < 8 * KB * KB; o += nt) {
         const int g = o / (KB * KB), i = (o / KB) % KB, c = o % KB;
         double s = 0.0;
         for (int r = 8 * g; r < 8 * g + 8 && r < Db; ++r) s = fma(q[r * ldq + i], q[r * ldq + c], s);
-        S8[o] = s;
+        S8[(g * KB + i) * (KB + 1) + c] = s;
     }
     for (int j = t; j < Db; j += nt) {
         const double d = Ls[j][j];
@@ -131,11 +132,12 @@ __device__ void diag_closed(double (*Ls)[LD], const double *q, int ldq, int Db, 
     }
     __syncthreads();
     for (int o = t; o < KB * KB; o += nt) {
+        const int oo = (o / KB) * (KB + 1) + o % KB;
         double run = 0.0;
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
-            const double b = S8[g * KB * KB + o];
-            S8[g * KB * KB + o] = run;
+            const double b = S8[g * KB * (KB + 1) + oo];
+            S8[g * KB * (KB + 1) + oo] = run;
             run += b;
         }
     }
@@ -150,16 +152,16 @@ __device__ void diag_closed(double (*Ls)[LD], const double *q, int ldq, int Db, 
     //    y = D^{-1/2} U'^{-1} z).  In both, a column is only combined with the columns before
     //    it, so a NaN column cannot reach earlier columns (R5, R6).
 #ifndef GCM_DIAG_THREAD_CHOL
-#define GCM_DIAG_THREAD_CHOL 0  // 1: per-thread KB x KB Cholesky for KB <= 8 (register-heavy; measured slower)
+#define GCM_DIAG_THREAD_CHOL 0  // per-thread KB x KB Cholesky for KB <= this (register-heavy; 0 = shuffle elimination for all)
 #endif
-    if constexpr (KB <= 8 && GCM_DIAG_THREAD_CHOL) {
+    if constexpr (KB <= GCM_DIAG_THREAD_CHOL) {
         for (int j = t; j < Db; j += nt) {
             double h[KB * (KB + 1) / 2];  // packed lower triangle, row-major: (i, c) at i(i+1)/2 + c
             const int g8 = j >> 3;
 #pragma unroll
             for (int i = 0; i < KB; ++i)
 #pragma unroll
-                for (int c = 0; c <= i; ++c) h[i * (i + 1) / 2 + c] = S8[(g8 * KB + i) * KB + c];
+                for (int c = 0; c <= i; ++c) h[i * (i + 1) / 2 + c] = S8[(g8 * KB + i) * (KB + 1) + c];
             for (int r = 8 * g8; r < j; ++r) {
                 double qr[KB];
 #pragma unroll
@@ -199,44 +201,72 @@ __device__ void diag_closed(double (*Ls)[LD], const double *q, int ldq, int Db, 
             for (int i = 0; i < KB; ++i) yv[j * LY + i] = z[i];
         }
     } else {
-        constexpr int G = 32 / (KB < 32 ? KB : 32);  // rows per warp
+        // RPL rows of H_j per lane (LPP = KB / RPL lanes per row problem, rows li + LPP u):
+        // each pivot-row shuffle feeds RPL rows, so the shuffles -- the throughput limit of
+        // this step when every warp eliminates -- drop by RPL
+        constexpr int RPL = KB >= 16 ? (KB >= 32 ? 2 : 4) : (KB >= 8 ? 2 : 1);
+        constexpr int LPP = KB / RPL;
+        constexpr int PPW = 32 / LPP;  // row problems per warp
         const int warp = t >> 5, lane = t & 31, nw = nt >> 5;
-        const int i = lane % KB, grp = lane / KB;
-        for (int base = warp * G; base < Db; base += nw * G) {
+        const int li = lane % LPP, grp = lane / LPP;
+        for (int base = warp * PPW; base < Db; base += nw * PPW) {
             const int j = base + grp;
             const bool act = j < Db;
             const int jj = act ? j : 0;
-            double a[KB];
+            double a[RPL][KB], z[RPL];
             const int g8 = jj >> 3;
 #pragma unroll
-            for (int c = 0; c < KB; ++c) a[c] = S8[(g8 * KB + i) * KB + c];
-            for (int r = 8 * g8; r < jj; ++r) {
-                const double qi = q[r * ldq + i];
+            for (int u = 0; u < RPL; ++u)
 #pragma unroll
-                for (int c = 0; c < KB; ++c) a[c] = fma(qi, q[r * ldq + c], a[c]);
+                for (int c = 0; c < KB; ++c) a[u][c] = S8[(g8 * KB + li + LPP * u) * (KB + 1) + c];
+            for (int r = 8 * g8; r < jj; ++r) {
+                double qr[KB];
+#pragma unroll
+                for (int c = 0; c < KB; ++c) qr[c] = q[r * ldq + c];
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) {
+                    const double qi = q[r * ldq + li + LPP * u];
+#pragma unroll
+                    for (int c = 0; c < KB; ++c) a[u][c] = fma(qi, qr[c], a[u][c]);
+                }
             }
 #pragma unroll
-            for (int c = 0; c < KB; ++c) a[c] = (i == c ? 1.0 : 0.0) + sg * a[c];
-            double z = dj[jj] * q[jj * ldq + i];
+            for (int u = 0; u < RPL; ++u) {
+                const int i = li + LPP * u;
+#pragma unroll
+                for (int c = 0; c < KB; ++c) a[u][c] = (i == c ? 1.0 : 0.0) + sg * a[u][c];
+                z[u] = dj[jj] * q[jj * ldq + i];
+            }
 #pragma unroll
             for (int c = 0; c < KB - 1; ++c) {
-                const bool below = i > c;
-                const double f = a[c] * fast_rcp(__shfl_sync(kFull, a[c], c, KB));
+                const int pl = c % LPP, pu = c / LPP;  // the pivot row's lane and slot
+                double f[RPL];
+                const double rp = fast_rcp(__shfl_sync(kFull, a[pu][c], pl, LPP));
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) f[u] = a[u][c] * rp;
 #pragma unroll
                 for (int c2 = c + 1; c2 < KB; ++c2) {
-                    const double x = __shfl_sync(kFull, a[c2], c, KB);
-                    if (below) a[c2] = fma(-f, x, a[c2]);
-                }
-                const double zc = __shfl_sync(kFull, z, c, KB);
-                if (below) z = fma(-f, zc, z);
-            }
-            double di = 0.0;
+                    const double x = __shfl_sync(kFull, a[pu][c2], pl, LPP);
 #pragma unroll
-            for (int c = 0; c < KB; ++c)
-                if (c == i) di = a[c];
-            // a non-positive pivot (an indefinite leading block: an earlier row failed) gives NaN
-            const double y = di > 0.0 ? z * fast_rsqrt(di) : __longlong_as_double(0x7ff8000000000000ll);
-            if (act) yv[jj * LY + i] = y;
+                    for (int u = 0; u < RPL; ++u)
+                        if (li + LPP * u > c) a[u][c2] = fma(-f[u], x, a[u][c2]);
+                }
+                const double zc = __shfl_sync(kFull, z[pu], pl, LPP);
+#pragma unroll
+                for (int u = 0; u < RPL; ++u)
+                    if (li + LPP * u > c) z[u] = fma(-f[u], zc, z[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < RPL; ++u) {
+                const int i = li + LPP * u;
+                double di = 0.0;
+#pragma unroll
+                for (int c = 0; c < KB; ++c)
+                    if (c == i) di = a[u][c];
+                // a non-positive pivot (an indefinite leading block: an earlier row failed) gives NaN
+                const double y = di > 0.0 ? z[u] * fast_rsqrt(di) : __longlong_as_double(0x7ff8000000000000ll);
+                if (act) yv[jj * LY + i] = y;
+            }
         }
     }
     __syncthreads();

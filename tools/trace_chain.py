@@ -69,3 +69,11 @@ if ok.any():
         print(f"  b={b:3d}  {(r[0]-t0)/1e3:8.1f} {(r[4]-t0)/1e3:8.1f} {(r[1]-t0)/1e3:8.1f} {(r[2]-t0)/1e3:8.1f}  cta {int(r[3])}")
     dur = w[ok, 2] - w[ok, 1]
     print(f"  sweep duration median {np.median(dur)/1e3:.1f} us, max {dur.max()/1e3:.1f}")
+
+db = (ctypes.c_longlong * (256 * 8))()
+if hasattr(lib, "gcm_debug_dtrace") and lib.gcm_debug_dtrace(db, 256 * 8) == 0:
+    dt = np.frombuffer(db, dtype=np.int64).reshape(256, 8).astype(np.float64)[:NB]
+    ok = dt[:, 5] > 0
+    print("diagonal sweep phases (us, median over blocks): loads+P polled / w+U^-1 / V,q / closed rows / triangle")
+    ph = [np.median(dt[ok, i + 1] - dt[ok, i]) / 1e3 for i in range(5)]
+    print("  " + "  ".join(f"{x:.1f}" for x in ph))
