@@ -51,8 +51,11 @@ __host__ __device__ constexpr int diag_closed_scratch(int KB) { return 8 * KB * 
 // so each step resolves a row PAIR inside one lane (q_{2l} = a_{2l}/L, q_{2l+1} from it
 // with one more FMA) and broadcasts both by shuffle: 32 dependent steps of ~FMA + FMA +
 // SHFL + 2 FMA instead of 64 of MUL + SHFL + FMA.  Called by ALL threads; synchronises.
-template <int KB, int LD>
+template <int KB, int LD, int RPW = 1>
 __device__ __forceinline__ void block_trsv(const double (*Ls)[LD], double *Y, int ldy, int Db, double *) {
+    // RPW right-hand sides per warp: the L entries a lane loads feed all of them (a CTA with
+    // many warps per block, e.g. dsolve's 32, would otherwise re-load every entry per warp and
+    // saturate the shared-memory pipe)
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int nw = blockDim.x >> 5;
     const int m0 = 2 * lane, m1 = 2 * lane + 1;
@@ -65,25 +68,34 @@ __device__ __forceinline__ void block_trsv(const double (*Ls)[LD], double *Y, in
     // the lane's L entries of the next pair are loaded a step ahead (off the shuffle chain);
     // entries past the block (Db < 64) or in the strictly lower part are read but masked out
     const int mr0 = v0 ? m0 : 0, mr1 = v1 ? m1 : 0;
-    for (int e = warp; e < KB; e += nw) {
-        double a0 = v0 ? Y[m0 * ldy + e] : 0.0;
-        double a1 = v1 ? Y[m1 * ldy + e] : 0.0;
+    for (int eb = warp * RPW; eb < KB; eb += nw * RPW) {
+        double a0[RPW], a1[RPW];
+#pragma unroll
+        for (int w = 0; w < RPW; ++w) {
+            const int e = eb + w;
+            a0[w] = (v0 && e < KB) ? Y[m0 * ldy + e] : 0.0;
+            a1[w] = (v1 && e < KB) ? Y[m1 * ldy + e] : 0.0;
+        }
         double l00 = Ls[mr0][0], l01 = Ls[mr0][1], l10 = Ls[mr1][0], l11 = Ls[mr1][1];
         for (int p = 0; p < np; ++p) {
             const int in = 2 * p + 2 < kD ? 2 * p + 2 : 0;
             const double n00 = Ls[mr0][in], n01 = Ls[mr0][in + 1], n10 = Ls[mr1][in], n11 = Ls[mr1][in + 1];
-            const double q0l = a0 * i0;
-            const double q1l = fma(-c1, q0l, a1 * i1);
-            const double q0 = __shfl_sync(kFull, q0l, p);
-            double q1 = __shfl_sync(kFull, q1l, p);
-            if (2 * p + 1 >= Db) q1 = 0.0;  // odd Db: the last pair has one row
-            if (lane == p) {
-                Y[m0 * ldy + e] = q0;
-                if (v1) Y[m1 * ldy + e] = q1;
-            }
-            if (lane > p) {  // rows of later lanes: a_m -= L(2p, m) q_{2p} + L(2p+1, m) q_{2p+1}
-                a0 = fma(-l01, q1, fma(-l00, q0, a0));
-                a1 = fma(-l11, q1, fma(-l10, q0, a1));
+            const bool two = 2 * p + 1 < Db;  // odd Db: the last pair has one row
+#pragma unroll
+            for (int w = 0; w < RPW; ++w) {
+                const double q0l = a0[w] * i0;
+                const double q1l = fma(-c1, q0l, a1[w] * i1);
+                const double q0 = __shfl_sync(kFull, q0l, p);
+                double q1 = __shfl_sync(kFull, q1l, p);
+                if (!two) q1 = 0.0;
+                if (lane == p && eb + w < KB) {
+                    Y[m0 * ldy + eb + w] = q0;
+                    if (v1) Y[m1 * ldy + eb + w] = q1;
+                }
+                if (lane > p) {  // rows of later lanes: a_m -= L(2p, m) q_{2p} + L(2p+1, m) q_{2p+1}
+                    a0[w] = fma(-l01, q1, fma(-l00, q0, a0[w]));
+                    a1[w] = fma(-l11, q1, fma(-l10, q0, a1[w]));
+                }
             }
             l00 = n00;
             l01 = n01;

@@ -63,7 +63,7 @@ namespace {
 
 constexpr int kMaxRanks = 8;  // virtual ranks / peers a kernel writes to
 constexpr int kPT = 256;      // pupdate threads
-constexpr int kDsT = 1024;    // dsolve threads (warp e solves update column e)
+constexpr int kDsT = 512;     // dsolve threads (block_trsv: 4 update columns per warp at KB >= 16)
 constexpr int kPassK = 32;    // update columns per pass (k > 32: sequential passes, R3)
 
 // -------------------------------------------------------------------------- layout (host)
@@ -237,6 +237,15 @@ __global__ void pinit_kernel(const double *__restrict__ V, int64_t ldv, int64_t 
 // residuals stay in shared memory for the whole kernel (they are dead after it: the block's
 // strips have no tiles below it), and every L tile is prefetched one step ahead (cp.async
 // double buffer), so the only exposed latency is the first load.
+// register-block shape of the residual update (pupdate_kernel, dsolve_kernel): kPT threads,
+// CPT adjacent strip columns x EPT update columns each
+template <int KB>
+struct PuShape {
+    static constexpr int CPT = KB >= 8 ? 2 : 1;
+    static constexpr int EPT = KB / (4 * CPT);
+    static constexpr int NCG = kD / CPT;  // column groups
+    static constexpr int LDT = kD + 2;    // row stride of the L tile (16-byte aligned)
+};
 constexpr int kDsMaxRows = 512;  // solve-block height the kernel's shared memory is sized for (KB <= 16)
 __device__ __forceinline__ void cp8(double *dst, const double *src, bool ok) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(ok ? src : nullptr),
@@ -248,13 +257,14 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
                                                        int64_t row0, int nrows, int sl0, double *res, double *chk,
                                                        const int64_t *chkoff, Peers peers, unsigned epoch) {
     extern __shared__ double sm_ds[];
+    constexpr int LDT = kD + 2;                  // row stride of an update tile (16-byte rows)
     double(*Ls)[kD + 1] = reinterpret_cast<double(*)[kD + 1]>(sm_ds);
-    double *Lt = sm_ds + kD * (kD + 1);          // [2][kD][kD+1] off-diagonal tiles
-    double *qv = Lt + 2 * kD * (kD + 1);         // [kD][KB+1]
-    double *rinv = qv + kD * (KB + 1);           // [kD]
+    double *Lt = sm_ds + kD * (kD + 1);          // [2][kD rows m][LDT]: Lt[m][c] = L(r0 + m, strip column c)
+    double *qv = Lt + 2 * kD * LDT;              // [kD][KB+2] (even stride: 16-byte pairs)
+    double *rinv = qv + kD * (KB + 2);           // [kD]
     double *R = rinv + kD;                       // [kDsMaxRows][KB]: the block's residuals
     const int t = threadIdx.x;
-    constexpr int LQ = KB + 1;
+    constexpr int LQ = KB + 2;
     const int na = (nrows + kD - 1) / kD;
     // the whole block's residuals (one round trip) and the first diagonal tile
     for (int o = t; o < na * kD * KB; o += kDsT) {
@@ -277,10 +287,10 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
         const int Da = (int)imin64(kD, n - r0);
         const int64_t lc2 = (int64_t)(sl0 + a2) * kD;
         const int D2 = (int)imin64(kD, n - (row0 + (int64_t)a2 * kD));
-        double *lt = Lt + buf * kD * (kD + 1);
+        double *lt = Lt + buf * kD * LDT;
         for (int idx = t; idx < kD * kD; idx += kDsT) {
-            const int c = idx / kD, m = idx % kD;
-            cp8(lt + c * (kD + 1) + m, L + (r0 + m) + (lc2 + c) * ldl, c < D2 && m < Da);
+            const int c = idx / kD, m = idx % kD;  // consecutive threads: consecutive rows (coalesced)
+            cp8(lt + m * LDT + c, L + (r0 + m) + (lc2 + c) * ldl, c < D2 && m < Da);
         }
     };
     load_diag(0);
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
             qv[m * LQ + e] = m < Da ? R[(a * kD + m) * KB + e] : 0.0;
         }
         __syncthreads();
-        block_trsv<KB>(Ls, qv, LQ, Da, rinv);
+        block_trsv<KB, kD + 1, (KB >= 16 ? 4 : 1)>(Ls, qv, LQ, Da, rinv);
         for (int o = t; o < Da * k; o += kDsT) {
             const int m = o / k, e = o % k;
             const double v = qv[m * LQ + e];
@@ -315,22 +325,53 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
             else asm volatile("cp.async.wait_group 1;" ::: "memory");
             __syncthreads();
             const int D2 = (int)imin64(kD, n - (row0 + (int64_t)a2 * kD));
-            const double *lt = Lt + buf * kD * (kD + 1);
+            const double *lt = Lt + buf * kD * LDT;
             double *ck = chk + (chkoff[sl0 + a2] + r0 / kD) * kD * k;  // tile (r0/64, strip a2)
-            for (int o = t; o < D2 * KB; o += kDsT) {
-                const int c = o / KB, e = o % KB;
-                double *rp = R + (a2 * kD + c) * KB + e;
-                const double old = *rp;
-                if (e < k) ck[c * k + e] = old;
-                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-                const double *l = lt + c * (kD + 1);
-                for (int m = 0; m < Da; m += 4) {
-                    s0 = fma(l[m], qv[m * LQ + e], s0);
-                    s1 = fma(l[m + 1], qv[(m + 1) * LQ + e], s1);
-                    s2 = fma(l[m + 2], qv[(m + 2) * LQ + e], s2);
-                    s3 = fma(l[m + 3], qv[(m + 3) * LQ + e], s3);
+            // pupdate's register block (2 columns x EPT update columns per thread, one 16-byte
+            // load per L pair, P pairs broadcast) on the first 256 threads: the update was
+            // shared-memory bound at one output per thread
+            using S = PuShape<KB>;
+            if (t < kPT) {
+                const int cg = t % S::NCG, eg = t / S::NCG;
+                const int c0 = cg * S::CPT, e0 = eg * S::EPT;
+                double acc[S::CPT][S::EPT];
+#pragma unroll
+                for (int u = 0; u < S::CPT; ++u)
+#pragma unroll
+                    for (int i = 0; i < S::EPT; ++i) {
+                        acc[u][i] = R[(a2 * kD + c0 + u) * KB + e0 + i];
+                        if (c0 + u < D2 && e0 + i < k) ck[(c0 + u) * k + e0 + i] = acc[u][i];
+                    }
+#pragma unroll 4
+                for (int m = 0; m < Da; ++m) {
+                    double l[S::CPT], pv[S::EPT];
+                    if constexpr (S::CPT == 2) {
+                        const double2 l2 = *reinterpret_cast<const double2 *>(lt + m * LDT + c0);
+                        l[0] = l2.x;
+                        l[1] = l2.y;
+                    } else {
+                        l[0] = lt[m * LDT + c0];
+                    }
+                    if constexpr (S::EPT % 2 == 0) {
+#pragma unroll
+                        for (int i = 0; i < S::EPT; i += 2) {
+                            const double2 p2 = *reinterpret_cast<const double2 *>(qv + m * LQ + e0 + i);
+                            pv[i] = p2.x;
+                            pv[i + 1] = p2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < S::EPT; ++i) pv[i] = qv[m * LQ + e0 + i];
+                    }
+#pragma unroll
+                    for (int u = 0; u < S::CPT; ++u)
+#pragma unroll
+                        for (int i = 0; i < S::EPT; ++i) acc[u][i] = fma(-l[u], pv[i], acc[u][i]);
                 }
-                *rp = old - ((s0 + s1) + (s2 + s3));
+#pragma unroll
+                for (int u = 0; u < S::CPT; ++u)
+#pragma unroll
+                    for (int i = 0; i < S::EPT; ++i) R[(a2 * kD + c0 + u) * KB + e0 + i] = acc[u][i];
             }
             __syncthreads();  // Lt[buf] is refilled two steps on
         }
@@ -351,13 +392,8 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
 // block: per row one 16-byte load of the L pair and EPT/2 16-byte loads of P feed CPT*EPT
 // FMAs); the L tile (row-major in shared memory) and the P rows of the next 64-row
 // sub-block stream in (cp.async, double buffered) under the current one.
-template <int KB>
-struct PuShape {
-    static constexpr int CPT = KB >= 8 ? 2 : 1;
-    static constexpr int EPT = KB / (4 * CPT);
-    static constexpr int NCG = kD / CPT;  // column groups
-    static constexpr int LDT = kD + 2;    // row stride of the L tile (16-byte aligned)
-};
+// KB here is the update columns ONE CTA handles: the lookahead launch splits a strip's
+// columns over gridDim.y CTAs (update columns blockIdx.y * KB ..) to cut its latency.
 template <int KB>
 __global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restrict__ L, int64_t ldl, int64_t n,
                                                         int64_t nloc, int k, int64_t row0, int nrows, int sl_first,
@@ -365,6 +401,7 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restric
                                                         const double *__restrict__ P, const unsigned *flag,
                                                         unsigned epoch) {
     using S = PuShape<KB>;
+    const int eb = blockIdx.y * KB;  // first update column of this CTA
     constexpr int CPT = S::CPT, EPT = S::EPT, LDT = S::LDT;
     extern __shared__ __align__(16) double sm_pu[];
     double *Lt = sm_pu;                // [2][kD rows m][LDT]: Lt[m][c] = L(r0 + m, strip column c)
@@ -376,12 +413,12 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restric
     const int nc = (int)imin64(kD, nloc - lc);
     const int na = (nrows + kD - 1) / kD;
     if (flag) wait_flag_sys(flag, epoch);
-    double *rs = res + (int64_t)sl * kD * k;
+    double *rs = res + (int64_t)sl * kD * k + eb;
     double acc[CPT][EPT];
 #pragma unroll
     for (int u = 0; u < CPT; ++u)
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) acc[u][i] = (c0 + u < nc && e0 + i < k) ? rs[(c0 + u) * k + e0 + i] : 0.0;
+        for (int i = 0; i < EPT; ++i) acc[u][i] = (c0 + u < nc && eb + e0 + i < k) ? rs[(c0 + u) * k + e0 + i] : 0.0;
     auto issue = [&](int a) {
         const int64_t r0 = row0 + (int64_t)a * kD;
         const int Da = (int)imin64(kD, n - r0);
@@ -396,9 +433,9 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restric
         }
         for (int idx = t; idx < kD * KB; idx += kPT) {
             const int m = idx / KB, e = idx % KB;
-            const bool ok = m < Da && e < k;
+            const bool ok = m < Da && eb + e < k;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(ps + idx)),
-                         "l"(ok ? P + (r0 + m) * k + e : P), "r"(ok ? 8 : 0)
+                         "l"(ok ? P + (r0 + m) * k + eb + e : P), "r"(ok ? 8 : 0)
                          : "memory");
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -414,12 +451,12 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restric
         }
         __syncthreads();
         {
-            double *ck = chk + (chkoff[sl] + r0 / kD) * kD * k;
+            double *ck = chk + (chkoff[sl] + r0 / kD) * kD * k + eb;
 #pragma unroll
             for (int u = 0; u < CPT; ++u)
 #pragma unroll
                 for (int i = 0; i < EPT; ++i)
-                    if (c0 + u < nc && e0 + i < k) ck[(c0 + u) * k + e0 + i] = acc[u][i];
+                    if (c0 + u < nc && eb + e0 + i < k) ck[(c0 + u) * k + e0 + i] = acc[u][i];
         }
         const double *lt = Lt + (a & 1) * kD * LDT + c0;
         const double *ps = Ps + (a & 1) * kD * KB + e0;
@@ -455,7 +492,7 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restric
     for (int u = 0; u < CPT; ++u)
 #pragma unroll
         for (int i = 0; i < EPT; ++i)
-            if (c0 + u < nc && e0 + i < k) rs[(c0 + u) * k + e0 + i] = acc[u][i];
+            if (c0 + u < nc && eb + e0 + i < k) rs[(c0 + u) * k + e0 + i] = acc[u][i];
 }
 
 // Q_b = P_b^T P_b per 64-row block (KB x KB, zero padded)
@@ -615,7 +652,7 @@ struct Rank {
 
 template <int KB>
 size_t dsolve_smem() {
-    return (size_t)(3 * kD * (kD + 1) + kD * (KB + 1) + kD + (KB <= 16 ? 512 : 256) * KB) * 8;
+    return (size_t)(kD * (kD + 1) + 2 * kD * (kD + 2) + kD * (KB + 2) + kD + (KB <= 16 ? kDsMaxRows : kDsMaxRows / 2) * KB) * 8;
 }
 template <int KB>
 size_t pupdate_smem() {
@@ -693,6 +730,9 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         st = check_cuda(cudaFuncSetAttribute(pupdate_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pupdate_smem<KB>()));
     if (st == GCM_OK)
+        st = check_cuda(cudaFuncSetAttribute(pupdate_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)pupdate_smem<8>()));
+    if (st == GCM_OK)
         st = check_cuda(cudaFuncSetAttribute(pdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pdiag_smem<KB>()));
     if (st != GCM_OK) return st;
@@ -766,9 +806,15 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                     const int rank_id = x.mode == Mode::Virtual ? ri : x.self;
                     const unsigned *flag =
                         (x.mode == Mode::Peer && rank_id != owner) ? x.peerFlag[x.self] + g : nullptr;
-                    pupdate_kernel<KB><<<s_hi - s_lo, kPT, pupdate_smem<KB>(), sp>>>(
-                        q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
-                        q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                    if (pass == 0 && KB > 8) {  // lookahead: the chain waits on it -- 8 update columns per CTA
+                        pupdate_kernel<8><<<dim3(s_hi - s_lo, KB / 8), kPT, pupdate_smem<8>(), sp>>>(
+                            q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                            q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                    } else {
+                        pupdate_kernel<KB><<<s_hi - s_lo, kPT, pupdate_smem<KB>(), sp>>>(
+                            q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                            q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                    }
                     count_launch();
                 }
             }
