@@ -27,6 +27,7 @@
 // (~(2*64*k + 64 + k) doubles per 64-row block), both written by the producing kernel
 // itself.  Layout: 1-D block-cyclic over columns (gcm.h), V rows follow their columns.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -63,7 +64,7 @@ namespace {
 
 constexpr int kMaxRanks = 8;  // virtual ranks / peers a kernel writes to
 constexpr int kPT = 256;      // pupdate threads
-constexpr int kDsT = 512;     // dsolve threads (block_trsv: 4 update columns per warp at KB >= 16)
+constexpr int kDsT = 512;     // dsolve threads (16 warps: 8 row tiles x 2 column groups)
 constexpr int kPassK = 32;    // update columns per pass (k > 32: sequential passes, R3)
 
 // -------------------------------------------------------------------------- layout (host)
@@ -159,7 +160,7 @@ Plan make_plan(int64_t n, int64_t nb, int R, int r, int k, bool tma_groups) {
 
 // workspace carve-up of one rank (byte offsets)
 struct Carve {
-    size_t P, res, chk, Q, G, U, panels, key, flags, ctr, gstrip, chkoff, dlb, dllc, full, tiles, total;
+    size_t P, res, chk, Winv, Q, G, U, panels, key, flags, ctr, gstrip, chkoff, dlb, dllc, full, tiles, total;
 };
 Carve carve(const Plan &p) {
     Carve c{};
@@ -173,6 +174,7 @@ Carve carve(const Plan &p) {
     c.P = take((size_t)p.NBc * p.nb * p.k * 8);
     c.res = take((size_t)std::max(p.nsl, 1) * kD * p.k * 8);
     c.chk = take((size_t)std::max<int64_t>(p.nchk, 1) * kD * p.k * 8);
+    c.Winv = take((size_t)std::max(p.nsl, 1) * kD * kD * 8);
     c.Q = take((size_t)p.NB64 * KB * KB * 8);
     c.G = take((size_t)p.NB64 * KB * KB * 8);
     c.U = take((size_t)p.NB64 * KB * KB * 8);
@@ -230,21 +232,22 @@ __global__ void pinit_kernel(const double *__restrict__ V, int64_t ldv, int64_t 
     }
 }
 
-// The owner's diagonal solve of column block g: P rows [row0, row0 + nrows) = L_gg^{-T} r_g,
-// 64-row sub-block a after sub-block a: the pair-row substitution of diag.cuh (one warp per
-// update column), the rows written to every rank's P, then the residuals (and Apply
-// checkpoints) of the block's later strips updated with them.  One CTA; the block's
-// residuals stay in shared memory for the whole kernel (they are dead after it: the block's
-// strips have no tiles below it), and every L tile is prefetched one step ahead (cp.async
-// double buffer), so the only exposed latency is the first load.
 // register-block shape of the residual update (pupdate_kernel, dsolve_kernel): kPT threads,
 // CPT adjacent strip columns x EPT update columns each
 template <int KB>
 struct PuShape {
+    // a warp covers LC lanes x CPT strip columns by LE lanes x EPT update columns, so one
+    // 16-byte L load serves LE lanes (broadcast) and one P load LC lanes: per row 3 shared
+    // wavefronts feed 8 FMAs at KB = 32 (a warp spanning all 64 columns needed 6)
     static constexpr int CPT = KB >= 8 ? 2 : 1;
-    static constexpr int EPT = KB / (4 * CPT);
-    static constexpr int NCG = kD / CPT;  // column groups
-    static constexpr int LDT = kD + 2;    // row stride of the L tile (16-byte aligned)
+    static constexpr int LE = KB >= 8 ? 4 : 2;     // lanes along update columns
+    static constexpr int LC = 32 / LE;             // lanes along strip columns
+    static constexpr int EPT = KB / (2 * LE);      // two warps along update columns
+    static constexpr int WC = kD / (LC * CPT);     // warps along strip columns
+    static constexpr int LDT = kD + 2;             // row stride of the L tile (16-byte aligned)
+    static_assert(WC * 2 * 32 == kPT && EPT >= 1, "kPT threads cover 64 columns x KB");
+    __device__ static int c0(int t) { return ((t >> 5) % WC * LC + (t & 31) % LC) * CPT; }
+    __device__ static int e0(int t) { return ((t >> 5) / WC * LE + (t & 31) / LC) * EPT; }
 };
 constexpr int kDsMaxRows = 512;  // solve-block height the kernel's shared memory is sized for (KB <= 16)
 __device__ __forceinline__ void cp8(double *dst, const double *src, bool ok) {
@@ -252,138 +255,49 @@ __device__ __forceinline__ void cp8(double *dst, const double *src, bool ok) {
                  "r"(ok ? 8 : 0)
                  : "memory");
 }
-template <int KB>
-__global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restrict__ L, int64_t ldl, int64_t n, int k,
-                                                       int64_t row0, int nrows, int sl0, double *res, double *chk,
-                                                       const int64_t *chkoff, Peers peers, unsigned epoch) {
-    extern __shared__ double sm_ds[];
-    constexpr int LDT = kD + 2;                  // row stride of an update tile (16-byte rows)
-    double(*Ls)[kD + 1] = reinterpret_cast<double(*)[kD + 1]>(sm_ds);
-    double *Lt = sm_ds + kD * (kD + 1);          // [2][kD rows m][LDT]: Lt[m][c] = L(r0 + m, strip column c)
-    double *qv = Lt + 2 * kD * LDT;              // [kD][KB+2] (even stride: 16-byte pairs)
-    double *rinv = qv + kD * (KB + 2);           // [kD]
-    double *R = rinv + kD;                       // [kDsMaxRows][KB]: the block's residuals
-    const int t = threadIdx.x;
-    constexpr int LQ = KB + 2;
-    const int na = (nrows + kD - 1) / kD;
-    // the whole block's residuals (one round trip) and the first diagonal tile
-    for (int o = t; o < na * kD * KB; o += kDsT) {
-        const int row = o / KB, e = o % KB;
-        const int a = row / kD, m = row % kD;
-        cp8(R + o, res + (int64_t)(sl0 + a) * kD * k + m * k + e, e < k && row < nrows);
+__device__ __forceinline__ void cp16(double *dst, const double *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Inverse of every local strip's 64x64 diagonal block (upper triangular U, U(i, j) =
+// L(r0 + i, lc + j), i <= j; PAPER.md's factor is the upper-triangular L of A = L^T L),
+// stored by rows: W[j * 64 + m] = (U^{-1})(j, m), zero for j > m and for m >= D.  It turns
+// dsolve's serial 64-step substitution q = U^{-T} r into the data-parallel product
+// q_m = sum_{j <= m} W(j, m) r_j (the inverted-diagonal-block TRSV of GPU BLAS libraries;
+// DESIGN.md R22), and it runs once per pass over all strips at once, off the solve chain.
+// Thread m computes column m by back substitution (U w = e_m), its 64 running sums in
+// registers at compile-time indices, every U entry a shared-memory broadcast.  The partial
+// sums of rows j > m are never formed, so a NaN in U reaches exactly the q_m that
+// substitution would reach.
+__global__ void __launch_bounds__(kD) pinv_kernel(const double *__restrict__ L, int64_t ldl, int64_t n,
+                                                  const int *gstrip, double *W) {
+    __shared__ __align__(16) double Us[kD][kD];  // Us[j][i] = U(i, j): column j of U
+    __shared__ double rd[kD];
+    const int sl = blockIdx.x, m = threadIdx.x;
+    const int64_t r0 = (int64_t)gstrip[sl] * kD, lc = (int64_t)sl * kD;
+    const int D = (int)imin64(kD, n - r0);
+    for (int idx = m; idx < kD * kD; idx += kD) {
+        const int j = idx / kD, i = idx % kD;  // consecutive threads: consecutive rows of column j
+        Us[j][i] = (i <= j && j < D) ? L[(r0 + i) + (lc + j) * ldl] : 0.0;
     }
-    auto load_diag = [&](int a) {
-        const int64_t r0 = row0 + (int64_t)a * kD;
-        const int Da = (int)imin64(kD, n - r0);
-        const int64_t lc = (int64_t)(sl0 + a) * kD;
-        for (int idx = t; idx < kD * kD; idx += kDsT) {
-            const int m = idx / kD, j = idx % kD;
-            cp8(&Ls[m][j], L + (r0 + j) + (lc + m) * ldl, m < Da && j <= m);
+    __syncthreads();
+    rd[m] = m < D ? 1.0 / Us[m][m] : 0.0;
+    __syncthreads();
+    const bool act = m < D;
+    double acc[kD];
+#pragma unroll
+    for (int i = 0; i < kD; ++i) acc[i] = i == m ? 1.0 : 0.0;
+#pragma unroll
+    for (int j = kD - 1; j >= 0; --j) {
+        if (act && j <= m) {
+            acc[j] *= rd[j];  // w_j
+#pragma unroll
+            for (int i = 0; i < j; ++i) acc[i] = fma(-Us[j][i], acc[j], acc[i]);
         }
-    };
-    // tile (a, a2): rows of sub-block a, columns of sub-block a2, into Lt[buf]
-    auto load_tile = [&](int a, int a2, int buf) {
-        const int64_t r0 = row0 + (int64_t)a * kD;
-        const int Da = (int)imin64(kD, n - r0);
-        const int64_t lc2 = (int64_t)(sl0 + a2) * kD;
-        const int D2 = (int)imin64(kD, n - (row0 + (int64_t)a2 * kD));
-        double *lt = Lt + buf * kD * LDT;
-        for (int idx = t; idx < kD * kD; idx += kDsT) {
-            const int c = idx / kD, m = idx % kD;  // consecutive threads: consecutive rows (coalesced)
-            cp8(lt + m * LDT + c, L + (r0 + m) + (lc2 + c) * ldl, c < D2 && m < Da);
-        }
-    };
-    load_diag(0);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    for (int a = 0; a < na; ++a) {
-        const int64_t r0 = row0 + (int64_t)a * kD;
-        const int Da = (int)imin64(kD, n - r0);
-        if (a + 1 < na) load_tile(a, a + 1, 0);  // first update tile of this step, under the solve
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");  // R, Ls(a) landed
-        __syncthreads();
-        for (int o = t; o < kD * KB; o += kDsT) {
-            const int m = o / KB, e = o % KB;
-            qv[m * LQ + e] = m < Da ? R[(a * kD + m) * KB + e] : 0.0;
-        }
-        __syncthreads();
-        block_trsv<KB, kD + 1, (KB >= 16 ? 4 : 1)>(Ls, qv, LQ, Da, rinv);
-        for (int o = t; o < Da * k; o += kDsT) {
-            const int m = o / k, e = o % k;
-            const double v = qv[m * LQ + e];
-            for (int r = 0; r < peers.R; ++r) peers.dst[r][(r0 + m) * k + e] = v;
-        }
-        if (a + 1 < na) load_diag(a + 1);  // Ls is free (the solve and the P stores read qv)
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        for (int a2 = a + 1; a2 < na; ++a2) {
-            const int buf = (a2 - a - 1) & 1;
-            if (a2 + 1 < na) load_tile(a, a2 + 1, buf ^ 1);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            // tile (a, a2) landed: at a2 = a + 1 the diagonal tile of a + 1 and tile (a, a + 2)
-            // may still be in flight, later only the tile just issued
-            if (a2 == a + 1) asm volatile("cp.async.wait_group 2;" ::: "memory");
-            else asm volatile("cp.async.wait_group 1;" ::: "memory");
-            __syncthreads();
-            const int D2 = (int)imin64(kD, n - (row0 + (int64_t)a2 * kD));
-            const double *lt = Lt + buf * kD * LDT;
-            double *ck = chk + (chkoff[sl0 + a2] + r0 / kD) * kD * k;  // tile (r0/64, strip a2)
-            // pupdate's register block (2 columns x EPT update columns per thread, one 16-byte
-            // load per L pair, P pairs broadcast) on the first 256 threads: the update was
-            // shared-memory bound at one output per thread
-            using S = PuShape<KB>;
-            if (t < kPT) {
-                const int cg = t % S::NCG, eg = t / S::NCG;
-                const int c0 = cg * S::CPT, e0 = eg * S::EPT;
-                double acc[S::CPT][S::EPT];
-#pragma unroll
-                for (int u = 0; u < S::CPT; ++u)
-#pragma unroll
-                    for (int i = 0; i < S::EPT; ++i) {
-                        acc[u][i] = R[(a2 * kD + c0 + u) * KB + e0 + i];
-                        if (c0 + u < D2 && e0 + i < k) ck[(c0 + u) * k + e0 + i] = acc[u][i];
-                    }
-#pragma unroll 4
-                for (int m = 0; m < Da; ++m) {
-                    double l[S::CPT], pv[S::EPT];
-                    if constexpr (S::CPT == 2) {
-                        const double2 l2 = *reinterpret_cast<const double2 *>(lt + m * LDT + c0);
-                        l[0] = l2.x;
-                        l[1] = l2.y;
-                    } else {
-                        l[0] = lt[m * LDT + c0];
-                    }
-                    if constexpr (S::EPT % 2 == 0) {
-#pragma unroll
-                        for (int i = 0; i < S::EPT; i += 2) {
-                            const double2 p2 = *reinterpret_cast<const double2 *>(qv + m * LQ + e0 + i);
-                            pv[i] = p2.x;
-                            pv[i + 1] = p2.y;
-                        }
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < S::EPT; ++i) pv[i] = qv[m * LQ + e0 + i];
-                    }
-#pragma unroll
-                    for (int u = 0; u < S::CPT; ++u)
-#pragma unroll
-                        for (int i = 0; i < S::EPT; ++i) acc[u][i] = fma(-l[u], pv[i], acc[u][i]);
-                }
-#pragma unroll
-                for (int u = 0; u < S::CPT; ++u)
-#pragma unroll
-                    for (int i = 0; i < S::EPT; ++i) R[(a2 * kD + c0 + u) * KB + e0 + i] = acc[u][i];
-            }
-            __syncthreads();  // Lt[buf] is refilled two steps on
-        }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
     }
-    if (peers.flag[0]) {  // PEER mode: the P rows are visible to every rank before the flag
-        __threadfence_system();
-        __syncthreads();
-        if (t == 0)
-            for (int r = 0; r < peers.R; ++r) st_release_sys(peers.flag[r], epoch);
-    }
+    double *w = W + (int64_t)sl * kD * kD;
+#pragma unroll
+    for (int j = 0; j < kD; ++j) w[j * kD + m] = (act && j <= m) ? acc[j] : 0.0;
 }
 
 // Every rank: residuals of its strips right of solve block g -= L_{rows of g, strip}^T P,
@@ -406,8 +320,8 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restric
     extern __shared__ __align__(16) double sm_pu[];
     double *Lt = sm_pu;                // [2][kD rows m][LDT]: Lt[m][c] = L(r0 + m, strip column c)
     double *Ps = sm_pu + 2 * kD * LDT;  // [2][kD][KB]
-    const int t = threadIdx.x, cg = t % S::NCG, eg = t / S::NCG;
-    const int c0 = cg * CPT, e0 = eg * EPT;
+    const int t = threadIdx.x;
+    const int c0 = S::c0(t), e0 = S::e0(t);
     const int sl = sl_first + blockIdx.x;
     const int64_t lc = (int64_t)sl * kD;
     const int nc = (int)imin64(kD, nloc - lc);
@@ -493,6 +407,307 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_kernel(const double *__restric
 #pragma unroll
         for (int i = 0; i < EPT; ++i)
             if (c0 + u < nc && eb + e0 + i < k) rs[(c0 + u) * k + e0 + i] = acc[u][i];
+}
+
+// The same update on the FP64 tensor cores (DMMA, mma.sync m8n8k4 .f64: D(8x8) += A(8x4) B(4x8)
+// with M = strip columns c, N = update columns e, K = rows m).  Warp tile TC x TE MMA tiles;
+// the L tile is staged column-major (Lc[c][m], 16-byte cp.async straight from L's columns)
+// with a 68-double column stride and the P tile with a KB + 4 row stride, so every fragment
+// load is one conflict-free shared wavefront per half warp.  Per 4 rows a warp issues TC + TE
+// fragment loads and TC * TE MMAs (256 FMAs each) where the DFMA form issued 4 * 3 loads and
+// 4 * 8 DFMAs; the accumulators hold the NEGATED residual (so each MMA adds L^T P).
+template <int KB>
+struct PmShape {
+    static constexpr int TC = KB >= 16 ? 2 : 1;   // 8-column MMA tiles per warp along strip columns
+    static constexpr int TE = KB >= 32 ? 2 : 1;   // ... along update columns
+    static constexpr int WC = kD / (8 * TC);      // warps along strip columns
+    static_assert(WC * (KB / (8 * TE)) * 32 == kPT, "kPT threads cover 64 columns x KB");
+    static constexpr int LDC = kD + 4;            // column stride of the L tile
+    static constexpr int LDP = KB + 4;            // row stride of the P tile
+};
+template <int KB>
+size_t pupdate_mma_smem() {
+    return (size_t)(2 * kD * PmShape<KB>::LDC + 2 * kD * PmShape<KB>::LDP) * 8;
+}
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+template <int KB>
+__global__ void __launch_bounds__(kPT, 2) pupdate_mma_kernel(const double *__restrict__ L, int64_t ldl, int64_t n,
+                                                            int64_t nloc, int k, int64_t row0, int nrows,
+                                                            int sl_first, double *res, double *chk,
+                                                            const int64_t *chkoff, const double *__restrict__ P,
+                                                            const unsigned *flag, unsigned epoch) {
+    using S = PmShape<KB>;
+    constexpr int TC = S::TC, TE = S::TE, LDC = S::LDC, LDP = S::LDP;
+    const int eb = blockIdx.y * KB;  // first update column of this CTA
+    extern __shared__ __align__(16) double sm_pm[];
+    double *Lc = sm_pm;                   // [2][kD strip columns c][LDC]: Lc[c][m] = L(r0 + m, lc + c)
+    double *Ps = sm_pm + 2 * kD * LDC;    // [2][kD rows m][LDP]
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int gi = lane >> 2, tg = lane & 3;
+    const int cw = (warp % S::WC) * 8 * TC, ew = (warp / S::WC) * 8 * TE;
+    const int sl = sl_first + blockIdx.x;
+    const int64_t lc = (int64_t)sl * kD;
+    const int nc = (int)imin64(kD, nloc - lc);
+    const int na = (nrows + kD - 1) / kD;
+    const int ke = k - eb;  // update columns of this CTA that exist
+    // 16-byte copies need 16-byte aligned columns (an even ldl and an aligned L)
+    const bool v16 = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0);
+    if (flag) wait_flag_sys(flag, epoch);
+    double *rs = res + (int64_t)sl * kD * k + eb;
+    double acc[TC][TE][2];
+#pragma unroll
+    for (int u = 0; u < TC; ++u)
+#pragma unroll
+        for (int v = 0; v < TE; ++v)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = cw + 8 * u + gi, e = ew + 8 * v + 2 * tg + h;
+                acc[u][v][h] = (c < nc && e < ke) ? -rs[c * k + e] : 0.0;
+            }
+    auto issue = [&](int a) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        const int Da = (int)imin64(kD, n - r0);
+        double *lcb = Lc + (a & 1) * kD * LDC;
+        double *ps = Ps + (a & 1) * kD * LDP;
+        if (v16) {
+            for (int idx = t; idx < kD * kD / 2; idx += kPT) {
+                const int c = idx >> 5, m = 2 * (idx & 31);  // a column's 64 rows: 32 consecutive threads
+                const int bytes = (c < nc && m < Da) ? (Da - m >= 2 ? 16 : 8) : 0;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(lcb + c * LDC + m)),
+                             "l"(bytes ? L + (r0 + m) + (lc + c) * ldl : L), "r"(bytes)
+                             : "memory");
+            }
+        } else {
+            for (int idx = t; idx < kD * kD; idx += kPT) {
+                const int c = idx >> 6, m = idx & 63;
+                const bool ok = c < nc && m < Da;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(lcb + c * LDC + m)),
+                             "l"(ok ? L + (r0 + m) + (lc + c) * ldl : L), "r"(ok ? 8 : 0)
+                             : "memory");
+            }
+        }
+        for (int idx = t; idx < kD * KB; idx += kPT) {
+            const int m = idx / KB, e = idx % KB;
+            const bool ok = m < Da && e < ke;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(ps + m * LDP + e)),
+                         "l"(ok ? P + (r0 + m) * k + eb + e : P), "r"(ok ? 8 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0);
+    for (int a = 0; a < na; ++a) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        if (a + 1 < na) {
+            issue(a + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        {
+            double *ck = chk + (chkoff[sl] + r0 / kD) * kD * k + eb;
+#pragma unroll
+            for (int u = 0; u < TC; ++u)
+#pragma unroll
+                for (int v = 0; v < TE; ++v)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = cw + 8 * u + gi, e = ew + 8 * v + 2 * tg + h;
+                        if (c < nc && e < ke) ck[c * k + e] = -acc[u][v][h];
+                    }
+        }
+        const double *la = Lc + (a & 1) * kD * LDC + (cw + gi) * LDC + tg;
+        const double *pb = Ps + (a & 1) * kD * LDP + tg * LDP + ew + gi;
+#pragma unroll 4
+        for (int m0 = 0; m0 < kD; m0 += 4) {
+            double af[TC], bf[TE];
+#pragma unroll
+            for (int u = 0; u < TC; ++u) af[u] = la[8 * u * LDC + m0];
+#pragma unroll
+            for (int v = 0; v < TE; ++v) bf[v] = pb[m0 * LDP + 8 * v];
+#pragma unroll
+            for (int u = 0; u < TC; ++u)
+#pragma unroll
+                for (int v = 0; v < TE; ++v) dmma_884(acc[u][v], af[u], bf[v]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < TC; ++u)
+#pragma unroll
+        for (int v = 0; v < TE; ++v)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = cw + 8 * u + gi, e = ew + 8 * v + 2 * tg + h;
+                if (c < nc && e < ke) rs[c * k + e] = -acc[u][v][h];
+            }
+}
+
+// The owner's diagonal solve of column block g: P rows [row0, row0 + nrows) = L_gg^{-T} r_g,
+// 64-row sub-block a after sub-block a: q_a = W_a^T r_a (W_a the inverted diagonal block of
+// pinv_kernel), the rows written to every rank's P, then the residuals (and Apply
+// checkpoints) of the block's later sub-blocks updated with them; both products on the FP64
+// tensor cores (DMMA m8n8k4), the diagonal 8x8 blocks of the first by DFMA so that a product
+// 0 * r_j with j > m is never formed (a NaN in r_j reaches q_m only for m >= j, as in
+// substitution).  One CTA; the block's residuals stay in shared memory for the whole kernel
+// (they are dead after it: the block's strips have no tiles below it), and every W and L
+// tile is prefetched a step ahead (cp.async), so the only exposed latency is the first load.
+template <int KB>
+struct DsShape {
+    static constexpr int NE = KB >= 8 ? KB : 8;  // update columns held (MMA N = 8: KB = 4 pads)
+    static constexpr int LDR = NE + 4;           // row stride of R and q (conflict-free B fragments)
+    static constexpr int LDW = kD + 4;           // row stride of W, column stride of the L tiles
+    static constexpr int ET = NE / 8;            // 8-column MMA tiles along update columns
+    static constexpr int TPW = (8 * ET + 15) / 16;  // of them per warp (16 warps, 8 row / column tiles)
+};
+template <int KB>
+__global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restrict__ L, int64_t ldl, int64_t n, int k,
+                                                       int64_t row0, int nrows, int sl0, double *res, double *chk,
+                                                       const int64_t *chkoff, const double *__restrict__ Winv,
+                                                       Peers peers, unsigned epoch) {
+    using S = DsShape<KB>;
+    constexpr int NE = S::NE, LDR = S::LDR, LDW = S::LDW, ET = S::ET, TPW = S::TPW;
+    extern __shared__ __align__(16) double sm_ds[];
+    double *Ws = sm_ds;                // [kD rows j][LDW]: W(j, m) of the current sub-block
+    double *Lc = Ws + kD * LDW;        // [2][kD columns c][LDW]: Lc[c][m] = L(r0 + m, column c of sub-block a2)
+    double *qv = Lc + 2 * kD * LDW;    // [kD][LDR]: q of the current sub-block
+    double *R = qv + kD * LDR;         // [rows][LDR]: the block's residuals
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gi = lane >> 2, tg = lane & 3;
+    const int na = (nrows + kD - 1) / kD;
+    const bool v16 = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0);
+    // the whole block's residuals (one round trip) and the first W
+    for (int o = t; o < na * kD * NE; o += kDsT) {
+        const int row = o / NE, e = o % NE;
+        const int a = row / kD, m = row % kD;
+        cp8(R + row * LDR + e, res + (int64_t)(sl0 + a) * kD * k + m * k + e, e < k && row < nrows);
+    }
+    auto load_w = [&](int a) {  // W of sub-block a: 32 KB, contiguous
+        const double *src = Winv + (int64_t)(sl0 + a) * kD * kD;
+        for (int idx = t; idx < kD * kD / 2; idx += kDsT) {
+            const int j = idx >> 5, m = 2 * (idx & 31);
+            cp16(Ws + j * LDW + m, src + j * kD + m);
+        }
+    };
+    // tile (a, a2): rows of sub-block a, columns of sub-block a2, column-major into Lc[buf]
+    auto load_tile = [&](int a, int a2, int buf) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        const int Da = (int)imin64(kD, n - r0);
+        const int64_t lc2 = (int64_t)(sl0 + a2) * kD;
+        const int D2 = (int)imin64(kD, n - (row0 + (int64_t)a2 * kD));
+        double *lt = Lc + buf * kD * LDW;
+        if (v16) {
+            for (int idx = t; idx < kD * kD / 2; idx += kDsT) {
+                const int c = idx >> 5, m = 2 * (idx & 31);  // a column's 64 rows: 32 consecutive threads
+                const int bytes = (c < D2 && m < Da) ? (Da - m >= 2 ? 16 : 8) : 0;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(lt + c * LDW + m)),
+                             "l"(bytes ? L + (r0 + m) + (lc2 + c) * ldl : L), "r"(bytes)
+                             : "memory");
+            }
+        } else {
+            for (int idx = t; idx < kD * kD; idx += kDsT) {
+                const int c = idx >> 6, m = idx & 63;
+                cp8(lt + c * LDW + m, L + (r0 + m) + (lc2 + c) * ldl, c < D2 && m < Da);
+            }
+        }
+    };
+    load_w(0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int a = 0; a < na; ++a) {
+        const int64_t r0 = row0 + (int64_t)a * kD;
+        const int Da = (int)imin64(kD, n - r0);
+        if (a + 1 < na) load_tile(a, a + 1, 0);  // first update tile of this step, under the solve
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // R, W(a) landed
+        __syncthreads();
+        // q = W^T r_a: M = rows m, N = update columns e, K = rows j; warp -> row tile, TPW column tiles
+        {
+            const int mt = warp % 8, eg = warp / 8;
+            if (eg * TPW < ET) {
+                const int m0 = mt * 8;
+                const double *Ra = R + a * kD * LDR;
+                double acc[TPW][2];
+#pragma unroll
+                for (int v = 0; v < TPW; ++v) acc[v][0] = acc[v][1] = 0.0;
+                for (int j0 = 0; j0 < m0; j0 += 4) {  // blocks strictly above the tile's rows: j < m
+                    const double af = Ws[(j0 + tg) * LDW + m0 + gi];
+#pragma unroll
+                    for (int v = 0; v < TPW; ++v) dmma_884(acc[v], af, Ra[(j0 + tg) * LDR + (eg * TPW + v) * 8 + gi]);
+                }
+                const int m = m0 + gi;
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int e = (eg * TPW + v) * 8 + 2 * tg + h;
+                        double s = acc[v][h];
+                        for (int j = m0; j <= m; ++j) s = fma(Ws[j * LDW + m], Ra[j * LDR + e], s);
+                        qv[m * LDR + e] = m < Da ? s : 0.0;  // rows past the block stay zero
+                    }
+            }
+        }
+        __syncthreads();
+        for (int o = t; o < Da * k; o += kDsT) {
+            const int m = o / k, e = o % k;
+            const double v = qv[m * LDR + e];
+            for (int r = 0; r < peers.R; ++r) peers.dst[r][(r0 + m) * k + e] = v;
+        }
+        if (a + 1 < na) load_w(a + 1);  // Ws is free (the P stores and updates read qv)
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        for (int a2 = a + 1; a2 < na; ++a2) {
+            const int buf = (a2 - a - 1) & 1;
+            if (a2 + 1 < na) load_tile(a, a2 + 1, buf ^ 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            // tile (a, a2) landed: at a2 = a + 1 W(a + 1) and tile (a, a + 2) may still be in
+            // flight, later only the tile just issued
+            if (a2 == a + 1) asm volatile("cp.async.wait_group 2;" ::: "memory");
+            else asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();
+            const int D2 = (int)imin64(kD, n - (row0 + (int64_t)a2 * kD));
+            double *ck = chk + (chkoff[sl0 + a2] + r0 / kD) * kD * k;  // tile (r0/64, strip a2)
+            // r_a2 -= L_tile^T q: M = strip columns c, N = update columns e, K = rows m
+            const int ct = warp % 8, eg = warp / 8;
+            if (eg * TPW < ET) {
+                const int c = ct * 8 + gi;
+                double *Rc = R + (a2 * kD + c) * LDR;
+                double acc[TPW][2];
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int e = (eg * TPW + v) * 8 + 2 * tg + h;
+                        const double r = Rc[e];
+                        if (c < D2 && e < k) ck[c * k + e] = r;
+                        acc[v][h] = -r;
+                    }
+                const double *la = Lc + buf * kD * LDW + c * LDW + tg;
+                const double *qb = qv + tg * LDR + eg * TPW * 8 + gi;
+#pragma unroll 4
+                for (int m0 = 0; m0 < kD; m0 += 4) {
+                    const double af = la[m0];
+#pragma unroll
+                    for (int v = 0; v < TPW; ++v) dmma_884(acc[v], af, qb[m0 * LDR + v * 8]);
+                }
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) Rc[(eg * TPW + v) * 8 + 2 * tg + h] = -acc[v][h];
+            }
+            __syncthreads();  // Lc[buf] is refilled two steps on
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+    }
+    if (peers.flag[0]) {  // PEER mode: the P rows are visible to every rank before the flag
+        __threadfence_system();
+        __syncthreads();
+        if (t == 0)
+            for (int r = 0; r < peers.R; ++r) st_release_sys(peers.flag[r], epoch);
+    }
 }
 
 // Q_b = P_b^T P_b per 64-row block (KB x KB, zero padded)
@@ -652,7 +867,8 @@ struct Rank {
 
 template <int KB>
 size_t dsolve_smem() {
-    return (size_t)(kD * (kD + 1) + 2 * kD * (kD + 2) + kD * (KB + 2) + kD + (KB <= 16 ? kDsMaxRows : kDsMaxRows / 2) * KB) * 8;
+    using S = DsShape<KB>;
+    return (size_t)(3 * kD * S::LDW + kD * S::LDR + (KB <= 16 ? kDsMaxRows : kDsMaxRows / 2) * S::LDR) * 8;
 }
 template <int KB>
 size_t pupdate_smem() {
@@ -703,6 +919,44 @@ gcm_status_t aux_stream(cudaStream_t *s, cudaEvent_t **ready, cudaEvent_t **done
     return GCM_OK;
 }
 
+// GCM_PANEL_TRACE=1 (debug): timing events around every solve block's kernels (solve, lookahead
+// on the call stream; the rest on the aux stream) and a per-phase summary on stderr after the
+// pass -- how much of the chain is the solve, the lookahead, and waiting for the rest.
+struct ChainTrace {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;  // per block: [solve start, solve end, lookahead end, rest end]
+    explicit ChainTrace(int NSB) {
+        on = std::getenv("GCM_PANEL_TRACE") != nullptr;
+        if (!on) return;
+        ev.resize((size_t)NSB * 4);
+        for (auto &e : ev) cudaEventCreate(&e);
+    }
+    void rec(int g, int i, cudaStream_t s) {
+        if (on) cudaEventRecord(ev[(size_t)g * 4 + i], s);
+    }
+    void report(int NSB) {
+        if (!on) return;
+        cudaEventSynchronize(ev.back());
+        cudaDeviceSynchronize();
+        double tot[4] = {0, 0, 0, 0};  // solve, lookahead, rest, gap before the next solve
+        for (int g = 0; g < NSB; ++g) {
+            float a = 0, b = 0, c = 0, d = 0;
+            cudaEventElapsedTime(&a, ev[g * 4 + 0], ev[g * 4 + 1]);
+            cudaEventElapsedTime(&b, ev[g * 4 + 1], ev[g * 4 + 2]);
+            cudaEventElapsedTime(&c, ev[g * 4 + 2], ev[g * 4 + 3]);
+            if (g + 1 < NSB) cudaEventElapsedTime(&d, ev[g * 4 + 2], ev[(g + 1) * 4 + 0]);
+            tot[0] += a, tot[1] += b, tot[2] += c, tot[3] += d;
+        }
+        float all = 0;
+        cudaEventElapsedTime(&all, ev[0], ev.back());
+        std::fprintf(stderr,
+                     "gcm panel trace: %d blocks, chain %.3f ms: solve %.3f, lookahead %.3f, gap %.3f; "
+                     "rest (aux, overlapped) %.3f ms\n",
+                     NSB, all, tot[0], tot[1], tot[3], tot[2]);
+        for (auto &e : ev) cudaEventDestroy(e);
+    }
+};
+
 // one pass (<= 32 update columns) over all ranks of `rk` (Virtual: all R; else rk has one entry)
 template <int KB>
 gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int k, int sigma, int64_t ebase,
@@ -733,6 +987,15 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         st = check_cuda(cudaFuncSetAttribute(pupdate_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pupdate_smem<8>()));
     if (st == GCM_OK)
+        st = check_cuda(cudaFuncSetAttribute(pupdate_mma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)pupdate_mma_smem<8>()));
+    constexpr int KBM = KB >= 8 ? KB : 8;  // (KB = 4 keeps the DFMA kernel)
+    if (st == GCM_OK)
+        st = check_cuda(cudaFuncSetAttribute(pupdate_mma_kernel<KBM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)pupdate_mma_smem<KBM>()));
+    // GCM_PU_DFMA=1: the residual updates on the DFMA kernel (A/B against the tensor-core one)
+    const bool pu_mma = KB >= 8 && std::getenv("GCM_PU_DFMA") == nullptr;
+    if (st == GCM_OK)
         st = check_cuda(cudaFuncSetAttribute(pdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pdiag_smem<KB>()));
     if (st != GCM_OK) return st;
@@ -747,6 +1010,12 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
     // 2. the right-looking solve over column blocks
     {
         ProfScope ps("ptrsv", stream);
+        for (auto &q : rk) {  // inverses of the diagonal blocks the solve chain multiplies by
+            if (q.plan.nsl == 0) continue;
+            pinv_kernel<<<q.plan.nsl, kD, 0, stream>>>(q.L, q.ldl, n, q.at<int>(q.cv.gstrip),
+                                                       q.at<double>(q.cv.Winv));
+            count_launch();
+        }
         cudaStream_t aux = nullptr;
         cudaEvent_t *p_ready = nullptr, *rest_done = nullptr;
         st = aux_stream(&aux, &p_ready, &rest_done);
@@ -756,8 +1025,10 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         if (st != GCM_OK) return st;
         const int64_t sb = rk[0].plan.sb;
         const int NSB = rk[0].plan.NSB;
+        ChainTrace tr(NSB);
         for (int g = 0; g < NSB; ++g) {  // solve blocks of sb rows (sb divides nb)
             const int64_t row0 = (int64_t)g * sb;
+            tr.rec(g, 0, stream);
             const int owner = (int)((row0 / nb) % R);
             const int nrows = (int)std::min<int64_t>(sb, n - row0);
             const int ol = x.mode == Mode::Virtual ? owner : (owner == x.self ? 0 : -1);
@@ -770,7 +1041,7 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                     for (int r = 0; r < R; ++r) p.flag[r] = x.peerFlag[r] + g;
                 dsolve_kernel<KB><<<1, kDsT, dsolve_smem<KB>(), stream>>>(
                     q.L, q.ldl, n, k, row0, nrows, sl0, q.at<double>(q.cv.res), q.at<double>(q.cv.chk),
-                    q.at<int64_t>(q.cv.chkoff), p, epoch);
+                    q.at<int64_t>(q.cv.chkoff), q.at<double>(q.cv.Winv), p, epoch);
                 count_launch();
             }
 #ifdef GCM_WITH_NCCL
@@ -786,6 +1057,7 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
             // lookahead: the strips of the NEXT solve block first, on the call's stream (after the
             // rest of block g-1, which touched the same residuals); the rest on the aux stream,
             // where it overlaps the next diagonal solve
+            tr.rec(g, 1, stream);
             if (g >= 1) {
                 st = check_cuda(cudaStreamWaitEvent(stream, rest_done[(g - 1) & 1], 0));
                 if (st != GCM_OK) return st;
@@ -793,6 +1065,7 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
             for (int pass = 0; pass < 2; ++pass) {
                 cudaStream_t sp = pass == 0 ? stream : aux;
                 if (pass == 1) {
+                    tr.rec(g, 2, stream);
                     st = check_cuda(cudaEventRecord(p_ready[g & 1], stream));
                     if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(aux, p_ready[g & 1], 0));
                     if (st != GCM_OK) return st;
@@ -806,7 +1079,15 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                     const int rank_id = x.mode == Mode::Virtual ? ri : x.self;
                     const unsigned *flag =
                         (x.mode == Mode::Peer && rank_id != owner) ? x.peerFlag[x.self] + g : nullptr;
-                    if (pass == 0 && KB > 8) {  // lookahead: the chain waits on it -- 8 update columns per CTA
+                    if (pass == 0 && KB > 8 && pu_mma) {  // lookahead: the chain waits on it -- 8 update columns per CTA
+                        pupdate_mma_kernel<8><<<dim3(s_hi - s_lo, KB / 8), kPT, pupdate_mma_smem<8>(), sp>>>(
+                            q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                            q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                    } else if (pu_mma) {
+                        pupdate_mma_kernel<KBM><<<s_hi - s_lo, kPT, pupdate_mma_smem<KBM>(), sp>>>(
+                            q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                            q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                    } else if (pass == 0 && KB > 8) {
                         pupdate_kernel<8><<<dim3(s_hi - s_lo, KB / 8), kPT, pupdate_smem<8>(), sp>>>(
                             q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
                             q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
@@ -819,8 +1100,10 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                 }
             }
             st = check_cuda(cudaEventRecord(rest_done[g & 1], aux));
+            tr.rec(g, 3, aux);
             if (st != GCM_OK) return st;
         }
+        tr.report(NSB);
         st = check_cuda(cudaStreamWaitEvent(stream, rest_done[(NSB - 1) & 1], 0));  // join the aux stream
         if (st == GCM_OK) st = check_cuda(cudaGetLastError());
         if (st != GCM_OK) return st;
