@@ -20,6 +20,7 @@ workload as the reference arm (rank 0 only).
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -523,6 +524,22 @@ def run_reference(args, world, rank):
             "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+@contextlib.contextmanager
+def stdout_to_stderr():
+    """File descriptor 1 -> 2 while the run executes: whatever native libraries print (NCCL's
+    version banner ignores NCCL_DEBUG on some boxes) goes to stderr, so the JSON line is the
+    only line bench.py writes to stdout."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -542,13 +559,15 @@ def main():
         if rank == 0:
             print(json.dumps(run_reference(args, world, rank)), flush=True)
         return
-    world, rank, local = dist_setup(args.gpus)
-    out = run_ours(args, world, rank, local)
+    with stdout_to_stderr():  # library banners (NCCL's version line) must not precede the JSON line
+        world, rank, local = dist_setup(args.gpus)
+        out = run_ours(args, world, rank, local)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist
-        dist.destroy_process_group()
+        with stdout_to_stderr():
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -49,6 +49,7 @@ constexpr int kTrsvThreads = 288;  // chain CTA: 2 critical + 6 prep + loader wa
 constexpr int kBKMax = 32;         // update columns per pass
 constexpr int kApplyT = 64;        // threads per apply CTA (= kD columns)
 constexpr int kLdT = kDT + 1;
+constexpr int kLdR = kDT + 4;  // column stride of a helper's ring tiles (conflict-free MMA fragments)
 #ifndef GCM_LOOKC
 #define GCM_LOOKC 4
 #endif
@@ -134,6 +135,9 @@ __device__ __forceinline__ long long gtime() {
 __device__ long long g_htrace[4096 * 8];  // hand-off timeline in globaltimer ns, indexed by strip s
 #define HTRACE(slot, s) (g_htrace[(s) * 8 + (slot)] = gtime())
 #define CTRACE(slot, s) (g_trace[(s) * 8 + (slot)] = clock64())
+// kernel timeline (globaltimer ns, max over CTAs): 0 trsv entry, 1 J1 done, 2 chain start, 3 chain end, 4 btma end
+#define JMARK(slot) (g_htrace[2001 * 8 + (slot)] = gtime())
+#define TLINE(slot) atomicMax(reinterpret_cast<unsigned long long *>(&g_htrace[2000 * 8 + (slot)]), (unsigned long long)gtime())
 // one helper's per-tile phases (clock64), rows = tile sequence number
 #define HPT(slot, val) ((h == 100 && t == 0 && seq < 2900) ? (void)(g_htrace[seq * 8 + (slot)] = (val)) : (void)0)
 __device__ long long g_trace[4096 * 8];
@@ -143,6 +147,8 @@ __device__ long long g_trace[4096 * 8];
 #define HTRACE(slot, s) ((void)0)
 #define CTRACE(slot, s) ((void)0)
 #define HPT(slot, val) ((void)0)
+#define TLINE(slot) ((void)0)
+#define JMARK(slot) ((void)0)
 #endif
 
 // Bytes of Apply checkpoints before the checkpoint interval CI doubles (2 GiB;
@@ -252,7 +258,12 @@ static_assert(kWin >= kLookC * kDT && kLookC <= 16, "p window indexed by row & (
 // (GCM_HELP_OWN_CAP=<m> lowers it at run time: the tests use it to drive the spill path,
 // which the default only reaches at n > ~50k (KB = 32) / ~107k (KB <= 16))
 __host__ __device__ constexpr int help_max_own(int KB) { return KB <= 16 ? 24 : 12; }
-constexpr int kHelpRing = 6;            // tiles (L tile + P block) a helper's feeder keeps in flight
+#ifndef GCM_HELP_RING
+#define GCM_HELP_RING 3
+#endif
+constexpr int kHelpRing = GCM_HELP_RING;  // tiles (L tile + P block) a helper's feeder keeps in flight
+// (3: a deeper ring bulk-copies P blocks before the chains have written them, and the compute
+// warps then re-poll every value; profiles/r02ar_ab_helper_ring.txt)
 #ifndef GCM_FASTBACK
 #define GCM_FASTBACK 2
 #endif
@@ -361,23 +372,30 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         double acc0[kRPC], acc1[kRPC];
 #pragma unroll
         for (int w = 0; w < kRPC; ++w) acc0[w] = acc1[w] = 0.0;
-        {  // - N p over this warp's share of the kSeg segment rows
+        {  // - N p over this warp's share of the kSeg segment rows: every shared load of the
+           // share issued before the first FMA (a load-FMA loop left each iteration waiting on
+           // its own loads: ~1.3k cycles per step, the chain's largest phase)
             constexpr int kPer = (kSeg + kPrepWarps - 1) / kPrepWarps;
             const int r0 = pw * kPer;
             const double *nrow = st + j * kLdN;
+            double l[kPer];
+            double2 pv[kPer];
 #pragma unroll
             for (int q = 0; q < kPer; ++q) {
                 const int R = r0 + q;
-                if (R < kSeg) {
-                    const double l = nrow[R];
-                    const double2 pv = *reinterpret_cast<const double2 *>(pwin + ((rs + R) & (kWin - 1)) * kRPC);
-                    if (q & 1) {
-                        acc1[0] = fma(-l, pv.x, acc1[0]);
-                        acc1[1] = fma(-l, pv.y, acc1[1]);
-                    } else {
-                        acc0[0] = fma(-l, pv.x, acc0[0]);
-                        acc0[1] = fma(-l, pv.y, acc0[1]);
-                    }
+                const bool in = kSeg % kPrepWarps == 0 || R < kSeg;
+                l[q] = in ? nrow[R] : 0.0;
+                pv[q] = in ? *reinterpret_cast<const double2 *>(pwin + ((rs + R) & (kWin - 1)) * kRPC)
+                           : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int q = 0; q < kPer; ++q) {
+                if (q & 1) {
+                    acc1[0] = fma(-l[q], pv[q].x, acc1[0]);
+                    acc1[1] = fma(-l[q], pv[q].y, acc1[1]);
+                } else {
+                    acc0[0] = fma(-l[q], pv[q].x, acc0[0]);
+                    acc0[1] = fma(-l[q], pv[q].y, acc0[1]);
                 }
             }
         }
@@ -397,6 +415,14 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         {  // + X^T r^{hand} over this warp's share of the 32 rows q
             constexpr int kPerX = (kDT + kPrepWarps - 1) / kPrepWarps;
             const double *X = st + kMXN + kDT * kDT;
+            double x[kPerX];
+            double2 hvv[kPerX];
+#pragma unroll
+            for (int u = 0; u < kPerX; ++u) {  // loads first (as above)
+                const int q = pw * kPerX + u;
+                x[u] = q <= j ? X[q * kDT + j] : 0.0;
+                hvv[u] = q <= j ? *reinterpret_cast<const double2 *>(hand + q * kRPC) : make_double2(0.0, 0.0);
+            }
 #pragma unroll
             for (int u = 0; u < kPerX; ++u) {
                 const int q = pw * kPerX + u;
@@ -404,10 +430,8 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
                 // multiplied -- a NaN residual of a later row must not reach row j (0 * NaN),
                 // or a NaN input would be reported at an earlier row (R5, R6)
                 if (q <= j) {
-                    const double x = X[q * kDT + j];
-                    const double2 hvv = *reinterpret_cast<const double2 *>(hand + q * kRPC);
-                    acc0[0] = fma(x, hvv.x, acc0[0]);
-                    acc0[1] = fma(x, hvv.y, acc0[1]);
+                    acc0[0] = fma(x[u], hvv[u].x, acc0[0]);
+                    acc0[1] = fma(x[u], hvv[u].y, acc0[1]);
                 }
             }
         }
@@ -446,6 +470,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         return;
     }
     if (warp > kSvcWarp) return;
+    if (t == 0) TLINE(2);
     for (int tb = 0; tb < NT; ++tb) {
         if (warp < kRPC) {
             const int w = warp, j = lane;
@@ -490,6 +515,7 @@ __device__ void trsv_chain(const TrsvArgs &a, double *smem, int c) {
         }
         named_bar(1, kSvcWarp * 32);  // B_{tb+1}: p_tb and prepX_{tb+1} ready
     }
+    if (t == 0) TLINE(3);
 }
 
 // ---------------------------------------------------------------- helper CTAs
@@ -503,75 +529,9 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
     const int k = a.k;
     const int NT = (int)((a.n + kDT - 1) / kDT);
 
-    // J1: per 32-block tb: X = L_tb,tb^{-1} (upper) and M = X^T L_{tb-1,tb}^T, the
-    // operands of the chain's critical step  p_tb = X^T prep - M p_{tb-1}.
-    for (int tb = h; tb < NT; tb += H) {
-        const int64_t r0 = (int64_t)tb * kDT;
-        const int nr = (int)imin64(kDT, a.n - r0);
-        double *Xs = Pt;  // reuse: [kDT][kLdT]  Xs[q][j] = X(q, j)   (needs kDT*kLdT <= kDT*KB + ... see smem plan)
-        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
-            const int c = idx / kDT, m = idx % kDT;
-            double v = 0.0;
-            if (c < nr && m <= c) v = a.L[(r0 + m) + (r0 + c) * a.ldl];
-            else if (c >= nr && m == c) v = 1.0;  // identity padding
-            Lb[c * kLdT + m] = v;
-        }
-        __syncthreads();
-        if (t < kDT) {
-            const int c = t;
-            double x[kDT];
-#pragma unroll
-            for (int j = kDT - 1; j >= 0; --j) {
-                double s = (j == c) ? 1.0 : 0.0;
-#pragma unroll
-                for (int m = j + 1; m < kDT; ++m)
-                    if (m <= c) s = fma(-Lb[m * kLdT + j], x[m], s);  // skipped, not times 0 (NaN inputs)
-                x[j] = j <= c ? s / Lb[j * kLdT + j] : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < kDT; ++j) Xs[j * kLdT + c] = x[j];
-        }
-        __syncthreads();
-        // Lb <- L tile (rows of block tb-1, columns of block tb):  Lb[q][m] = L(row (tb-1)*32+m, col tb*32+q)
-        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
-            const int q = idx / kDT, m = idx % kDT;
-            Lb[q * kLdT + m] = (tb > 0 && q < nr) ? a.L[(r0 - kDT + m) + (r0 + q) * a.ldl] : 0.0;
-        }
-        // segment (rows rs .. rs+kSeg-1 = blocks tb-kLookC .. tb-2, columns of block tb) into the
-        // (still idle) tile ring:  sg[q][R] = L(rs + R, tb*32 + q), zero above row 0
-        double *sg = rs + kHelpMaxOwn * kDT * KB;
-        const int64_t rseg = r0 - (int64_t)kLookC * kDT;
-        for (int idx = t; idx < kDT * kSeg; idx += kTrsvThreads) {
-            const int q = idx / kSeg, R = idx % kSeg;
-            sg[q * kLdN + R] = (q < nr && rseg + R >= 0) ? a.L[(rseg + R) + (r0 + q) * a.ldl] : 0.0;
-        }
-        __syncthreads();
-        double *mx = a.MX + (int64_t)tb * kMXStride;
-        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
-            const int m = idx / kDT, j = idx % kDT;  // M(j, m) = sum_{q <= j} X(q, j) L(m, q)
-            // X is upper triangular: the q > j terms are skipped, not multiplied by zero, so a
-            // NaN entry of a later column cannot reach row j (DESIGN.md R5, R6)
-            double s0 = 0.0, s1 = 0.0;
-            for (int q = 0; q <= j; q += 2) {
-                s0 = fma(Xs[q * kLdT + j], Lb[q * kLdT + m], s0);
-                if (q + 1 <= j) s1 = fma(Xs[(q + 1) * kLdT + j], Lb[(q + 1) * kLdT + m], s1);
-            }
-            mx[kMXN + m * kDT + j] = s0 + s1;                        // M^T row-major: (m, j)
-            mx[kMXN + kDT * kDT + m * kDT + j] = Xs[m * kLdT + j];   // X row-major: (q=m, j)
-        }
-        for (int idx = t; idx < kDT * kSeg; idx += kTrsvThreads) {
-            const int j = idx / kSeg, R = idx % kSeg;  // N(j, R) = sum_{q <= j} X(q, j) L(rs + R, q)
-            double s0 = 0.0, s1 = 0.0;
-            for (int q = 0; q <= j; q += 2) {
-                s0 = fma(Xs[q * kLdT + j], sg[q * kLdN + R], s0);
-                if (q + 1 <= j) s1 = fma(Xs[(q + 1) * kLdT + j], sg[(q + 1) * kLdN + R], s1);
-            }
-            mx[j * kLdN + R] = s0 + s1;
-        }
-        cta_publish(a.lflag + tb, a.epoch);
-    }
-
-    // J2: column strips s = h, h+H, ...
+    // J2 set-up first (residual = V of every owned strip, the early hand-offs and the tile
+    // (0, s) checkpoints): the chain's first steps wait on those hand-offs, which used to come
+    // after all of this helper's J1 blocks.  Column strips s = h, h+H, ...
     auto rptr = [&](int i, int s) -> double * {  // residual of owned strip #i (smem or global)
         return i < a.own_cap ? rs + i * kDT * KB : a.rcur + (int64_t)s * kDT * k;
     };
@@ -594,6 +554,93 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
         }
     }
     __syncthreads();
+    // J1: per 32-block tb: X = L_tb,tb^{-1} (upper) and M = X^T L_{tb-1,tb}^T, the
+    // operands of the chain's critical step  p_tb = X^T prep - M p_{tb-1}.
+    for (int tb = h; tb < NT; tb += H) {
+        if (t == 0 && h == 0 && tb == 0) JMARK(0);
+        const int64_t r0 = (int64_t)tb * kDT;
+        const int nr = (int)imin64(kDT, a.n - r0);
+        double *Xs = Pt;  // reuse: [kDT][kLdT]  Xs[q][j] = X(q, j)   (needs kDT*kLdT <= kDT*KB + ... see smem plan)
+        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
+            const int c = idx / kDT, m = idx % kDT;
+            double v = 0.0;
+            if (c < nr && m <= c) v = a.L[(r0 + m) + (r0 + c) * a.ldl];
+            else if (c >= nr && m == c) v = 1.0;  // identity padding
+            Lb[c * kLdT + m] = v;
+        }
+        __syncthreads();
+        if (t == 0 && h == 0 && tb == 0) JMARK(1);
+        // X column c by back substitution in column (axpy) form: x_j = acc_j / L_jj, then
+        // acc_i -= L(i, j) x_j for i < j -- 32 independent running sums per thread, so the
+        // dependent chain is one multiply + one FMA per row (the row form chained ~16 FMAs and
+        // a division per row: 15 us of the kernel's start-up).  Columns j > c are skipped, not
+        // multiplied by zero (NaN inputs).
+        double *rd = rs + kHelpMaxOwn * kDT * KB + kDT * kLdN;  // [kDT] in the idle ring, after the segment
+        if (t < kDT) rd[t] = 1.0 / Lb[t * kLdT + t];
+        __syncthreads();
+        if (t < kDT) {
+            const int c = t;
+            double acc[kDT];
+#pragma unroll
+            for (int i = 0; i < kDT; ++i) acc[i] = i == c ? 1.0 : 0.0;
+#pragma unroll
+            for (int j = kDT - 1; j >= 0; --j) {
+                if (j <= c) {
+                    acc[j] *= rd[j];
+#pragma unroll
+                    for (int i = 0; i < j; ++i) acc[i] = fma(-Lb[j * kLdT + i], acc[j], acc[i]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kDT; ++j) Xs[j * kLdT + c] = j <= c ? acc[j] : 0.0;
+        }
+        __syncthreads();
+        if (t == 0 && h == 0 && tb == 0) JMARK(2);
+        // Lb <- L tile (rows of block tb-1, columns of block tb):  Lb[q][m] = L(row (tb-1)*32+m, col tb*32+q)
+        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
+            const int q = idx / kDT, m = idx % kDT;
+            Lb[q * kLdT + m] = (tb > 0 && q < nr) ? a.L[(r0 - kDT + m) + (r0 + q) * a.ldl] : 0.0;
+        }
+        // segment (rows rs .. rs+kSeg-1 = blocks tb-kLookC .. tb-2, columns of block tb) into the
+        // (still idle) tile ring:  sg[q][R] = L(rs + R, tb*32 + q), zero above row 0
+        double *sg = rs + kHelpMaxOwn * kDT * KB;
+        const int64_t rseg = r0 - (int64_t)kLookC * kDT;
+        for (int idx = t; idx < kDT * kSeg; idx += kTrsvThreads) {
+            const int q = idx / kSeg, R = idx % kSeg;
+            sg[q * kLdN + R] = (q < nr && rseg + R >= 0) ? a.L[(rseg + R) + (r0 + q) * a.ldl] : 0.0;
+        }
+        __syncthreads();
+        if (t == 0 && h == 0 && tb == 0) JMARK(3);
+        double *mx = a.MX + (int64_t)tb * kMXStride;
+        for (int idx = t; idx < kDT * kDT; idx += kTrsvThreads) {
+            const int m = idx / kDT, j = idx % kDT;  // M(j, m) = sum_{q <= j} X(q, j) L(m, q)
+            // X is upper triangular: the q > j terms are skipped, not multiplied by zero, so a
+            // NaN entry of a later column cannot reach row j (DESIGN.md R5, R6)
+            // (fully unrolled with the q > j FMAs predicated off: the loads pipeline)
+            double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int q = 0; q < kDT; ++q) {
+                const double xv = Xs[q * kLdT + j], lv = Lb[q * kLdT + m];
+                if (q <= j) s[q & 3] = fma(xv, lv, s[q & 3]);
+            }
+            mx[kMXN + m * kDT + j] = (s[0] + s[1]) + (s[2] + s[3]);  // M^T row-major: (m, j)
+            mx[kMXN + kDT * kDT + m * kDT + j] = Xs[m * kLdT + j];   // X row-major: (q=m, j)
+        }
+        for (int idx = t; idx < kDT * kSeg; idx += kTrsvThreads) {
+            const int j = idx / kSeg, R = idx % kSeg;  // N(j, R) = sum_{q <= j} X(q, j) L(rs + R, q)
+            double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int q = 0; q < kDT; ++q) {
+                const double xv = Xs[q * kLdT + j], lv = sg[q * kLdN + R];
+                if (q <= j) s[q & 3] = fma(xv, lv, s[q & 3]);
+            }
+            mx[j * kLdN + R] = (s[0] + s[1]) + (s[2] + s[3]);
+        }
+        cta_publish(a.lflag + tb, a.epoch);
+        if (t == 0 && h == 0 && tb == 0) JMARK(4);
+    }
+    if (t == 0) TLINE(1);
+
     // Tiles (tb, s), s owned and > tb, in tb-major order, flow through a ring of
     // kHelpRing shared-memory slots (L tile + P block).  Warp 8 (the feeder) runs
     // ahead: it issues the static L tile as soon as a slot is free, waits until
@@ -614,7 +661,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
             x.ii = first_owned_after(x.tb);
         }
     };
-    constexpr int kSlot = kDT * kLdT + kDT * KB;  // L tile [32][kLdT] + P block [32][k] (dense, bulk copy)
+    constexpr int kSlot = kDT * kLdR + kDT * KB;  // L tile [32][kLdR] + P block [32][k] (dense, bulk copy)
     double *ring = rs + kHelpMaxOwn * kDT * KB;  // [kHelpRing][kSlot]
     unsigned long long *full = reinterpret_cast<unsigned long long *>(ring + kHelpRing * kSlot);
     unsigned long long *empty = full + kHelpRing;
@@ -654,7 +701,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
             const int64_t c0 = (int64_t)s * kDT;
             const int nc = (int)imin64(kDT, a.n - c0);
             for (int cc = 0; cc < nc; ++cc)  // lane = row: coalesced 256-byte column segments
-                cp_async8(stg + cc * kLdT + lane, a.L + ((int64_t)it.tb * kDT + lane) + (c0 + cc) * a.ldl);
+                cp_async8(stg + cc * kLdR + lane, a.L + ((int64_t)it.tb * kDT + lane) + (c0 + cc) * a.ldl);
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
             if (fast_tile(it.tb, s)) {  // tiles next to the hand-off: the compute warps poll pfast themselves
                 if (lane == 0) mbar_arrive(full + slot);
@@ -665,7 +712,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 const unsigned bytes = (unsigned)(kDT * k) * 8u;
                 mbar_arrive_expect_tx(full + slot, bytes);
-                bulk_g2s(stg + kDT * kLdT, a.pfast + (int64_t)it.tb * kDT * k, bytes, full + slot);
+                bulk_g2s(stg + kDT * kLdR, a.pfast + (int64_t)it.tb * kDT * k, bytes, full + slot);
             }
         }
         cp_async_wait_all();
@@ -690,7 +737,7 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
         const int ii = pit.ii;
         const int s = h + ii * H;
         const double *Lt = ring + slot * kSlot;
-        const double *Pt = Lt + kDT * kLdT;
+        const double *Pt = Lt + kDT * kLdR;
         const int64_t c0 = (int64_t)s * kDT;
         const int nc = (int)imin64(kDT, a.n - c0);
         double *r = rptr(ii, s);
@@ -752,75 +799,119 @@ __device__ unsigned long long *trsv_helper(const TrsvArgs &a, double *smem, int 
             if (t == 0 && chain_handoff) HTRACE(3, 3000 + s);
         }
         HPT(2, clock64());
-        constexpr int EG = KB / 2;
-        constexpr int kGemmT = 16 * EG;
-        static_assert(kGemmT <= kHelpCompute, "helper GEMM threads");
-        if (t < kGemmT) {
-            const int cq = t / EG, eg = t % EG;
-            const int ca = 2 * cq, e = 2 * eg;
-            // four interleaved partial sums per output: FMA chains 8 deep, not 32
-            double acc[4][4];
+        if constexpr (KB >= 8) {
+            // r[c][e] -= sum_m L(m, c) P[m][e] on the FP64 tensor cores (DMMA m8n8k4: M = strip
+            // columns, N = update columns, K = rows; warp = 8 columns x 8 * TPW update columns):
+            // 8 dependent MMAs per output tile instead of ~32 DFMA rounds on shared loads
+            constexpr int ET = KB / 8, TPW = ET >= 2 ? ET / 2 : 1;
+            const int cw = warp % 4, eg = warp / 4;
+            if (eg * TPW < ET) {
+                const int gi = lane >> 2, tg = lane & 3;
+                const int c = cw * 8 + gi;
+                double acc[TPW][2];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+                for (int v = 0; v < TPW; ++v) acc[v][0] = acc[v][1] = 0.0;
+                const double *la = Lt + c * kLdR + tg;
 #pragma unroll
-                for (int o = 0; o < 4; ++o) acc[q][o] = 0.0;
-            if (e < k) {
-                const double *La = Lt + ca * kLdT, *Lb2 = La + kLdT;
-                if ((k & 1) == 0) {
+                for (int m0 = 0; m0 < kDT; m0 += 4) {
+                    const double af = la[m0];
 #pragma unroll
-                    for (int m = 0; m < kDT; ++m) {
-                        const double2 pv = *reinterpret_cast<const double2 *>(Pt + m * k + e);
-                        const double la = La[m], lb = Lb2[m];
-                        acc[m & 3][0] = fma(la, pv.x, acc[m & 3][0]);
-                        acc[m & 3][1] = fma(la, pv.y, acc[m & 3][1]);
-                        acc[m & 3][2] = fma(lb, pv.x, acc[m & 3][2]);
-                        acc[m & 3][3] = fma(lb, pv.y, acc[m & 3][3]);
-                    }
-                } else {
-                    const bool e1 = e + 1 < k;
-#pragma unroll
-                    for (int m = 0; m < kDT; ++m) {
-                        const double p0 = Pt[m * k + e], p1 = e1 ? Pt[m * k + e + 1] : 0.0;
-                        const double la = La[m], lb = Lb2[m];
-                        acc[m & 3][0] = fma(la, p0, acc[m & 3][0]);
-                        acc[m & 3][1] = fma(la, p1, acc[m & 3][1]);
-                        acc[m & 3][2] = fma(lb, p0, acc[m & 3][2]);
-                        acc[m & 3][3] = fma(lb, p1, acc[m & 3][3]);
+                    for (int v = 0; v < TPW; ++v) {
+                        const int e = (eg * TPW + v) * 8 + gi;
+                        dmma_884(acc[v], af, e < k ? Pt[(m0 + tg) * k + e] : 0.0);
                     }
                 }
-            }
-            const double s00 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
-            const double s01 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
-            const double s10 = (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]);
-            const double s11 = (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]);
-            const double sv[2][2] = {{s00, s01}, {s10, s11}};
-            HPT(3, clock64());
-            if (t == 0 && chain_handoff) HTRACE(4, 3000 + s);
-            double vout[2][2];
+                HPT(3, clock64());
+                if (t == 0 && chain_handoff) HTRACE(4, 3000 + s);
+                double *ck = checkpoint ? a.chk + (chk_count_before_pow2(s64, a.CIlog) + (b64 >> a.CIlog)) * kD * k +
+                                              ((s % 2) * kDT + c) * k
+                                        : nullptr;
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
+                for (int v = 0; v < TPW; ++v)
 #pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const int c = ca + i, ee = e + j;
-                    double v = 0.0;
-                    if (c < nc && ee < k) {
-                        double *rr = r + c * ld + ee;
-                        *rr = v = *rr - sv[i][j];
-                        if (chain_handoff) st_handoff(a.rchain + c0 * k + (int64_t)c * k + ee, v);
-                        if (chain_handoff && t == 0 && i == 0 && j == 0) HTRACE(5, 3000 + s);
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int ee = (eg * TPW + v) * 8 + 2 * tg + hh;
+                        if (c < nc && ee < k) {
+                            double *rr = r + c * ld + ee;
+                            const double nv = *rr - acc[v][hh];
+                            *rr = nv;
+                            if (chain_handoff) st_handoff(a.rchain + c0 * k + (int64_t)c * k + ee, nv);
+                            if (chain_handoff && t == 0 && v == 0 && hh == 0) HTRACE(5, 3000 + s);
+                            if (ck) ck[ee] = nv;  // the chain does not wait for these
+                        }
                     }
-                    vout[i][j] = v;
-                }
             }
-            if (checkpoint) {  // the chain does not wait for these
-#pragma unroll
+        } else {
+            constexpr int EG = KB / 2;
+            constexpr int kGemmT = 16 * EG;
+            static_assert(kGemmT <= kHelpCompute, "helper GEMM threads");
+            if (t < kGemmT) {
+                const int cq = t / EG, eg = t % EG;
+                const int ca = 2 * cq, e = 2 * eg;
+                // four interleaved partial sums per output: FMA chains 8 deep, not 32
+                double acc[4][4];
+    #pragma unroll
+                for (int q = 0; q < 4; ++q)
+    #pragma unroll
+                    for (int o = 0; o < 4; ++o) acc[q][o] = 0.0;
+                if (e < k) {
+                    const double *La = Lt + ca * kLdR, *Lb2 = La + kLdR;
+                    if ((k & 1) == 0) {
+    #pragma unroll
+                        for (int m = 0; m < kDT; ++m) {
+                            const double2 pv = *reinterpret_cast<const double2 *>(Pt + m * k + e);
+                            const double la = La[m], lb = Lb2[m];
+                            acc[m & 3][0] = fma(la, pv.x, acc[m & 3][0]);
+                            acc[m & 3][1] = fma(la, pv.y, acc[m & 3][1]);
+                            acc[m & 3][2] = fma(lb, pv.x, acc[m & 3][2]);
+                            acc[m & 3][3] = fma(lb, pv.y, acc[m & 3][3]);
+                        }
+                    } else {
+                        const bool e1 = e + 1 < k;
+    #pragma unroll
+                        for (int m = 0; m < kDT; ++m) {
+                            const double p0 = Pt[m * k + e], p1 = e1 ? Pt[m * k + e + 1] : 0.0;
+                            const double la = La[m], lb = Lb2[m];
+                            acc[m & 3][0] = fma(la, p0, acc[m & 3][0]);
+                            acc[m & 3][1] = fma(la, p1, acc[m & 3][1]);
+                            acc[m & 3][2] = fma(lb, p0, acc[m & 3][2]);
+                            acc[m & 3][3] = fma(lb, p1, acc[m & 3][3]);
+                        }
+                    }
+                }
+                const double s00 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+                const double s01 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+                const double s10 = (acc[0][2] + acc[1][2]) + (acc[2][2] + acc[3][2]);
+                const double s11 = (acc[0][3] + acc[1][3]) + (acc[2][3] + acc[3][3]);
+                const double sv[2][2] = {{s00, s01}, {s10, s11}};
+                HPT(3, clock64());
+                if (t == 0 && chain_handoff) HTRACE(4, 3000 + s);
+                double vout[2][2];
+    #pragma unroll
                 for (int i = 0; i < 2; ++i) {
-                    const int c = ca + i;
-                    double *ck = a.chk + (chk_count_before_pow2(s64, a.CIlog) + (b64 >> a.CIlog)) * kD * k +
-                                 ((s % 2) * kDT + c) * k;
-#pragma unroll
-                    for (int j = 0; j < 2; ++j)
-                        if (c < nc && e + j < k) ck[e + j] = vout[i][j];
+    #pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int c = ca + i, ee = e + j;
+                        double v = 0.0;
+                        if (c < nc && ee < k) {
+                            double *rr = r + c * ld + ee;
+                            *rr = v = *rr - sv[i][j];
+                            if (chain_handoff) st_handoff(a.rchain + c0 * k + (int64_t)c * k + ee, v);
+                            if (chain_handoff && t == 0 && i == 0 && j == 0) HTRACE(5, 3000 + s);
+                        }
+                        vout[i][j] = v;
+                    }
+                }
+                if (checkpoint) {  // the chain does not wait for these
+    #pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int c = ca + i;
+                        double *ck = a.chk + (chk_count_before_pow2(s64, a.CIlog) + (b64 >> a.CIlog)) * kD * k +
+                                     ((s % 2) * kDT + c) * k;
+    #pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            if (c < nc && e + j < k) ck[e + j] = vout[i][j];
+                    }
                 }
             }
         }
@@ -1155,6 +1246,7 @@ __global__ void __launch_bounds__(kT2Threads, 2) btma_kernel(const __grid_consta
     }
     extern __shared__ __align__(16) unsigned char smem_t2[];
     btma_body<KB>(tm, n, k, chk, Ui, panels, NB, blockIdx.x, s0, smem_t2, 0);
+    if (threadIdx.x == 0) TLINE(4);
 }
 
 // ---------------------------------------------------------------- worker mode
@@ -1222,6 +1314,7 @@ __global__ void __launch_bounds__(kTrsvThreads, 1) trsv_kernel(const __grid_cons
     // every CTA is resident (cooperative launch): the Apply grid may be scheduled onto SMs
     // as our CTAs exit (programmatic dependent launch); it waits on our flags, not on us
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x == 0 && blockIdx.x == 0) TLINE(0);
     if ((int)blockIdx.x < a.NC)
         trsv_chain(a, smem_trsv, blockIdx.x);
     else if ((int)blockIdx.x == a.NC) {
@@ -1294,7 +1387,7 @@ gcm_status_t blocked_pass(double *L, int64_t n, int64_t ldl, double *V, int k, i
     if (st != GCM_OK) return st;
     const size_t smem_chain = (size_t)ChainSmem::total * sizeof(double);
     const size_t smem_help = (size_t)(kDT * kLdT + kDT * std::max(KB, kLdT) + help_max_own(KB) * kDT * KB +
-                                      kHelpRing * (kDT * kLdT + kDT * (KB + 1)) + 3 * kHelpRing) *
+                                      kHelpRing * (kDT * kLdR + kDT * (KB + 1)) + 3 * kHelpRing) *
                              sizeof(double);
     const size_t smem_diag = (size_t)bdiag_smem_doubles(KB) * sizeof(double);
     size_t smem = std::max(std::max(smem_chain, smem_help), smem_diag);

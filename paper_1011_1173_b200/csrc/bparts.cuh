@@ -280,6 +280,14 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
     }
 }
 
+// One FP64 tensor-core step (DMMA, mma.sync m8n8k4 .f64): c(8x8) += a(8x4) b(4x8), lane l
+// holding a[l/4][l%4], b[l%4][l/4] and c[l/4][2(l%4) .. 2(l%4)+1] (PTX ISA fragment layout).
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+
 // CI == 1 Apply through TMA (L 16-byte aligned, ldl even): one CTA of 128 threads per
 // (row block b, 2C column strips = 128*C columns); thread t owns columns t + 128q
 // (q < C, C = 4 for KB <= 16, else 2), so each broadcast (gamma, delta) load feeds 2C

@@ -429,11 +429,6 @@ template <int KB>
 size_t pupdate_mma_smem() {
     return (size_t)(2 * kD * PmShape<KB>::LDC + 2 * kD * PmShape<KB>::LDP) * 8;
 }
-__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-        : "+d"(c[0]), "+d"(c[1])
-        : "d"(a), "d"(b));
-}
 template <int KB>
 __global__ void __launch_bounds__(kPT, 2) pupdate_mma_kernel(const double *__restrict__ L, int64_t ldl, int64_t n,
                                                             int64_t nloc, int k, int64_t row0, int nrows,

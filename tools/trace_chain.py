@@ -77,3 +77,17 @@ if hasattr(lib, "gcm_debug_dtrace") and lib.gcm_debug_dtrace(db, 256 * 8) == 0:
     print("diagonal sweep phases (us, median over blocks): loads+P polled / w+U^-1 / V,q / closed rows / triangle")
     ph = [np.median(dt[ok, i + 1] - dt[ok, i]) / 1e3 for i in range(5)]
     print("  " + "  ".join(f"{x:.1f}" for x in ph))
+
+# kernel timeline (TLINE): us after trsv entry, max over CTAs
+tl = hall[2000]
+if tl[0] > 0:
+    names = ["trsv entry", "J1 done (last helper)", "chain start (CTA 0)", "chain end (last CTA)", "btma end (last CTA)"]
+    sw = hall[1000:1000 + NB]
+    print("kernel timeline (us after trsv entry):")
+    for i, nm in enumerate(names):
+        print(f"  {nm:24s} {(tl[i] - tl[0]) / 1e3:8.1f}")
+    print(f"  last sweep done          {(sw[:, 2].max() - tl[0]) / 1e3:8.1f}")
+jm = hall[2001]
+if jm[0] > 0:
+    print("J1 of helper 0, block 0 (us after trsv entry): start / Lb+X loads / X / tiles+segment / M,N / published")
+    print("  " + " ".join(f"{(x - tl[0]) / 1e3:.1f}" for x in jm[:5]))
