@@ -451,18 +451,10 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_mma_kernel(const double *__res
     const int ke = k - eb;  // update columns of this CTA that exist
     // 16-byte copies need 16-byte aligned columns (an even ldl and an aligned L)
     const bool v16 = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0);
+    // P rows by 16-byte copies when every (row, column pair) is 16-byte aligned
+    const bool p16 = (k % 2 == 0) && (eb % 2 == 0) && ((reinterpret_cast<uintptr_t>(P) & 15) == 0);
     if (flag) wait_flag_sys(flag, epoch);
     double *rs = res + (int64_t)sl * kD * k + eb;
-    double acc[TC][TE][2];
-#pragma unroll
-    for (int u = 0; u < TC; ++u)
-#pragma unroll
-        for (int v = 0; v < TE; ++v)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int c = cw + 8 * u + gi, e = ew + 8 * v + 2 * tg + h;
-                acc[u][v][h] = (c < nc && e < ke) ? -rs[c * k + e] : 0.0;
-            }
     auto issue = [&](int a) {
         const int64_t r0 = row0 + (int64_t)a * kD;
         const int Da = (int)imin64(kD, n - r0);
@@ -485,16 +477,37 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_mma_kernel(const double *__res
                              : "memory");
             }
         }
-        for (int idx = t; idx < kD * KB; idx += kPT) {
-            const int m = idx / KB, e = idx % KB;
-            const bool ok = m < Da && e < ke;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(ps + m * LDP + e)),
-                         "l"(ok ? P + (r0 + m) * k + eb + e : P), "r"(ok ? 8 : 0)
-                         : "memory");
+        if (p16) {
+            for (int idx = t; idx < kD * KB / 2; idx += kPT) {
+                const int m = idx / (KB / 2), e = 2 * (idx % (KB / 2));
+                const int bytes = (m < Da && e < ke) ? (ke - e >= 2 ? 16 : 8) : 0;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(ps + m * LDP + e)),
+                             "l"(bytes ? P + (r0 + m) * k + eb + e : P), "r"(bytes)
+                             : "memory");
+            }
+        } else {
+            for (int idx = t; idx < kD * KB; idx += kPT) {
+                const int m = idx / KB, e = idx % KB;
+                const bool ok = m < Da && e < ke;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(ps + m * LDP + e)),
+                             "l"(ok ? P + (r0 + m) * k + eb + e : P), "r"(ok ? 8 : 0)
+                             : "memory");
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    issue(0);
+    issue(0);  // before the residual loads: their first use would stall the issue of the copies
+    const int64_t ckbase = chkoff[sl];
+    double acc[TC][TE][2];
+#pragma unroll
+    for (int u = 0; u < TC; ++u)
+#pragma unroll
+        for (int v = 0; v < TE; ++v)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = cw + 8 * u + gi, e = ew + 8 * v + 2 * tg + h;
+                acc[u][v][h] = (c < nc && e < ke) ? -rs[c * k + e] : 0.0;
+            }
     for (int a = 0; a < na; ++a) {
         const int64_t r0 = row0 + (int64_t)a * kD;
         if (a + 1 < na) {
@@ -505,7 +518,7 @@ __global__ void __launch_bounds__(kPT, 2) pupdate_mma_kernel(const double *__res
         }
         __syncthreads();
         {
-            double *ck = chk + (chkoff[sl] + r0 / kD) * kD * k + eb;
+            double *ck = chk + (ckbase + r0 / kD) * kD * k + eb;
 #pragma unroll
             for (int u = 0; u < TC; ++u)
 #pragma unroll

@@ -1,0 +1,5 @@
+out=gpurun_out/r02au; mkdir -p $out
+timeout 900 python -m pytest tests/test_gpu_dist.py -q -x 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge.py -q -x -k panel 2>&1 | tail -1
+python tools/panel_trace.py 100000 32 2>&1 | tail -1
+python tools/panel_trace.py 100000 16 2>&1 | tail -1
