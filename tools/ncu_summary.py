@@ -26,15 +26,37 @@ SCALE = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "mse
 
 
 def family(name):
-    for f in ("trsv", "btma", "btile", "bapply", "bdiag", "batched", "diag_chain", "panel_apply"):
+    for f in ("trsv", "btma", "btile", "bapply", "bdiag", "batched", "diag_chain", "panel_apply", "papply", "pupdate",
+              "dsolve", "pinv", "pdiag", "ptile"):
         if f in name:
             return "bapply" if f in ("btma", "btile") else f
     return None
 
 
+def from_long_csv(path):
+    """An `ncu --csv --log-file` capture (one row per metric, e.g. application replay) as the
+    wide (header, units, rows) form of `--page raw --csv`."""
+    lines = [ln for ln in open(path) if ln.startswith('"')]
+    rows = list(csv.reader(lines))
+    h = rows[0]
+    ki, mi, ui, vi, ii = (h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Unit"),
+                          h.index("Metric Value"), h.index("ID"))
+    per, units = {}, {}
+    for r in rows[1:]:
+        d = per.setdefault(r[ii], {"Kernel Name": r[ki]})
+        d[r[mi]] = r[vi]
+        units[r[mi]] = r[ui]
+    hdr = ["Kernel Name"] + sorted(units)
+    return hdr, [""] + [units[m] for m in hdr[1:]], [[d.get(c, "") for c in hdr] for d in per.values()]
+
+
 def main(rep, out, note):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
+    if rep.endswith(".csv"):
+        hdr, units, body = from_long_csv(rep)
+        rows = [hdr, units] + body
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     res = {}
     for r in rows[2:]:
