@@ -158,11 +158,11 @@ gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     if (env && std::strcmp(env, "panel") == 0) return GCM_ALGO_PANEL;
     (void)k;
     // the chain-shortened path wins once there is more
-    // than a handful of row blocks; tiny factors keep the two-kernel sweep; very large
-    // factors take the column-block (panel) algorithm, whose residual updates are plain
-    // block GEMMs instead of the blocked path's per-strip helpers (n = 1e5, k = 32:
-    // 107 vs 131 ms, profiles/r02t_*).
-    if (n >= 50000) return GCM_ALGO_PANEL;
+    // than a handful of row blocks; tiny factors keep the two-kernel sweep; large factors
+    // take the column-block (panel) algorithm, whose residual updates run on the FP64 tensor
+    // cores (n = 20000, k = 32: 4.0 vs 5.0 ms; n = 40000: 12.3 vs 18.1 ms; at n = 12000 the two
+    // are level, profiles/r02bg_crossover.txt).
+    if (n >= 16000) return GCM_ALGO_PANEL;
     return n >= 256 ? GCM_ALGO_BLOCKED : GCM_ALGO_SWEEP;
 }
 

@@ -160,7 +160,7 @@ Plan make_plan(int64_t n, int64_t nb, int R, int r, int k, bool tma_groups) {
 
 // workspace carve-up of one rank (byte offsets)
 struct Carve {
-    size_t P, res, chk, Winv, Q, G, U, panels, key, flags, ctr, gstrip, chkoff, dlb, dllc, full, tiles, total;
+    size_t P, res, chk, Winv, Q, G, U, panels, key, flags, ctr, sflag, gstrip, chkoff, dlb, dllc, full, tiles, total;
 };
 Carve carve(const Plan &p) {
     Carve c{};
@@ -182,6 +182,7 @@ Carve carve(const Plan &p) {
     c.key = take(8);
     c.flags = take((size_t)(p.NSB + 1) * 4);
     c.ctr = take(16);
+    c.sflag = take((size_t)p.NB64 * kD * p.k * 8);  // persistent chain: strip hand-offs (self-validating)
     c.gstrip = take((size_t)std::max(p.nsl, 1) * 4);
     c.chkoff = take((size_t)std::max(p.nsl, 1) * 8);
     c.dlb = take((size_t)std::max<size_t>(p.dl_b.size(), 1) * 4);
@@ -718,6 +719,316 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
     }
 }
 
+// ------------------------------------------------------------------ persistent chain (one rank)
+// GCM_ALGO_PANEL with one rank replaces the per-solve-block launches (dsolve, lookahead and
+// rest pupdate) by ONE cooperative kernel working in 64-row steps:
+//   CTA 0 (solver), step b:  r_b = the hand-off of strip b (its residual after P_{<= b-2}, from
+//     its helper; V itself for b < 2) = the checkpoint of tile (b-1, b), minus L_{b-1,b}^T q_{b-1}
+//     (its own one-block lookahead), then q_b = W_b^T r_b (W_b = L_bb^{-1}, pinv_kernel) -- both
+//     on DMMA -- published as P's rows; W_{b+1} and L_{b,b+1} are copied under the product;
+//   CTAs 1.. (helpers): strip s >= 2 belongs to helper (s - 2) mod H; tiles (b, s), b <= s - 2,
+//     in b-major order: poll P_b, checkpoint, r_s -= L_{b,s}^T P_b (DMMA), and after b = s - 2
+//     hand r_s to the solver.  The strip's L tile is staged before the poll; residuals of the
+//     first OWN owned strips stay in shared memory between tiles (the rest round-trip res[]).
+// P and the hand-offs are self-validating values (st_value / ld_value: the pass arms both with
+// all-ones), so a consumer needs one L2 round trip and no flag.  No CTA waits on a later one
+// (the solver on hand-offs of earlier tiles, helpers on P blocks the solver publishes without
+// waiting for them), so the cooperative grid cannot deadlock.
+constexpr int kPcT = 512;
+#ifdef GCM_PC_TRACE  // solver step timeline (globaltimer ns): tools/pchain_trace.py
+__device__ long long g_pc_trace[4096 * 4];
+__device__ __forceinline__ long long pc_now() {
+    long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
+#define PC_MARK(b, slot) \
+    do {                 \
+        if (t == 0 && (b) < 4096) g_pc_trace[(b) * 4 + (slot)] = pc_now(); \
+    } while (0)
+#else
+#define PC_MARK(b, slot) ((void)0)
+#endif
+template <int KB>
+struct PcShape {
+    static constexpr int NE = KB >= 8 ? KB : 8;
+    static constexpr int LDR = NE + 4;
+    static constexpr int LDW = kD + 4;
+    static constexpr int ET = NE / 8;
+    static constexpr int TPW = (8 * ET + 15) / 16;
+    static constexpr int OWN = KB >= 32 ? 5 : 10;  // helper strips whose residual stays in shared memory
+    static constexpr size_t solver_doubles = 2 * kD * LDW + 3 * kD * LDR;
+    static constexpr size_t helper_doubles = 2 * kD * LDW + kD * LDR + (OWN + 2) * kD * LDR;  // + spill slots
+    static constexpr size_t doubles = solver_doubles > helper_doubles ? solver_doubles : helper_doubles;
+};
+template <int KB>
+size_t pchain_smem() {
+    return PcShape<KB>::doubles * 8;
+}
+// self-validating values (the pass arms P and the hand-off buffer with all-ones, a NaN pattern no
+// producer stores: NaNs are canonicalised): a consumer polls the value itself -- one L2 round
+// trip, no flag, no fence
+__device__ __forceinline__ void st_value(double *p, double v) {
+    chaos_delay();
+    const double w = v == v ? v : __longlong_as_double(0x7ff8000000000000ll);
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(w) : "memory");
+}
+template <int KB>
+__global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restrict__ L, int64_t ldl, int64_t n, int k,
+                                                        int NB, double *res, double *chk, const int64_t *chkoff,
+                                                        const double *__restrict__ Winv, double *P, double *hand) {
+    using S = PcShape<KB>;
+    constexpr int NE = S::NE, LDR = S::LDR, LDW = S::LDW, ET = S::ET, TPW = S::TPW;
+    extern __shared__ __align__(16) double sm_pc[];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gi = lane >> 2, tg = lane & 3;
+    const bool v16 = (ldl % 2 == 0) && ((reinterpret_cast<uintptr_t>(L) & 15) == 0);
+    // the warp's output tiles: strip columns c = ct*8 + gi, update columns e = (eg*TPW + v)*8 + 2tg + h
+    const int ct = warp % 8, eg = warp / 8;
+    const bool mma_warp = eg * TPW < ET;
+    const int c = ct * 8 + gi;
+    auto ecol = [&](int v, int h) { return (eg * TPW + v) * 8 + 2 * tg + h; };
+    // L(rows of block rb, columns of block cb) -> dst[c][m] (column-major, stride LDW), zero outside
+    auto load_tile = [&](double *dst, int rb, int cb) {
+        const int64_t r0 = (int64_t)rb * kD, c0 = (int64_t)cb * kD;
+        const int Dr = (int)imin64(kD, n - r0), Dc = (int)imin64(kD, n - c0);
+        if (v16) {
+            for (int idx = t; idx < kD * kD / 2; idx += kPcT) {
+                const int cc = idx >> 5, m = 2 * (idx & 31);
+                const int bytes = (cc < Dc && m < Dr) ? (Dr - m >= 2 ? 16 : 8) : 0;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + cc * LDW + m)),
+                             "l"(bytes ? L + (r0 + m) + (c0 + cc) * ldl : L), "r"(bytes)
+                             : "memory");
+            }
+        } else {
+            for (int idx = t; idx < kD * kD; idx += kPcT) {
+                const int cc = idx >> 6, m = idx & 63;
+                cp8(dst + cc * LDW + m, L + (r0 + m) + (c0 + cc) * ldl, cc < Dc && m < Dr);
+            }
+        }
+    };
+    // rows [0, nrows) x k of a row-major (ld k) global block -> dst[m][LDR], zero outside
+    auto load_rows = [&](double *dst, const double *src, int nrows) {
+        for (int o = t; o < kD * NE; o += kPcT) {
+            const int m = o / NE, e = o % NE;
+            cp8(dst + m * LDR + e, src + (int64_t)m * k + e, m < nrows && e < k);
+        }
+    };
+    // acc += A^T B: A = tile dst[c][m] (stride LDW), B = rows [m][LDR]; K = 64
+    auto mma_tile = [&](double (&acc)[TPW][2], const double *A, const double *B) {
+        const double *la = A + c * LDW + tg;
+        const double *qb = B + tg * LDR + eg * TPW * 8 + gi;
+#pragma unroll 4
+        for (int m0 = 0; m0 < kD; m0 += 4) {
+            const double af = la[m0];
+#pragma unroll
+            for (int v = 0; v < TPW; ++v) dmma_884(acc[v], af, qb[m0 * LDR + v * 8]);
+        }
+    };
+
+    if (blockIdx.x == 0) {
+        // ------------------------------------------------------------ solver
+        double *Ws = sm_pc;                 // [kD][LDW]
+        double *Lt1 = Ws + kD * LDW;        // L_{b-1,b}
+        double *qh = Lt1 + kD * LDW;        // [2][kD][LDR]: q_b at b % 2
+        double *rb = qh + 2 * kD * LDR;     // [kD][LDR]
+        auto load_w = [&](int b) {
+            const double *src = Winv + (int64_t)b * kD * kD;
+            for (int idx = t; idx < kD * kD / 2; idx += kPcT) {
+                const int j = idx >> 5, m = 2 * (idx & 31);
+                cp16(Ws + j * LDW + m, src + j * kD + m);
+            }
+        };
+        load_w(0);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        for (int b = 0; b < NB; ++b) {
+            const int64_t r0 = (int64_t)b * kD;
+            const int Db = (int)imin64(kD, n - r0);
+            // W_b and this step's lookahead tiles were issued during step b - 1
+            PC_MARK(b, 0);
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();
+            PC_MARK(b, 1);
+            if (mma_warp) {
+                // r_b: V for b < 2, else strip b's hand-off (its residual after P_{<= b-2};
+                // self-validating, polled per value) = the checkpoint of tile (b - 1, b)
+                double r[TPW][2];
+                const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)c * k;
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int e = ecol(v, h);
+                        r[v][h] = (c < Db && e < k) ? (b < 2 ? src[e] : ld_value(src + e)) : 0.0;
+                    }
+                double acc[TPW][2];
+                double *ck1 = b >= 1 ? chk + (chkoff[b] + b - 1) * kD * k + (int64_t)c * k : nullptr;
+                PC_MARK(b, 2);
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int e = ecol(v, h);
+                        acc[v][h] = -r[v][h];
+                        if (ck1 && c < Db && e < k) ck1[e] = r[v][h];
+                    }
+                if (b >= 1) mma_tile(acc, Lt1, qh + ((b - 1) % 2) * kD * LDR);
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) rb[c * LDR + ecol(v, h)] = -acc[v][h];  // r^{(b)}
+            }
+            __syncthreads();
+            if (b + 1 < NB) {  // the next step's lookahead tile, under this step's product and publish
+                load_tile(Lt1, b, b + 1);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+            // q_b = W^T r^{(b)} (dsolve's product: DMMA above the 8-row diagonal tiles, masked
+            // DFMA on them, so a product 0 * r_j with j > m is never formed)
+            double *qv = qh + (b % 2) * kD * LDR;
+            if (mma_warp) {
+                const int m0 = ct * 8;
+                double acc[TPW][2];
+#pragma unroll
+                for (int v = 0; v < TPW; ++v) acc[v][0] = acc[v][1] = 0.0;
+                for (int j0 = 0; j0 < m0; j0 += 4) {
+                    const double af = Ws[(j0 + tg) * LDW + m0 + gi];
+#pragma unroll
+                    for (int v = 0; v < TPW; ++v) dmma_884(acc[v], af, rb[(j0 + tg) * LDR + (eg * TPW + v) * 8 + gi]);
+                }
+                const int m = m0 + gi;
+                double wd[8];  // W(m0 .. m0+7, m): loaded up front, the FMA chain then runs on registers
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) wd[jj] = Ws[(m0 + jj) * LDW + m];
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int e = ecol(v, h);
+                        double rd[8];
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) rd[jj] = rb[(m0 + jj) * LDR + e];
+                        double s = acc[v][h];
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj)
+                            if (jj <= gi) s = fma(wd[jj], rd[jj], s);  // j <= m only
+                        s = m < Db ? s : 0.0;  // rows past the block stay zero
+                        qv[m * LDR + e] = s;
+                        if (m < Db && e < k) st_value(P + (r0 + m) * k + e, s);  // published
+                    }
+            }
+            __syncthreads();  // Ws, rb free
+            PC_MARK(b, 3);
+            if (b + 1 < NB) {
+                load_w(b + 1);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+        }
+        return;
+    }
+    // ---------------------------------------------------------------- helpers
+    const int h = blockIdx.x - 1, H = gridDim.x - 1;
+    double *Lh = sm_pc;                 // [2][kD][LDW]: this tile and the next
+    double *Ph = Lh + 2 * kD * LDW;     // [kD][LDR]
+    double *Rs = Ph + kD * LDR;         // [OWN + 2][kD][LDR]: residuals of the first OWN owned strips,
+                                        //   then one spill slot per tile buffer
+    int nown = 0;
+    for (int s = 2 + h; s < NB; s += H) ++nown;
+    if (nown == 0) return;
+    auto rload = [&](double *dst, int s) {
+        load_rows(dst, res + (int64_t)s * kD * k, (int)imin64(kD, n - (int64_t)s * kD));
+    };
+    for (int i = 0; i < nown && i < S::OWN; ++i) rload(Rs + i * kD * LDR, 2 + h + i * H);
+    // tiles (b, strip #i) in b-major order, b <= s_i - 2; the next tile's copies fly under this one
+    struct It {
+        int b, i;
+    };
+    const int last_b = 2 + h + (nown - 1) * H - 2;  // the last tile row any owned strip needs
+    auto imin = [&](int b) { return b <= h ? 0 : (b - h + H - 1) / H; };
+    auto valid = [&](const It &x) { return x.b <= last_b && x.i < nown; };
+    auto adv = [&](It &x) {
+        if (++x.i >= nown) {
+            ++x.b;
+            x.i = imin(x.b);
+        }
+    };
+    // (a spilled residual is copied with its tile unless the tile just before is the same strip's:
+    // that tile's result is not stored yet, it hands its registers over instead)
+    auto stage = [&](const It &x, int buf, bool same_strip) {
+        const int s = 2 + h + x.i * H;
+        load_tile(Lh + buf * kD * LDW, x.b, s);
+        if (x.i >= S::OWN && !same_strip) rload(Rs + (S::OWN + buf) * kD * LDR, s);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    It cur{0, 0};
+    stage(cur, 0, false);  // (the residual slots' copies are in this first group)
+    int buf = 0, pb = -1;
+    while (valid(cur)) {
+        It nx = cur;
+        adv(nx);
+        const bool chained = valid(nx) && nx.i == cur.i;
+        if (valid(nx)) stage(nx, buf ^ 1, chained);
+        const int b = cur.b, i = cur.i, s = 2 + h + i * H;
+        const int64_t r0 = (int64_t)b * kD;
+        const int Db = (int)imin64(kD, n - r0);
+        if (b != pb) {  // P_b, polled per value (every load in flight before the first wait)
+            constexpr int PPT = (kD * NE + kPcT - 1) / kPcT;
+            unsigned long long u[PPT];
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+                const int o = t + q * kPcT, m = o / NE, e = o % NE;
+                u[q] = (o < kD * NE && m < Db && e < k) ? ld_relaxed_u64(P + (r0 + m) * k + e) : 0ull;
+            }
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+                const int o = t + q * kPcT, m = o / NE, e = o % NE;
+                if (o < kD * NE) {
+                    if (u[q] == kEmpty) u[q] = __double_as_longlong(ld_value(P + (r0 + m) * k + e));
+                    Ph[m * LDR + e] = __longlong_as_double((long long)u[q]);
+                }
+            }
+            pb = b;
+        }
+        if (valid(nx)) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        double *Rt = Rs + (i < S::OWN ? i : S::OWN + buf) * kD * LDR;
+        const int Dc = (int)imin64(kD, n - (int64_t)s * kD);
+        if (mma_warp) {
+            double acc[TPW][2];
+            double *ck = b >= 1 ? chk + (chkoff[s] + b) * kD * k + (int64_t)c * k : nullptr;
+#pragma unroll
+            for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int e = ecol(v, hh);
+                    const double r = Rt[c * LDR + e];
+                    acc[v][hh] = -r;
+                    if (ck && c < Dc && e < k) ck[e] = r;
+                }
+            mma_tile(acc, Lh + buf * kD * LDW, Ph);
+            const bool hoff = b == s - 2;
+            double *rg = res + (int64_t)s * kD * k + (int64_t)c * k;
+            double *hg = hand + (int64_t)s * kD * k + (int64_t)c * k;
+#pragma unroll
+            for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int e = ecol(v, hh);
+                    Rt[c * LDR + e] = -acc[v][hh];
+                    if (chained && i >= S::OWN) Rs[(S::OWN + (buf ^ 1)) * kD * LDR + c * LDR + e] = -acc[v][hh];
+                    if (c < Dc && e < k) {
+                        if (i >= S::OWN) rg[e] = -acc[v][hh];
+                        if (hoff) st_value(hg + e, -acc[v][hh]);  // strip s's hand-off to the solver
+                    }
+                }
+        }
+        __threadfence_block();  // spilled residuals: stores before a later tile's copies read them
+        __syncthreads();
+        cur = nx;
+        buf ^= 1;
+    }
+}
+
 // Q_b = P_b^T P_b per 64-row block (KB x KB, zero padded)
 template <int KB>
 __global__ void pgram_kernel(const double *__restrict__ P, int64_t n, int k, double *Q) {
@@ -965,6 +1276,50 @@ struct ChainTrace {
     }
 };
 
+// One rank: the persistent chain while each helper owns a few strips; at n ~ 1e5 (10+ strips per
+// helper) the per-solve-block launches, whose residual updates spread over every SM, are faster
+// (68.2 vs 71.9 ms; n = 40000: 14.1 vs 12.3 ms).  GCM_PCHAIN=0 / 1 forces either (A/B, tests).
+bool pchain_enabled(int NB64) {
+    const char *e = std::getenv("GCM_PCHAIN");
+    if (e) return e[0] != '0';
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        clear_stale_error();
+    return NB64 - 2 <= 6 * (nsm - 1);
+}
+template <int KB>
+gcm_status_t pchain_launch(Rank &q, int64_t n, int k, int NB64, cudaStream_t stream) {
+    double *hand = q.at<double>(q.cv.sflag);
+    // P and the hand-offs start all-ones: the "not yet written" pattern consumers poll for
+    gcm_status_t st = check_cuda(cudaMemsetAsync(hand, 0xff, (size_t)NB64 * kD * k * 8, stream));
+    if (st == GCM_OK) st = check_cuda(cudaMemsetAsync(q.Pbuf(), 0xff, (size_t)n * k * 8, stream));
+    if (st != GCM_OK) return st;
+    const size_t smem = pchain_smem<KB>();
+    st = check_cuda(cudaFuncSetAttribute(pchain_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (st != GCM_OK) return st;
+    int dev = 0, nsm = 0, per_sm = 0;
+    st = check_cuda(cudaGetDevice(&dev));
+    if (st == GCM_OK) st = check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (st == GCM_OK)
+        st = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pchain_kernel<KB>, kPcT, smem));
+    if (st != GCM_OK) return st;
+    if (per_sm < 1) return GCM_ECUDA;
+    // the solver + one helper per strip that needs hand-offs (strips 2 ..), at most one CTA per SM
+    int grid = (int)std::max(1, std::min(nsm * per_sm, 1 + std::max(0, NB64 - 2)));
+    // GCM_PCHAIN_GRID=<g> caps the grid (tests: few helpers own many strips -> the spill slots)
+    if (const char *e = std::getenv("GCM_PCHAIN_GRID")) grid = std::max(2, std::min(grid, std::atoi(e)));
+    const double *L = q.L;
+    int64_t ldl = q.ldl;
+    double *res = q.at<double>(q.cv.res), *chk = q.at<double>(q.cv.chk), *P = q.Pbuf();
+    const int64_t *chkoff = q.at<int64_t>(q.cv.chkoff);
+    const double *W = q.at<double>(q.cv.Winv);
+    void *args[] = {(void *)&L, &ldl, &n, &k, &NB64, &res, &chk, (void *)&chkoff, (void *)&W, &P, &hand};
+    st = check_cuda(cudaLaunchCooperativeKernel((const void *)pchain_kernel<KB>, dim3(grid), dim3(kPcT), args, smem,
+                                                stream));
+    count_launch();
+    return st;
+}
+
 // one pass (<= 32 update columns) over all ranks of `rk` (Virtual: all R; else rk has one entry)
 template <int KB>
 gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int k, int sigma, int64_t ebase,
@@ -1024,97 +1379,102 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                                                        q.at<double>(q.cv.Winv));
             count_launch();
         }
-        cudaStream_t aux = nullptr;
-        cudaEvent_t *p_ready = nullptr, *rest_done = nullptr;
-        st = aux_stream(&aux, &p_ready, &rest_done);
-        if (st != GCM_OK) return st;
-        st = check_cuda(cudaEventRecord(p_ready[1], stream));  // the aux stream starts after this call's prologue
-        if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(aux, p_ready[1], 0));
-        if (st != GCM_OK) return st;
-        const int64_t sb = rk[0].plan.sb;
-        const int NSB = rk[0].plan.NSB;
-        ChainTrace tr(NSB);
-        for (int g = 0; g < NSB; ++g) {  // solve blocks of sb rows (sb divides nb)
-            const int64_t row0 = (int64_t)g * sb;
-            tr.rec(g, 0, stream);
-            const int owner = (int)((row0 / nb) % R);
-            const int nrows = (int)std::min<int64_t>(sb, n - row0);
-            const int ol = x.mode == Mode::Virtual ? owner : (owner == x.self ? 0 : -1);
-            if (ol >= 0) {
-                Rank &q = rk[ol];
-                // owner's local strip of row0's column: local block (row0/nb)/R, offset row0 % nb
-                const int sl0 = (int)((((row0 / nb) / R) * nb + row0 % nb) / kD);
-                Peers p = peers_P(ol);
-                if (x.mode == Mode::Peer)
-                    for (int r = 0; r < R; ++r) p.flag[r] = x.peerFlag[r] + g;
-                dsolve_kernel<KB><<<1, kDsT, dsolve_smem<KB>(), stream>>>(
-                    q.L, q.ldl, n, k, row0, nrows, sl0, q.at<double>(q.cv.res), q.at<double>(q.cv.chk),
-                    q.at<int64_t>(q.cv.chkoff), q.at<double>(q.cv.Winv), p, epoch);
-                count_launch();
-            }
-#ifdef GCM_WITH_NCCL
-            if (x.mode == Mode::Nccl) {
-                double *Pg = rk[0].Pbuf() + row0 * k;
-                st = ncclBroadcast(Pg, Pg, (size_t)nrows * k, ncclDouble, owner, (ncclComm_t)x.nccl, stream) ==
-                             ncclSuccess
-                         ? GCM_OK
-                         : GCM_ENCCL;
-                if (st != GCM_OK) return st;
-            }
-#endif
-            // lookahead: the strips of the NEXT solve block first, on the call's stream (after the
-            // rest of block g-1, which touched the same residuals); the rest on the aux stream,
-            // where it overlaps the next diagonal solve
-            tr.rec(g, 1, stream);
-            if (g >= 1) {
-                st = check_cuda(cudaStreamWaitEvent(stream, rest_done[(g - 1) & 1], 0));
-                if (st != GCM_OK) return st;
-            }
-            for (int pass = 0; pass < 2; ++pass) {
-                cudaStream_t sp = pass == 0 ? stream : aux;
-                if (pass == 1) {
-                    tr.rec(g, 2, stream);
-                    st = check_cuda(cudaEventRecord(p_ready[g & 1], stream));
-                    if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(aux, p_ready[g & 1], 0));
-                    if (st != GCM_OK) return st;
-                }
-                for (int ri = 0; ri < nloc_ranks; ++ri) {
-                    Rank &q = rk[ri];
-                    const int slf = q.plan.first_strip_after[g];
-                    const int sla = g + 1 < NSB ? q.plan.first_strip_after[g + 1] : q.plan.nsl;
-                    const int s_lo = pass == 0 ? slf : sla, s_hi = pass == 0 ? sla : q.plan.nsl;
-                    if (s_lo >= s_hi) continue;
-                    const int rank_id = x.mode == Mode::Virtual ? ri : x.self;
-                    const unsigned *flag =
-                        (x.mode == Mode::Peer && rank_id != owner) ? x.peerFlag[x.self] + g : nullptr;
-                    if (pass == 0 && KB > 8 && pu_mma) {  // lookahead: the chain waits on it -- 8 update columns per CTA
-                        pupdate_mma_kernel<8><<<dim3(s_hi - s_lo, KB / 8), kPT, pupdate_mma_smem<8>(), sp>>>(
-                            q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
-                            q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
-                    } else if (pu_mma) {
-                        pupdate_mma_kernel<KBM><<<s_hi - s_lo, kPT, pupdate_mma_smem<KBM>(), sp>>>(
-                            q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
-                            q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
-                    } else if (pass == 0 && KB > 8) {
-                        pupdate_kernel<8><<<dim3(s_hi - s_lo, KB / 8), kPT, pupdate_smem<8>(), sp>>>(
-                            q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
-                            q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
-                    } else {
-                        pupdate_kernel<KB><<<s_hi - s_lo, kPT, pupdate_smem<KB>(), sp>>>(
-                            q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
-                            q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
-                    }
+        if (R == 1 && x.mode == Mode::Virtual && pchain_enabled(NB64)) {
+            st = pchain_launch<KB>(rk[0], n, k, NB64, stream);
+            if (st != GCM_OK) return st;
+        } else {
+            cudaStream_t aux = nullptr;
+            cudaEvent_t *p_ready = nullptr, *rest_done = nullptr;
+            st = aux_stream(&aux, &p_ready, &rest_done);
+            if (st != GCM_OK) return st;
+            st = check_cuda(cudaEventRecord(p_ready[1], stream));  // the aux stream starts after this call's prologue
+            if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(aux, p_ready[1], 0));
+            if (st != GCM_OK) return st;
+            const int64_t sb = rk[0].plan.sb;
+            const int NSB = rk[0].plan.NSB;
+            ChainTrace tr(NSB);
+            for (int g = 0; g < NSB; ++g) {  // solve blocks of sb rows (sb divides nb)
+                const int64_t row0 = (int64_t)g * sb;
+                tr.rec(g, 0, stream);
+                const int owner = (int)((row0 / nb) % R);
+                const int nrows = (int)std::min<int64_t>(sb, n - row0);
+                const int ol = x.mode == Mode::Virtual ? owner : (owner == x.self ? 0 : -1);
+                if (ol >= 0) {
+                    Rank &q = rk[ol];
+                    // owner's local strip of row0's column: local block (row0/nb)/R, offset row0 % nb
+                    const int sl0 = (int)((((row0 / nb) / R) * nb + row0 % nb) / kD);
+                    Peers p = peers_P(ol);
+                    if (x.mode == Mode::Peer)
+                        for (int r = 0; r < R; ++r) p.flag[r] = x.peerFlag[r] + g;
+                    dsolve_kernel<KB><<<1, kDsT, dsolve_smem<KB>(), stream>>>(
+                        q.L, q.ldl, n, k, row0, nrows, sl0, q.at<double>(q.cv.res), q.at<double>(q.cv.chk),
+                        q.at<int64_t>(q.cv.chkoff), q.at<double>(q.cv.Winv), p, epoch);
                     count_launch();
                 }
+    #ifdef GCM_WITH_NCCL
+                if (x.mode == Mode::Nccl) {
+                    double *Pg = rk[0].Pbuf() + row0 * k;
+                    st = ncclBroadcast(Pg, Pg, (size_t)nrows * k, ncclDouble, owner, (ncclComm_t)x.nccl, stream) ==
+                                 ncclSuccess
+                             ? GCM_OK
+                             : GCM_ENCCL;
+                    if (st != GCM_OK) return st;
+                }
+    #endif
+                // lookahead: the strips of the NEXT solve block first, on the call's stream (after the
+                // rest of block g-1, which touched the same residuals); the rest on the aux stream,
+                // where it overlaps the next diagonal solve
+                tr.rec(g, 1, stream);
+                if (g >= 1) {
+                    st = check_cuda(cudaStreamWaitEvent(stream, rest_done[(g - 1) & 1], 0));
+                    if (st != GCM_OK) return st;
+                }
+                for (int pass = 0; pass < 2; ++pass) {
+                    cudaStream_t sp = pass == 0 ? stream : aux;
+                    if (pass == 1) {
+                        tr.rec(g, 2, stream);
+                        st = check_cuda(cudaEventRecord(p_ready[g & 1], stream));
+                        if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(aux, p_ready[g & 1], 0));
+                        if (st != GCM_OK) return st;
+                    }
+                    for (int ri = 0; ri < nloc_ranks; ++ri) {
+                        Rank &q = rk[ri];
+                        const int slf = q.plan.first_strip_after[g];
+                        const int sla = g + 1 < NSB ? q.plan.first_strip_after[g + 1] : q.plan.nsl;
+                        const int s_lo = pass == 0 ? slf : sla, s_hi = pass == 0 ? sla : q.plan.nsl;
+                        if (s_lo >= s_hi) continue;
+                        const int rank_id = x.mode == Mode::Virtual ? ri : x.self;
+                        const unsigned *flag =
+                            (x.mode == Mode::Peer && rank_id != owner) ? x.peerFlag[x.self] + g : nullptr;
+                        if (pass == 0 && KB > 8 && pu_mma) {  // lookahead: the chain waits on it -- 8 update columns per CTA
+                            pupdate_mma_kernel<8><<<dim3(s_hi - s_lo, KB / 8), kPT, pupdate_mma_smem<8>(), sp>>>(
+                                q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                                q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                        } else if (pu_mma) {
+                            pupdate_mma_kernel<KBM><<<s_hi - s_lo, kPT, pupdate_mma_smem<KBM>(), sp>>>(
+                                q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                                q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                        } else if (pass == 0 && KB > 8) {
+                            pupdate_kernel<8><<<dim3(s_hi - s_lo, KB / 8), kPT, pupdate_smem<8>(), sp>>>(
+                                q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                                q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                        } else {
+                            pupdate_kernel<KB><<<s_hi - s_lo, kPT, pupdate_smem<KB>(), sp>>>(
+                                q.L, q.ldl, n, q.plan.nloc, k, row0, nrows, s_lo, q.at<double>(q.cv.res),
+                                q.at<double>(q.cv.chk), q.at<int64_t>(q.cv.chkoff), q.Pbuf(), flag, epoch);
+                        }
+                        count_launch();
+                    }
+                }
+                st = check_cuda(cudaEventRecord(rest_done[g & 1], aux));
+                tr.rec(g, 3, aux);
+                if (st != GCM_OK) return st;
             }
-            st = check_cuda(cudaEventRecord(rest_done[g & 1], aux));
-            tr.rec(g, 3, aux);
+            tr.report(NSB);
+            st = check_cuda(cudaStreamWaitEvent(stream, rest_done[(NSB - 1) & 1], 0));  // join the aux stream
+            if (st == GCM_OK) st = check_cuda(cudaGetLastError());
             if (st != GCM_OK) return st;
         }
-        tr.report(NSB);
-        st = check_cuda(cudaStreamWaitEvent(stream, rest_done[(NSB - 1) & 1], 0));  // join the aux stream
-        if (st == GCM_OK) st = check_cuda(cudaGetLastError());
-        if (st != GCM_OK) return st;
     }
     // 3. prefix Grams (replicated), 4. diagonal sweeps of the local diagonal blocks
     {
@@ -1555,3 +1915,9 @@ gcm_status_t gcm_modify_dist(gcm_comm_t, double *, int64_t, int64_t, int64_t, do
 #endif
 
 }  // extern "C"
+
+#ifdef GCM_PC_TRACE
+extern "C" int gcm_debug_pc_trace(long long *host, int count) {
+    return (int)cudaMemcpyFromSymbol(host, gcm::g_pc_trace, sizeof(long long) * count);
+}
+#endif

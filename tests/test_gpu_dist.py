@@ -158,3 +158,39 @@ def test_dist_single_rank_peer_mode(gd, comm1_peer, n, k, nb, sigma):
         assert gcm.read_info(info)[0] == (oi.code, oi.col, oi.row)
         assert col_scaled_max(upper(L.cpu().numpy()), upper(Lo)) <= 1e-12
         assert row_scaled_max(V.cpu().numpy(), Vo) <= 1e-11
+
+
+@pytest.mark.parametrize("grid", [2, 4])
+@pytest.mark.parametrize("n,k", [(3000, 16), (2200, 33), (1500, 5)])
+def test_pchain_few_helpers_spill(gd, grid, n, k, monkeypatch):
+    """The one-rank persistent chain (GCM_ALGO_PANEL) with its grid capped at 2 / 4 CTAs: one or
+    three helpers own every strip, so most residuals live in the spill slots and round-trip
+    through res[] between tiles (the default grid only does that at n ~ 1e5)."""
+    gcm, _ = gd
+    monkeypatch.setenv("GCM_PCHAIN_GRID", str(grid))
+    for sigma in (1, -1):
+        Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=n + k + grid, lower_fill=np.nan)
+        Lo, Vo = Lbuf.copy(), Vbuf.copy()
+        oracle.modify_a(Lo, Vo, sigma)
+        L, V = torch.from_numpy(Lbuf).cuda(), torch.from_numpy(Vbuf).cuda()
+        gcm.modify(L, V, sigma, algo="panel")
+        torch.cuda.synchronize()
+        assert col_scaled_max(upper(L.cpu().numpy()), upper(Lo)) <= 1e-12
+        assert row_scaled_max(V.cpu().numpy(), Vo) <= 1e-11
+
+
+@pytest.mark.parametrize("n,k", [(3000, 16), (2500, 33)])
+def test_panel_launch_chain_one_rank(gd, n, k, monkeypatch):
+    """GCM_PCHAIN=0: the one-rank panel path through the per-solve-block launches (dsolve,
+    lookahead and rest pupdate on the aux stream) -- what AUTO runs at n ~ 1e5."""
+    gcm, _ = gd
+    monkeypatch.setenv("GCM_PCHAIN", "0")
+    for sigma in (1, -1):
+        Lbuf, Vbuf, _ = synth.paper_instance(n, k, sigma, seed=n + 3 * k, lower_fill=np.nan)
+        Lo, Vo = Lbuf.copy(), Vbuf.copy()
+        oracle.modify_a(Lo, Vo, sigma)
+        L, V = torch.from_numpy(Lbuf).cuda(), torch.from_numpy(Vbuf).cuda()
+        gcm.modify(L, V, sigma, algo="panel")
+        torch.cuda.synchronize()
+        assert col_scaled_max(upper(L.cpu().numpy()), upper(Lo)) <= 1e-12
+        assert row_scaled_max(V.cpu().numpy(), Vo) <= 1e-11
