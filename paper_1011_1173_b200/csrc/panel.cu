@@ -725,11 +725,13 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
 //   CTA 0 (solver), step b:  r_b = the hand-off of strip b (its residual after P_{<= b-2}, from
 //     its helper; V itself for b < 2) = the checkpoint of tile (b-1, b), minus L_{b-1,b}^T q_{b-1}
 //     (its own one-block lookahead), then q_b = W_b^T r_b (W_b = L_bb^{-1}, pinv_kernel) -- both
-//     on DMMA -- published as P's rows; W_{b+1} and L_{b,b+1} are copied under the product;
+//     on DMMA -- published as P's rows; W_{b+1}, L_{b,b+1} and strip b+1's hand-off are loaded
+//     under the step (a two-block lookahead measured slower: the solver's SM is the bottleneck);
 //   CTAs 1.. (helpers): strip s >= 2 belongs to helper (s - 2) mod H; tiles (b, s), b <= s - 2,
-//     in b-major order: poll P_b, checkpoint, r_s -= L_{b,s}^T P_b (DMMA), and after b = s - 2
-//     hand r_s to the solver.  The strip's L tile is staged before the poll; residuals of the
-//     first OWN owned strips stay in shared memory between tiles (the rest round-trip res[]).
+//     in b-major order: poll P_b (prefetched a row ahead), checkpoint, r_s -= L_{b,s}^T P_b
+//     (DMMA), and after b = s - 2 hand r_s to the solver.  The next tile is staged under the
+//     current one; residuals of the first OWN owned strips stay in shared memory between tiles
+//     (the rest round-trip res[]).
 // P and the hand-offs are self-validating values (st_value / ld_value: the pass arms both with
 // all-ones), so a consumer needs one L2 round trip and no flag.  No CTA waits on a later one
 // (the solver on hand-offs of earlier tiles, helpers on P blocks the solver publishes without
@@ -746,8 +748,14 @@ __device__ __forceinline__ long long pc_now() {
     do {                 \
         if (t == 0 && (b) < 4096) g_pc_trace[(b) * 4 + (slot)] = pc_now(); \
     } while (0)
+// helper blockIdx.x == 40: per tile (sequence number q) 0 top, 1 P in smem, 2 tile landed, 3 MMA done
+#define PH_MARK(q, slot) \
+    do {                 \
+        if (t == 0 && blockIdx.x == 40 && (q) < 1024) g_pc_trace[(3072 + (q)) * 4 + (slot)] = pc_now(); \
+    } while (0)
 #else
 #define PC_MARK(b, slot) ((void)0)
+#define PH_MARK(q, slot) ((void)0)
 #endif
 template <int KB>
 struct PcShape {
@@ -757,7 +765,7 @@ struct PcShape {
     static constexpr int ET = NE / 8;
     static constexpr int TPW = (8 * ET + 15) / 16;
     static constexpr int OWN = KB >= 32 ? 5 : 10;  // helper strips whose residual stays in shared memory
-    static constexpr size_t solver_doubles = 2 * kD * LDW + 3 * kD * LDR;
+    static constexpr size_t solver_doubles = 4 * kD * LDW + 3 * kD * LDR;  // 2 W, 2 lookahead tiles
     static constexpr size_t helper_doubles = 2 * kD * LDW + kD * LDR + (OWN + 2) * kD * LDR;  // + spill slots
     static constexpr size_t doubles = solver_doubles > helper_doubles ? solver_doubles : helper_doubles;
 };
@@ -827,30 +835,51 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
 
     if (blockIdx.x == 0) {
         // ------------------------------------------------------------ solver
-        double *Ws = sm_pc;                 // [kD][LDW]
-        double *Lt1 = Ws + kD * LDW;        // L_{b-1,b}
-        double *qh = Lt1 + kD * LDW;        // [2][kD][LDR]: q_b at b % 2
+        double *Ws = sm_pc;                 // [2][kD][LDW]: W_b at b % 2
+        double *Lt = Ws + 2 * kD * LDW;     // [2][kD][LDW]: L_{b-1,b} at b % 2
+        double *qh = Lt + 2 * kD * LDW;     // [2][kD][LDR]: q_b at b % 2
         double *rb = qh + 2 * kD * LDR;     // [kD][LDR]
         auto load_w = [&](int b) {
             const double *src = Winv + (int64_t)b * kD * kD;
+            double *dst = Ws + (b & 1) * kD * LDW;
             for (int idx = t; idx < kD * kD / 2; idx += kPcT) {
                 const int j = idx >> 5, m = 2 * (idx & 31);
-                cp16(Ws + j * LDW + m, src + j * kD + m);
+                cp16(dst + j * LDW + m, src + j * kD + m);
             }
+        };
+        // strip b's hand-off values of this lane (V for b < 2), issued a step ahead
+        unsigned long long rn[TPW][2];
+        auto issue_hand = [&](int b) {
+            const int64_t r0 = (int64_t)b * kD;
+            const int Db = (int)imin64(kD, n - r0);
+            const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)c * k;
+#pragma unroll
+            for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int e = ecol(v, h);
+                    rn[v][h] = (c < Db && e < k) ? ld_relaxed_u64(src + e) : 0ull;
+                }
         };
         load_w(0);
         asm volatile("cp.async.commit_group;" ::: "memory");
+        if (mma_warp) issue_hand(0);
         for (int b = 0; b < NB; ++b) {
             const int64_t r0 = (int64_t)b * kD;
             const int Db = (int)imin64(kD, n - r0);
-            // W_b and this step's lookahead tiles were issued during step b - 1
+            // W_b and L_{b-1,b} were issued at the top of step b - 1
             PC_MARK(b, 0);
             asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncthreads();
+            __syncthreads();  // also: step b - 1's reads of the buffers refilled next are done
             PC_MARK(b, 1);
+            if (b + 1 < NB) {  // the next step's W and lookahead tile fly under this whole step
+                load_w(b + 1);
+                load_tile(Lt + ((b + 1) & 1) * kD * LDW, b, b + 1);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
             if (mma_warp) {
                 // r_b: V for b < 2, else strip b's hand-off (its residual after P_{<= b-2};
-                // self-validating, polled per value) = the checkpoint of tile (b - 1, b)
+                // self-validating) = the checkpoint of tile (b - 1, b)
                 double r[TPW][2];
                 const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)c * k;
 #pragma unroll
@@ -858,7 +887,9 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int e = ecol(v, h);
-                        r[v][h] = (c < Db && e < k) ? (b < 2 ? src[e] : ld_value(src + e)) : 0.0;
+                        unsigned long long u = rn[v][h];
+                        if (b >= 2 && c < Db && e < k && u == kEmpty) u = __double_as_longlong(ld_value(src + e));
+                        r[v][h] = __longlong_as_double((long long)u);
                     }
                 double acc[TPW][2];
                 double *ck1 = b >= 1 ? chk + (chkoff[b] + b - 1) * kD * k + (int64_t)c * k : nullptr;
@@ -871,34 +902,31 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                         acc[v][h] = -r[v][h];
                         if (ck1 && c < Db && e < k) ck1[e] = r[v][h];
                     }
-                if (b >= 1) mma_tile(acc, Lt1, qh + ((b - 1) % 2) * kD * LDR);
+                if (b >= 1) mma_tile(acc, Lt + (b & 1) * kD * LDW, qh + ((b - 1) & 1) * kD * LDR);
 #pragma unroll
                 for (int v = 0; v < TPW; ++v)
 #pragma unroll
                     for (int h = 0; h < 2; ++h) rb[c * LDR + ecol(v, h)] = -acc[v][h];  // r^{(b)}
             }
             __syncthreads();
-            if (b + 1 < NB) {  // the next step's lookahead tile, under this step's product and publish
-                load_tile(Lt1, b, b + 1);
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
             // q_b = W^T r^{(b)} (dsolve's product: DMMA above the 8-row diagonal tiles, masked
             // DFMA on them, so a product 0 * r_j with j > m is never formed)
-            double *qv = qh + (b % 2) * kD * LDR;
+            const double *Wb = Ws + (b & 1) * kD * LDW;
+            double *qv = qh + (b & 1) * kD * LDR;
             if (mma_warp) {
                 const int m0 = ct * 8;
                 double acc[TPW][2];
 #pragma unroll
                 for (int v = 0; v < TPW; ++v) acc[v][0] = acc[v][1] = 0.0;
                 for (int j0 = 0; j0 < m0; j0 += 4) {
-                    const double af = Ws[(j0 + tg) * LDW + m0 + gi];
+                    const double af = Wb[(j0 + tg) * LDW + m0 + gi];
 #pragma unroll
                     for (int v = 0; v < TPW; ++v) dmma_884(acc[v], af, rb[(j0 + tg) * LDR + (eg * TPW + v) * 8 + gi]);
                 }
                 const int m = m0 + gi;
                 double wd[8];  // W(m0 .. m0+7, m): loaded up front, the FMA chain then runs on registers
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) wd[jj] = Ws[(m0 + jj) * LDW + m];
+                for (int jj = 0; jj < 8; ++jj) wd[jj] = Wb[(m0 + jj) * LDW + m];
 #pragma unroll
                 for (int v = 0; v < TPW; ++v)
 #pragma unroll
@@ -915,13 +943,9 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                         qv[m * LDR + e] = s;
                         if (m < Db && e < k) st_value(P + (r0 + m) * k + e, s);  // published
                     }
+                if (b + 1 < NB) issue_hand(b + 1);  // in flight under the next step's wait
             }
-            __syncthreads();  // Ws, rb free
             PC_MARK(b, 3);
-            if (b + 1 < NB) {
-                load_w(b + 1);
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
         }
         return;
     }
@@ -961,7 +985,22 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
     };
     It cur{0, 0};
     stage(cur, 0, false);  // (the residual slots' copies are in this first group)
-    int buf = 0, pb = -1;
+    int buf = 0, pb = -1, seq = 0;
+    // P values of the next tile row, loaded one tile ahead (self-validating: a non-empty
+    // value is final; the rest are polled when that row's first tile starts)
+    constexpr int PPT = (kD * NE + kPcT - 1) / kPcT;
+    unsigned long long pn[PPT];
+    int pn_b = -1;
+    auto issue_p = [&](int bn) {
+        const int64_t rn0 = (int64_t)bn * kD;
+        const int Dn = (int)imin64(kD, n - rn0);
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+            const int o = t + q * kPcT, m = o / NE, e = o % NE;
+            pn[q] = (o < kD * NE && m < Dn && e < k) ? ld_relaxed_u64(P + (rn0 + m) * k + e) : 0ull;
+        }
+        pn_b = bn;
+    };
     while (valid(cur)) {
         It nx = cur;
         adv(nx);
@@ -970,14 +1009,13 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         const int b = cur.b, i = cur.i, s = 2 + h + i * H;
         const int64_t r0 = (int64_t)b * kD;
         const int Db = (int)imin64(kD, n - r0);
+        PH_MARK(seq, 0);
         if (b != pb) {  // P_b, polled per value (every load in flight before the first wait)
-            constexpr int PPT = (kD * NE + kPcT - 1) / kPcT;
+            if (pn_b != b) issue_p(b);
             unsigned long long u[PPT];
 #pragma unroll
-            for (int q = 0; q < PPT; ++q) {
-                const int o = t + q * kPcT, m = o / NE, e = o % NE;
-                u[q] = (o < kD * NE && m < Db && e < k) ? ld_relaxed_u64(P + (r0 + m) * k + e) : 0ull;
-            }
+            for (int q = 0; q < PPT; ++q) u[q] = pn[q];
+            if (valid(nx) && nx.b != b) issue_p(nx.b);  // the next row's P, under this tile
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
                 const int o = t + q * kPcT, m = o / NE, e = o % NE;
@@ -987,10 +1025,14 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                 }
             }
             pb = b;
+        } else if (valid(nx) && nx.b != b && pn_b != nx.b) {
+            issue_p(nx.b);
         }
+        PH_MARK(seq, 1);
         if (valid(nx)) asm volatile("cp.async.wait_group 1;" ::: "memory");
         else asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncthreads();
+        PH_MARK(seq, 2);
         double *Rt = Rs + (i < S::OWN ? i : S::OWN + buf) * kD * LDR;
         const int Dc = (int)imin64(kD, n - (int64_t)s * kD);
         if (mma_warp) {
@@ -1022,10 +1064,12 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                     }
                 }
         }
+        PH_MARK(seq, 3);
         __threadfence_block();  // spilled residuals: stores before a later tile's copies read them
         __syncthreads();
         cur = nx;
         buf ^= 1;
+        ++seq;
     }
 }
 

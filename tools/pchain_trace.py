@@ -31,3 +31,16 @@ print(f"{NB} steps, solver span {(tr[-1, 3] - tr[0, 0]) / 1e3:.1f} us, step medi
 for i, nm in [(1, "W/tiles landed"), (2, "hand-off in regs"), (3, "q published")]:
     d = tr[3:, i] - tr[3:, i - 1]
     print(f"  {nm:18s} +{np.median(d):7.0f} ns (p90 {np.percentile(d, 90):7.0f})")
+hp = np.frombuffer(buf, dtype=np.int64).reshape(4096, 4)[3072:3072 + 1024].astype(np.float64)
+nt = int(np.argmax(hp[:, 0] == 0)) or 1024
+if nt > 4:
+    hp = hp[:nt]
+    per = np.diff(hp[:, 0])
+    print(f"helper CTA 40: {nt} tiles, period median {np.median(per):.0f} ns")
+    for i, nm in [(1, "P in smem"), (2, "tile landed"), (3, "MMA + epilogue")]:
+        d = hp[2:, i] - hp[2:, i - 1]
+        print(f"  {nm:16s} +{np.median(d):7.0f} ns (p90 {np.percentile(d, 90):7.0f})")
+    # when did P_b become visible vs the solver's publish of step b (tile b of this helper)
+    pub = tr[:, 3]
+    lag = [hp[q, 1] - pub[q] for q in range(min(nt, NB)) if pub[q] > 0]
+    print(f"  P in smem - solver publish (same b): median {np.median(lag):.0f} ns")
