@@ -722,12 +722,14 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
 // ------------------------------------------------------------------ persistent chain (one rank)
 // GCM_ALGO_PANEL with one rank replaces the per-solve-block launches (dsolve, lookahead and
 // rest pupdate) by ONE cooperative kernel working in 64-row steps:
-//   CTA 0 (solver), step b:  r_b = the hand-off of strip b (its residual after P_{<= b-2}, from
+//   CTAs 0 .. NS-1 (solvers, 8 update columns each: the right-hand sides of P = L^{-T} V are
+//     independent, so each solver's DMMA work per step is an 8-column slice), step b:
+//     r_b = the hand-off of strip b (its residual after P_{<= b-2}, from
 //     its helper; V itself for b < 2) = the checkpoint of tile (b-1, b), minus L_{b-1,b}^T q_{b-1}
 //     (its own one-block lookahead), then q_b = W_b^T r_b (W_b = L_bb^{-1}, pinv_kernel) -- both
 //     on DMMA -- published as P's rows; W_{b+1}, L_{b,b+1} and strip b+1's hand-off are loaded
 //     under the step (a two-block lookahead measured slower: the solver's SM is the bottleneck);
-//   CTAs 1.. (helpers): strip s >= 2 belongs to helper (s - 2) mod H; tiles (b, s), b <= s - 2,
+//   CTAs NS.. (helpers): strip s >= 2 belongs to helper (s - 2) mod H; tiles (b, s), b <= s - 2,
 //     in b-major order: poll P_b (prefetched a row ahead), checkpoint, r_s -= L_{b,s}^T P_b
 //     (DMMA), and after b = s - 2 hand r_s to the solver.  The next tile is staged under the
 //     current one; residuals of the first OWN owned strips stay in shared memory between tiles
@@ -746,7 +748,7 @@ __device__ __forceinline__ long long pc_now() {
 }
 #define PC_MARK(b, slot) \
     do {                 \
-        if (t == 0 && (b) < 4096) g_pc_trace[(b) * 4 + (slot)] = pc_now(); \
+        if (t == 0 && blockIdx.x == 0 && (b) < 4096) g_pc_trace[(b) * 4 + (slot)] = pc_now(); \
     } while (0)
 // helper blockIdx.x == 40: per tile (sequence number q) 0 top, 1 P in smem, 2 tile landed, 3 MMA done
 #define PH_MARK(q, slot) \
@@ -765,7 +767,8 @@ struct PcShape {
     static constexpr int ET = NE / 8;
     static constexpr int TPW = (8 * ET + 15) / 16;
     static constexpr int OWN = KB >= 32 ? 5 : 10;  // helper strips whose residual stays in shared memory
-    static constexpr size_t solver_doubles = 4 * kD * LDW + 3 * kD * LDR;  // 2 W, 2 lookahead tiles
+    static constexpr int NS = NE / 8;  // solver CTAs
+    static constexpr size_t solver_doubles = 4 * kD * LDW + 3 * kD * 12;  // 2 W, 2 lookahead tiles, q, r
     static constexpr size_t helper_doubles = 2 * kD * LDW + kD * LDR + (OWN + 2) * kD * LDR;  // + spill slots
     static constexpr size_t doubles = solver_doubles > helper_doubles ? solver_doubles : helper_doubles;
 };
@@ -833,12 +836,17 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         }
     };
 
-    if (blockIdx.x == 0) {
-        // ------------------------------------------------------------ solver
+    constexpr int NS = S::NS;  // solver CTAs: 8 update columns each (the right-hand sides are independent)
+    if ((int)blockIdx.x < NS) {
+        // ------------------------------------------------------------ solver for columns es .. es+7
+        constexpr int LDQ = 12;              // row stride of the solver's q / r (8 columns + pad)
+        const int es = blockIdx.x * 8;
         double *Ws = sm_pc;                 // [2][kD][LDW]: W_b at b % 2
         double *Lt = Ws + 2 * kD * LDW;     // [2][kD][LDW]: L_{b-1,b} at b % 2
-        double *qh = Lt + 2 * kD * LDW;     // [2][kD][LDR]: q_b at b % 2
-        double *rb = qh + 2 * kD * LDR;     // [kD][LDR]
+        double *qh = Lt + 2 * kD * LDW;     // [2][kD][LDQ]: q_b at b % 2
+        double *rb = qh + 2 * kD * LDQ;     // [kD][LDQ]
+        const bool sw = warp < 8;           // warp = 8-row tile (MMA warps)
+        const int sc = warp * 8 + gi;       // this lane's strip column / output row
         auto load_w = [&](int b) {
             const double *src = Winv + (int64_t)b * kD * kD;
             double *dst = Ws + (b & 1) * kD * LDW;
@@ -847,23 +855,28 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                 cp16(dst + j * LDW + m, src + j * kD + m);
             }
         };
+        // acc (8 x 8 tile per warp, lane: row sc, columns 2tg, 2tg+1) += A^T B, K = 64
+        auto mma8 = [&](double (&a2)[2], const double *A, const double *B) {
+            const double *la = A + sc * LDW + tg;
+            const double *qb = B + tg * LDQ + gi;
+#pragma unroll 4
+            for (int m0 = 0; m0 < kD; m0 += 4) dmma_884(a2, la[m0], qb[m0 * LDQ]);
+        };
         // strip b's hand-off values of this lane (V for b < 2), issued a step ahead
-        unsigned long long rn[TPW][2];
+        unsigned long long rn[2];
         auto issue_hand = [&](int b) {
             const int64_t r0 = (int64_t)b * kD;
             const int Db = (int)imin64(kD, n - r0);
-            const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)c * k;
+            const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)sc * k + es;
 #pragma unroll
-            for (int v = 0; v < TPW; ++v)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int e = ecol(v, h);
-                    rn[v][h] = (c < Db && e < k) ? ld_relaxed_u64(src + e) : 0ull;
-                }
+            for (int h = 0; h < 2; ++h) {
+                const int e = 2 * tg + h;
+                rn[h] = (sc < Db && es + e < k) ? ld_relaxed_u64(src + e) : 0ull;
+            }
         };
         load_w(0);
         asm volatile("cp.async.commit_group;" ::: "memory");
-        if (mma_warp) issue_hand(0);
+        if (sw) issue_hand(0);
         for (int b = 0; b < NB; ++b) {
             const int64_t r0 = (int64_t)b * kD;
             const int Db = (int)imin64(kD, n - r0);
@@ -877,72 +890,53 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                 load_tile(Lt + ((b + 1) & 1) * kD * LDW, b, b + 1);
                 asm volatile("cp.async.commit_group;" ::: "memory");
             }
-            if (mma_warp) {
+            if (sw) {
                 // r_b: V for b < 2, else strip b's hand-off (its residual after P_{<= b-2};
                 // self-validating) = the checkpoint of tile (b - 1, b)
-                double r[TPW][2];
-                const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)c * k;
+                const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)sc * k + es;
+                double *ck1 = b >= 1 ? chk + (chkoff[b] + b - 1) * kD * k + (int64_t)sc * k + es : nullptr;
+                double acc[2];
 #pragma unroll
-                for (int v = 0; v < TPW; ++v)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int e = ecol(v, h);
-                        unsigned long long u = rn[v][h];
-                        if (b >= 2 && c < Db && e < k && u == kEmpty) u = __double_as_longlong(ld_value(src + e));
-                        r[v][h] = __longlong_as_double((long long)u);
-                    }
-                double acc[TPW][2];
-                double *ck1 = b >= 1 ? chk + (chkoff[b] + b - 1) * kD * k + (int64_t)c * k : nullptr;
+                for (int h = 0; h < 2; ++h) {
+                    const int e = 2 * tg + h;
+                    unsigned long long u = rn[h];
+                    if (b >= 2 && sc < Db && es + e < k && u == kEmpty) u = __double_as_longlong(ld_value(src + e));
+                    const double r = __longlong_as_double((long long)u);
+                    acc[h] = -r;
+                    if (ck1 && sc < Db && es + e < k) ck1[e] = r;
+                }
                 PC_MARK(b, 2);
+                if (b >= 1) mma8(acc, Lt + (b & 1) * kD * LDW, qh + ((b - 1) & 1) * kD * LDQ);
 #pragma unroll
-                for (int v = 0; v < TPW; ++v)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int e = ecol(v, h);
-                        acc[v][h] = -r[v][h];
-                        if (ck1 && c < Db && e < k) ck1[e] = r[v][h];
-                    }
-                if (b >= 1) mma_tile(acc, Lt + (b & 1) * kD * LDW, qh + ((b - 1) & 1) * kD * LDR);
-#pragma unroll
-                for (int v = 0; v < TPW; ++v)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) rb[c * LDR + ecol(v, h)] = -acc[v][h];  // r^{(b)}
+                for (int h = 0; h < 2; ++h) rb[sc * LDQ + 2 * tg + h] = -acc[h];  // r^{(b)}
             }
             __syncthreads();
-            // q_b = W^T r^{(b)} (dsolve's product: DMMA above the 8-row diagonal tiles, masked
-            // DFMA on them, so a product 0 * r_j with j > m is never formed)
+            // q_b = W^T r^{(b)} (DMMA above the 8-row diagonal tiles, masked DFMA on them, so a
+            // product 0 * r_j with j > m is never formed)
             const double *Wb = Ws + (b & 1) * kD * LDW;
-            double *qv = qh + (b & 1) * kD * LDR;
-            if (mma_warp) {
-                const int m0 = ct * 8;
-                double acc[TPW][2];
-#pragma unroll
-                for (int v = 0; v < TPW; ++v) acc[v][0] = acc[v][1] = 0.0;
-                for (int j0 = 0; j0 < m0; j0 += 4) {
-                    const double af = Wb[(j0 + tg) * LDW + m0 + gi];
-#pragma unroll
-                    for (int v = 0; v < TPW; ++v) dmma_884(acc[v], af, rb[(j0 + tg) * LDR + (eg * TPW + v) * 8 + gi]);
-                }
+            double *qv = qh + (b & 1) * kD * LDQ;
+            if (sw) {
+                const int m0 = warp * 8;
+                double qa[2] = {0.0, 0.0};
+                for (int j0 = 0; j0 < m0; j0 += 4) dmma_884(qa, Wb[(j0 + tg) * LDW + m0 + gi], rb[(j0 + tg) * LDQ + gi]);
                 const int m = m0 + gi;
                 double wd[8];  // W(m0 .. m0+7, m): loaded up front, the FMA chain then runs on registers
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) wd[jj] = Wb[(m0 + jj) * LDW + m];
 #pragma unroll
-                for (int v = 0; v < TPW; ++v)
+                for (int h = 0; h < 2; ++h) {
+                    const int e = 2 * tg + h;
+                    double rd[8];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int e = ecol(v, h);
-                        double rd[8];
+                    for (int jj = 0; jj < 8; ++jj) rd[jj] = rb[(m0 + jj) * LDQ + e];
+                    double s = qa[h];
 #pragma unroll
-                        for (int jj = 0; jj < 8; ++jj) rd[jj] = rb[(m0 + jj) * LDR + e];
-                        double s = acc[v][h];
-#pragma unroll
-                        for (int jj = 0; jj < 8; ++jj)
-                            if (jj <= gi) s = fma(wd[jj], rd[jj], s);  // j <= m only
-                        s = m < Db ? s : 0.0;  // rows past the block stay zero
-                        qv[m * LDR + e] = s;
-                        if (m < Db && e < k) st_value(P + (r0 + m) * k + e, s);  // published
-                    }
+                    for (int jj = 0; jj < 8; ++jj)
+                        if (jj <= gi) s = fma(wd[jj], rd[jj], s);  // j <= m only
+                    s = m < Db ? s : 0.0;  // rows past the block stay zero
+                    qv[m * LDQ + e] = s;
+                    if (m < Db && es + e < k) st_value(P + (r0 + m) * k + es + e, s);  // published
+                }
                 if (b + 1 < NB) issue_hand(b + 1);  // in flight under the next step's wait
             }
             PC_MARK(b, 3);
@@ -950,7 +944,7 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         return;
     }
     // ---------------------------------------------------------------- helpers
-    const int h = blockIdx.x - 1, H = gridDim.x - 1;
+    const int h = blockIdx.x - NS, H = gridDim.x - NS;
     double *Lh = sm_pc;                 // [2][kD][LDW]: this tile and the next
     double *Ph = Lh + 2 * kD * LDW;     // [kD][LDR]
     double *Rs = Ph + kD * LDR;         // [OWN + 2][kD][LDR]: residuals of the first OWN owned strips,
@@ -1349,9 +1343,11 @@ gcm_status_t pchain_launch(Rank &q, int64_t n, int k, int NB64, cudaStream_t str
     if (st != GCM_OK) return st;
     if (per_sm < 1) return GCM_ECUDA;
     // the solver + one helper per strip that needs hand-offs (strips 2 ..), at most one CTA per SM
-    int grid = (int)std::max(1, std::min(nsm * per_sm, 1 + std::max(0, NB64 - 2)));
+    constexpr int NS = PcShape<KB>::NS;
+    int grid = (int)std::max(NS, std::min(nsm * per_sm, NS + std::max(0, NB64 - 2)));
     // GCM_PCHAIN_GRID=<g> caps the grid (tests: few helpers own many strips -> the spill slots)
-    if (const char *e = std::getenv("GCM_PCHAIN_GRID")) grid = std::max(2, std::min(grid, std::atoi(e)));
+    if (const char *e = std::getenv("GCM_PCHAIN_GRID")) grid = std::max(NS + 1, std::min(grid, std::atoi(e)));
+    if (grid <= NS && NB64 > 2) grid = NS + 1;
     const double *L = q.L;
     int64_t ldl = q.ldl;
     double *res = q.at<double>(q.cv.res), *chk = q.at<double>(q.cv.chk), *P = q.Pbuf();
