@@ -156,13 +156,12 @@ gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     if (env && std::strcmp(env, "sweep") == 0) return GCM_ALGO_SWEEP;
     if (env && std::strcmp(env, "blocked") == 0) return GCM_ALGO_BLOCKED;
     if (env && std::strcmp(env, "panel") == 0) return GCM_ALGO_PANEL;
-    (void)k;
     // the chain-shortened path wins once there is more
     // than a handful of row blocks; tiny factors keep the two-kernel sweep; large factors
-    // take the column-block (panel) algorithm, whose residual updates run on the FP64 tensor
-    // cores (n = 20000, k = 32: 4.0 vs 5.0 ms; n = 40000: 12.3 vs 18.1 ms; at n = 12000 the two
-    // are level, profiles/r02bg_crossover.txt).
-    if (n >= 16000) return GCM_ALGO_PANEL;
+    // take the column-block (panel) algorithm, whose solve chain and residual updates run on
+    // the FP64 tensor cores (profiles/r02bj_crossover.txt: level with BLOCKED at n = 8000 for
+    // k <= 16 and n = 10000 for k = 32; n = 16000, k = 32: 2.65 vs 3.33 ms).
+    if (n >= (k <= 16 ? 8000 : 11000)) return GCM_ALGO_PANEL;
     return n >= 256 ? GCM_ALGO_BLOCKED : GCM_ALGO_SWEEP;
 }
 

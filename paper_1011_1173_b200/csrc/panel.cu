@@ -877,7 +877,11 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         load_w(0);
         asm volatile("cp.async.commit_group;" ::: "memory");
         if (sw) issue_hand(0);
+        int64_t ckn = chkoff[0];  // checkpoint offset of strip b, loaded a step ahead (a global load
+                                  // issued just before its use stalled the step on its latency)
         for (int b = 0; b < NB; ++b) {
+            const int64_t ckb = ckn;
+            if (b + 1 < NB) ckn = chkoff[b + 1];
             const int64_t r0 = (int64_t)b * kD;
             const int Db = (int)imin64(kD, n - r0);
             // W_b and L_{b-1,b} were issued at the top of step b - 1
@@ -894,7 +898,7 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                 // r_b: V for b < 2, else strip b's hand-off (its residual after P_{<= b-2};
                 // self-validating) = the checkpoint of tile (b - 1, b)
                 const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)sc * k + es;
-                double *ck1 = b >= 1 ? chk + (chkoff[b] + b - 1) * kD * k + (int64_t)sc * k + es : nullptr;
+                double *ck1 = b >= 1 ? chk + (ckb + b - 1) * kD * k + (int64_t)sc * k + es : nullptr;
                 double acc[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -1003,6 +1007,7 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         const int b = cur.b, i = cur.i, s = 2 + h + i * H;
         const int64_t r0 = (int64_t)b * kD;
         const int Db = (int)imin64(kD, n - r0);
+        const int64_t cks = chkoff[s];  // issued before the P poll: its latency hides there
         PH_MARK(seq, 0);
         if (b != pb) {  // P_b, polled per value (every load in flight before the first wait)
             if (pn_b != b) issue_p(b);
@@ -1031,17 +1036,22 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         const int Dc = (int)imin64(kD, n - (int64_t)s * kD);
         if (mma_warp) {
             double acc[TPW][2];
-            double *ck = b >= 1 ? chk + (chkoff[s] + b) * kD * k + (int64_t)c * k : nullptr;
 #pragma unroll
             for (int v = 0; v < TPW; ++v)
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const int e = ecol(v, hh);
-                    const double r = Rt[c * LDR + e];
-                    acc[v][hh] = -r;
-                    if (ck && c < Dc && e < k) ck[e] = r;
-                }
+                for (int hh = 0; hh < 2; ++hh) acc[v][hh] = -Rt[c * LDR + ecol(v, hh)];
             mma_tile(acc, Lh + buf * kD * LDW, Ph);
+            PH_MARK(seq, 3);
+            if (b >= 1) {  // checkpoint (b, s): the residual before this tile (still in Rt)
+                double *ck = chk + (cks + b) * kD * k + (int64_t)c * k;
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int e = ecol(v, hh);
+                        if (c < Dc && e < k) ck[e] = Rt[c * LDR + e];
+                    }
+            }
             const bool hoff = b == s - 2;
             double *rg = res + (int64_t)s * kD * k + (int64_t)c * k;
             double *hg = hand + (int64_t)s * kD * k + (int64_t)c * k;
@@ -1058,7 +1068,6 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                     }
                 }
         }
-        PH_MARK(seq, 3);
         __threadfence_block();  // spilled residuals: stores before a later tile's copies read them
         __syncthreads();
         cur = nx;

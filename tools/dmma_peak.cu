@@ -53,6 +53,67 @@ __global__ void dmma_tput(double *out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// NCH independent accumulator chains per warp, fragments from shared memory (the pchain tile pattern)
+template <int NCH>
+__global__ void dmma_chains(double *out, int iters) {
+    __shared__ double sa[64 * 68], sb[64 * 20];
+    for (int i = threadIdx.x; i < 64 * 68; i += blockDim.x) sa[i] = 1e-3 * i;
+    for (int i = threadIdx.x; i < 64 * 20; i += blockDim.x) sb[i] = 1e-3 * i;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, gi = lane >> 2, tg = lane & 3, w = threadIdx.x >> 5;
+    double c[NCH][2] = {};
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll 4
+        for (int m0 = 0; m0 < 64; m0 += 4) {
+            const double a = sa[((w & 7) * 8 + gi) * 68 + m0 + tg];
+#pragma unroll
+            for (int q = 0; q < NCH; ++q) {
+                const double b = sb[(m0 + tg) * 20 + q * 8 + gi];
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                             : "+d"(c[q][0]), "+d"(c[q][1]) : "d"(a), "d"(b));
+            }
+        }
+    }
+    double s = 0;
+    for (int q = 0; q < NCH; ++q) s += c[q][0] + c[q][1];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+template <int NCH>
+void run_chains(int warps) {
+    double *out;
+    cudaMalloc(&out, 148 * 1024 * 8);
+    dmma_chains<NCH><<<148, warps * 32>>>(out, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 2048;
+    cudaEventRecord(e0);
+    dmma_chains<NCH><<<148, warps * 32>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fmas = 148.0 * warps * iters * 16 * NCH * 256;
+    std::printf("{\"chains_per_warp\": %d, \"warps_per_cta\": %d, \"ctas\": 148, \"tflops\": %.2f}\n", NCH, warps,
+                2 * fmas / (ms * 1e-3) / 1e12);
+    cudaFree(out);
+}
+
+// dependent-chain latency of one DMMA.8x8x4 (one warp)
+__global__ void dmma_lat(double *out, long long *cyc, int iters) {
+    double a = 1e-3 * threadIdx.x, b = 1e-3, c[2] = {0, 0};
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = c[0] + c[1];
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
 template <int SHAPE>
 void run(const char *name, double fma_per_instr, int instr_per_iter) {
     double *out;
@@ -83,5 +144,19 @@ int main() {
     run<1>("m16n8k4", 512, 16);
     run<2>("m16n8k8", 1024, 8);
     run<3>("m16n8k16", 2048, 8);
+    {
+        double *out;
+        long long *cyc, h = 0;
+        cudaMalloc(&out, 32 * 8);
+        cudaMalloc(&cyc, 8);
+        dmma_lat<<<1, 32>>>(out, cyc, 64);
+        dmma_lat<<<1, 32>>>(out, cyc, 1024);
+        cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        std::printf("{\"dmma_884_dependent_latency_cycles\": %.2f}\n", (double)h / (1024.0 * 16));
+    }
+    run_chains<1>(16);
+    run_chains<2>(16);
+    run_chains<2>(8);
+    run_chains<4>(8);
     return 0;
 }
