@@ -408,7 +408,7 @@ def kernel_units(name, n, k, batch, per_step=1):
     PER PASS, so the bytes are per pass too)."""
     tri = 8 * n * (n + 1) // 2  # bytes of the upper triangle
     kp = k / per_step  # update columns per launch (average)
-    if name == "blocked":  # TRSV kernel + the Apply grid overlapped with it (one profiling scope)
+    if name in ("blocked", "pchain"):  # solve chain + sweeps + the Apply overlapped with it (one scope)
         return {"bound": "hbm" if kp < 16 else "alu", "bytes": 8 * n * (n + 1) + 16 * n * kp,
                 "flops": 6 * kp * n * (n - 1) / 2,
                 "what": f"one pass of {kp:g} update columns (TRSV + fused sweeps + overlapped Apply): upper "

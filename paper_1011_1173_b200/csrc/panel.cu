@@ -91,6 +91,7 @@ struct Plan {
     std::vector<int> dl_b;                  // local diagonal 64-row blocks
     std::vector<int64_t> dl_lc;             //   and their first local column
     std::vector<int2> full;                 // TMA Apply items (b, first local strip of 4)
+    std::vector<int> full_off, tiles_off;   // one rank: items sorted by b; row block b's are [off[b], off[b+1])
     std::vector<int2> tiles;                // single-tile Apply items (b, local strip)
     int64_t sb;                             // solve-block height (<= nb, dsolve's shared-memory cap)
     int NSB;                                // solve blocks
@@ -155,12 +156,25 @@ Plan make_plan(int64_t n, int64_t nb, int R, int r, int k, bool tma_groups) {
             }
         }
     }
+    if (R == 1) {  // the persistent chain's overlapped Apply takes the items row block by row block
+        auto by_b = [](const int2 &x, const int2 &y) { return x.x < y.x || (x.x == y.x && x.y < y.y); };
+        std::sort(p.full.begin(), p.full.end(), by_b);
+        std::sort(p.tiles.begin(), p.tiles.end(), by_b);
+        auto offsets = [&](const std::vector<int2> &v, std::vector<int> &off) {
+            off.assign(p.NB64 + 1, 0);
+            for (const int2 &x : v) ++off[x.x + 1];
+            for (int b = 0; b < p.NB64; ++b) off[b + 1] += off[b];
+        };
+        offsets(p.full, p.full_off);
+        offsets(p.tiles, p.tiles_off);
+    }
     return p;
 }
 
 // workspace carve-up of one rank (byte offsets)
 struct Carve {
-    size_t P, res, chk, Winv, Q, G, U, panels, key, flags, ctr, sflag, gstrip, chkoff, dlb, dllc, full, tiles, total;
+    size_t P, res, chk, Winv, Q, G, U, panels, key, flags, ctr, sflag, rowcnt, gstrip, chkoff, dlb, dllc, full, tiles,
+        total;
 };
 Carve carve(const Plan &p) {
     Carve c{};
@@ -183,6 +197,7 @@ Carve carve(const Plan &p) {
     c.flags = take((size_t)(p.NSB + 1) * 4);
     c.ctr = take(16);
     c.sflag = take((size_t)p.NB64 * kD * p.k * 8);  // persistent chain: strip hand-offs (self-validating)
+    c.rowcnt = take((size_t)p.NB64 * 4);              // persistent chain: tiles of row block b checkpointed
     c.gstrip = take((size_t)std::max(p.nsl, 1) * 4);
     c.chkoff = take((size_t)std::max(p.nsl, 1) * 8);
     c.dlb = take((size_t)std::max<size_t>(p.dl_b.size(), 1) * 4);
@@ -787,7 +802,8 @@ __device__ __forceinline__ void st_value(double *p, double v) {
 template <int KB>
 __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restrict__ L, int64_t ldl, int64_t n, int k,
                                                         int NB, double *res, double *chk, const int64_t *chkoff,
-                                                        const double *__restrict__ Winv, double *P, double *hand) {
+                                                        const double *__restrict__ Winv, double *P, double *hand,
+                                                        unsigned *rowcnt) {
     using S = PcShape<KB>;
     constexpr int NE = S::NE, LDR = S::LDR, LDW = S::LDW, ET = S::ET, TPW = S::TPW;
     extern __shared__ __align__(16) double sm_pc[];
@@ -915,6 +931,10 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                 for (int h = 0; h < 2; ++h) rb[sc * LDQ + 2 * tg + h] = -acc[h];  // r^{(b)}
             }
             __syncthreads();
+            if (b >= 1 && t == 0) {  // tile (b-1, b): checkpoint written, L_{b-1,b} consumed
+                __threadfence();
+                atomicAdd(rowcnt + (b - 1), 1u);
+            }
             // q_b = W^T r^{(b)} (DMMA above the 8-row diagonal tiles, masked DFMA on them, so a
             // product 0 * r_j with j > m is never formed)
             const double *Wb = Ws + (b & 1) * kD * LDW;
@@ -1070,6 +1090,10 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         }
         __threadfence_block();  // spilled residuals: stores before a later tile's copies read them
         __syncthreads();
+        if (t == 0) {  // tile (b, s): checkpoint written, L tile consumed (the overlapped Apply's cue)
+            __threadfence();
+            atomicAdd(rowcnt + b, 1u);
+        }
         cur = nx;
         buf ^= 1;
         ++seq;
@@ -1078,8 +1102,8 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
 
 // Q_b = P_b^T P_b per 64-row block (KB x KB, zero padded)
 template <int KB>
-__global__ void pgram_kernel(const double *__restrict__ P, int64_t n, int k, double *Q) {
-    const int b = blockIdx.x;
+__global__ void pgram_kernel(const double *__restrict__ P, int64_t n, int k, double *Q, int b0 = 0) {
+    const int b = b0 + blockIdx.x;
     for (int o = threadIdx.x; o < KB * KB; o += blockDim.x) {
         const int i = o / KB, j = o % KB;
         double s = 0.0;
@@ -1098,6 +1122,33 @@ __global__ void pscan_kernel(const double *__restrict__ Q, int NB, double *G) {
         const double q = Q[(int64_t)b * KB * KB + o];
         G[(int64_t)b * KB * KB + o] = run;
         run += q;
+    }
+}
+
+// G_b for b in [b0, b1), continuing the prefix of the blocks before b0 (row-block chunks of the
+// persistent chain's overlapped tail, in order on one stream)
+template <int KB>
+__global__ void pscan_range_kernel(const double *__restrict__ Q, int b0, int b1, double *G) {
+    const int o = threadIdx.x;
+    if (o >= KB * KB) return;
+    double run = b0 == 0 ? 0.0 : G[(int64_t)(b0 - 1) * KB * KB + o] + Q[(int64_t)(b0 - 1) * KB * KB + o];
+    for (int b = b0; b < b1; ++b) {
+        const double q = Q[(int64_t)b * KB * KB + o];
+        G[(int64_t)b * KB * KB + o] = run;
+        run += q;
+    }
+}
+// waits until every tile (b, s), s > b, of row blocks b0 .. b1-1 is checkpointed and its L tile
+// consumed (rowcnt[b] = tiles of row b: NB - 2 - b helper tiles + one per solver CTA)
+__global__ void pwait_rows_kernel(const unsigned *rowcnt, int b0, int b1, int NB, int NS) {
+    for (int b = b0 + (int)threadIdx.x; b < b1; b += blockDim.x) {
+        const unsigned want = (unsigned)(NB - 2 - b + NS);
+        if (b > NB - 2) continue;
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(rowcnt + b) : "memory");
+            if (v != want) __nanosleep(256);
+        } while (v != want);
     }
 }
 
@@ -1335,11 +1386,15 @@ bool pchain_enabled(int NB64) {
     return NB64 - 2 <= 6 * (nsm - 1);
 }
 template <int KB>
-gcm_status_t pchain_launch(Rank &q, int64_t n, int k, int NB64, cudaStream_t stream) {
+gcm_status_t pchain_launch(Rank &q, int64_t n, int k, int NB64, cudaStream_t stream, cudaEvent_t armed, int reserve) {
     double *hand = q.at<double>(q.cv.sflag);
+    unsigned *rowcnt = q.at<unsigned>(q.cv.rowcnt);
     // P and the hand-offs start all-ones: the "not yet written" pattern consumers poll for
     gcm_status_t st = check_cuda(cudaMemsetAsync(hand, 0xff, (size_t)NB64 * kD * k * 8, stream));
     if (st == GCM_OK) st = check_cuda(cudaMemsetAsync(q.Pbuf(), 0xff, (size_t)n * k * 8, stream));
+    if (st == GCM_OK) st = check_cuda(cudaMemsetAsync(rowcnt, 0, (size_t)NB64 * 4, stream));
+    if (st != GCM_OK) return st;
+    if (armed) st = check_cuda(cudaEventRecord(armed, stream));  // the overlapped tail starts after this
     if (st != GCM_OK) return st;
     const size_t smem = pchain_smem<KB>();
     st = check_cuda(cudaFuncSetAttribute(pchain_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1353,7 +1408,8 @@ gcm_status_t pchain_launch(Rank &q, int64_t n, int k, int NB64, cudaStream_t str
     if (per_sm < 1) return GCM_ECUDA;
     // the solver + one helper per strip that needs hand-offs (strips 2 ..), at most one CTA per SM
     constexpr int NS = PcShape<KB>::NS;
-    int grid = (int)std::max(NS, std::min(nsm * per_sm, NS + std::max(0, NB64 - 2)));
+    // (reserve: SMs left to the overlapped tail's sweeps and Apply while the chain runs)
+    int grid = (int)std::max(NS, std::min(nsm * per_sm - reserve, NS + std::max(0, NB64 - 2)));
     // GCM_PCHAIN_GRID=<g> caps the grid (tests: few helpers own many strips -> the spill slots)
     if (const char *e = std::getenv("GCM_PCHAIN_GRID")) grid = std::max(NS + 1, std::min(grid, std::atoi(e)));
     if (grid <= NS && NB64 > 2) grid = NS + 1;
@@ -1362,11 +1418,68 @@ gcm_status_t pchain_launch(Rank &q, int64_t n, int k, int NB64, cudaStream_t str
     double *res = q.at<double>(q.cv.res), *chk = q.at<double>(q.cv.chk), *P = q.Pbuf();
     const int64_t *chkoff = q.at<int64_t>(q.cv.chkoff);
     const double *W = q.at<double>(q.cv.Winv);
-    void *args[] = {(void *)&L, &ldl, &n, &k, &NB64, &res, &chk, (void *)&chkoff, (void *)&W, &P, &hand};
+    void *args[] = {(void *)&L, &ldl, &n, &k, &NB64, &res, &chk, (void *)&chkoff, (void *)&W, &P, &hand, &rowcnt};
     st = check_cuda(cudaLaunchCooperativeKernel((const void *)pchain_kernel<KB>, dim3(grid), dim3(kPcT), args, smem,
                                                 stream));
     count_launch();
     return st;
+}
+
+// The persistent chain's tail -- prefix Grams, diagonal sweeps and the Apply -- row block by row
+// block while the chain still runs: chunk c's kernels go to the auxiliary stream behind a
+// pwait_rows_kernel that waits for the chunk's row counters (every tile of those rows
+// checkpointed, its L tile consumed), so they run on the SMs the chain leaves free (or frees
+// as its helpers finish); the last chunk runs on the call's stream after the chain.
+template <int KB>
+gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, int NB64, cudaStream_t stream,
+                         cudaStream_t aux, cudaEvent_t armed, cudaEvent_t aux_done) {
+    constexpr int NS = PcShape<KB>::NS;
+    const size_t smem_t2 = t2_smem_bytes(KB);
+    gcm_status_t st = check_cuda(
+        cudaFuncSetAttribute(papply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t2));
+    if (st != GCM_OK) return st;
+    // row blocks per chunk: a chunk's sweeps and Apply are latency-bound waves, so few chunks
+    // (GCM_PCHAIN_CHUNKS, default 2)
+    const char *ce = std::getenv("GCM_PCHAIN_CHUNKS");
+    const int want = ce ? std::max(1, std::atoi(ce)) : 2;
+    const int cs = std::max(4, (NB64 + want - 1) / want);
+    ApplyMap map{q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff), q.plan.nloc};
+    auto chunk = [&](int B0, int B1, cudaStream_t s, bool wait) -> gcm_status_t {
+        if (wait) {
+            pwait_rows_kernel<<<1, 64, 0, s>>>(q.at<unsigned>(q.cv.rowcnt), B0, B1, NB64, NS);
+            count_launch();
+        }
+        pgram_kernel<KB><<<B1 - B0, KB * KB <= 1024 ? KB * KB : 1024, 0, s>>>(q.Pbuf(), n, k, q.at<double>(q.cv.Q), B0);
+        pscan_range_kernel<KB><<<1, KB * KB, 0, s>>>(q.at<double>(q.cv.Q), B0, B1, q.at<double>(q.cv.G));
+        pdiag_kernel<KB><<<B1 - B0, kDiagThreads, pdiag_smem<KB>(), s>>>(
+            q.L, q.ldl, n, q.V, std::max<int64_t>(q.plan.nloc, 1), k, sigma, q.Pbuf(), q.Ubuf(),
+            q.at<double>(q.cv.G), q.panbuf(), q.at<unsigned long long>(q.cv.key), ebase, q.at<int>(q.cv.dlb) + B0,
+            q.at<int64_t>(q.cv.dllc) + B0);
+        count_launch(3);
+        const int f0 = q.plan.full_off[B0], f1 = q.plan.full_off[B1];
+        const int t0 = q.plan.tiles_off[B0], t1 = q.plan.tiles_off[B1];
+        if (q.tma && f1 > f0) {
+            papply_kernel<KB><<<(unsigned)(f1 - f0), kT2Threads, smem_t2, s>>>(
+                q.tm, n, k, q.at<double>(q.cv.chk), q.Ubuf(), q.panbuf(), NB64, q.at<int2>(q.cv.full) + f0, map);
+            count_launch();
+        }
+        if (t1 > t0) {
+            ptile_kernel<KB><<<(unsigned)(t1 - t0), kD, 0, s>>>(q.L, q.ldl, q.plan.nloc, k, q.at<double>(q.cv.chk),
+                                                               q.Ubuf(), q.panbuf(), q.at<int2>(q.cv.tiles) + t0,
+                                                               q.at<int64_t>(q.cv.chkoff));
+            count_launch();
+        }
+        return check_cuda(cudaGetLastError());
+    };
+    const int nchunks = (NB64 + cs - 1) / cs;
+    if (nchunks > 1) {
+        st = check_cuda(cudaStreamWaitEvent(aux, armed, 0));
+        for (int c = 0; c + 1 < nchunks && st == GCM_OK; ++c) st = chunk(c * cs, (c + 1) * cs, aux, true);
+        if (st == GCM_OK) st = check_cuda(cudaEventRecord(aux_done, aux));
+        if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(stream, aux_done, 0));
+        if (st != GCM_OK) return st;
+    }
+    return chunk((nchunks - 1) * cs, NB64, stream, false);  // after the chain (stream order)
 }
 
 // one pass (<= 32 update columns) over all ranks of `rk` (Virtual: all R; else rk has one entry)
@@ -1375,6 +1488,11 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                         unsigned epoch, const Exchange &x, cudaStream_t stream) {
     gcm_status_t st = GCM_OK;
     const int nloc_ranks = (int)rk.size();
+    // one rank: the persistent chain, with its tail overlapped unless GCM_PCHAIN_TAIL=0
+    const int NB64_ = (int)((n + kD - 1) / kD);
+    const bool use_pchain = R == 1 && x.mode == Mode::Virtual && pchain_enabled(NB64_);
+    const char *tail_env = std::getenv("GCM_PCHAIN_TAIL");
+    bool tail_overlap = use_pchain && !(tail_env && tail_env[0] == '0');
     const int NBc = (int)((n + nb - 1) / nb), NB64 = (int)((n + kD - 1) / kD);
     auto peers_P = [&](int owner_local) {
         Peers p{};
@@ -1421,15 +1539,25 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
     }
     // 2. the right-looking solve over column blocks
     {
-        ProfScope ps("ptrsv", stream);
+        // (with the overlapped tail the scope holds the whole pass: 'pchain')
+        ProfScope ps(tail_overlap ? "pchain" : "ptrsv", stream);
         for (auto &q : rk) {  // inverses of the diagonal blocks the solve chain multiplies by
             if (q.plan.nsl == 0) continue;
             pinv_kernel<<<q.plan.nsl, kD, 0, stream>>>(q.L, q.ldl, n, q.at<int>(q.cv.gstrip),
                                                        q.at<double>(q.cv.Winv));
             count_launch();
         }
-        if (R == 1 && x.mode == Mode::Virtual && pchain_enabled(NB64)) {
-            st = pchain_launch<KB>(rk[0], n, k, NB64, stream);
+        if (use_pchain) {
+            cudaStream_t aux = nullptr;
+            cudaEvent_t *ev_a = nullptr, *ev_b = nullptr;
+            st = aux_stream(&aux, &ev_a, &ev_b);
+            if (st != GCM_OK) return st;
+            // GCM_PCHAIN_RESERVE=<m>: SMs kept free of chain CTAs for the overlapped tail (default 0)
+            const char *re = std::getenv("GCM_PCHAIN_RESERVE");
+            const int reserve = tail_overlap && re ? std::max(0, std::atoi(re)) : 0;
+            st = pchain_launch<KB>(rk[0], n, k, NB64, stream, tail_overlap ? ev_a[0] : nullptr, reserve);
+            if (st == GCM_OK && tail_overlap)
+                st = pchain_tail<KB>(rk[0], n, k, sigma, ebase, NB64, stream, aux, ev_a[0], ev_b[0]);
             if (st != GCM_OK) return st;
         } else {
             cudaStream_t aux = nullptr;
@@ -1525,6 +1653,7 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
             if (st != GCM_OK) return st;
         }
     }
+    if (tail_overlap) return check_cuda(cudaGetLastError());  // the tail ran with the chain
     // 3. prefix Grams (replicated), 4. diagonal sweeps of the local diagonal blocks
     {
         ProfScope ps("psweep", stream);
