@@ -280,6 +280,38 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
     }
 }
 
+// Inverse of one 64x64 upper-triangular block U (U(i, j) = Lb[i + j * ldl], i <= j < D), by 64
+// threads: thread m computes column m of U^{-1} by back substitution (U w = e_m), its 64 running
+// sums in registers at compile-time indices, every U entry a shared-memory broadcast; the
+// partial sums of rows j > m are never formed, so a NaN in U reaches exactly the entries
+// substitution would reach.  Stored by rows: w[j * 64 + m] = (U^{-1})(j, m), zero for j > m and
+// for m >= D.  Us: [kD][kD] shared scratch, rd: [kD].
+__device__ __forceinline__ void pinv_block(const double *__restrict__ Lb, int64_t ldl, int D, double *w,
+                                           double (*Us)[kD], double *rd) {
+    const int m = threadIdx.x;
+    for (int idx = m; idx < kD * kD; idx += kD) {
+        const int j = idx / kD, i = idx % kD;  // consecutive threads: consecutive rows of column j
+        Us[j][i] = (i <= j && j < D) ? Lb[i + (int64_t)j * ldl] : 0.0;
+    }
+    __syncthreads();
+    rd[m] = m < D ? 1.0 / Us[m][m] : 0.0;
+    __syncthreads();
+    const bool act = m < D;
+    double acc[kD];
+#pragma unroll
+    for (int i = 0; i < kD; ++i) acc[i] = i == m ? 1.0 : 0.0;
+#pragma unroll
+    for (int j = kD - 1; j >= 0; --j) {
+        if (act && j <= m) {
+            acc[j] *= rd[j];  // w_j
+#pragma unroll
+            for (int i = 0; i < j; ++i) acc[i] = fma(-Us[j][i], acc[j], acc[i]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kD; ++j) w[j * kD + m] = (act && j <= m) ? acc[j] : 0.0;
+}
+
 // One FP64 tensor-core step (DMMA, mma.sync m8n8k4 .f64): c(8x8) += a(8x4) b(4x8), lane l
 // holding a[l/4][l%4], b[l%4][l/4] and c[l/4][2(l%4) .. 2(l%4)+1] (PTX ISA fragment layout).
 __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {

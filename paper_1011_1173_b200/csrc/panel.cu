@@ -287,33 +287,12 @@ __device__ __forceinline__ void cp16(double *dst, const double *src) {
 // substitution would reach.
 __global__ void __launch_bounds__(kD) pinv_kernel(const double *__restrict__ L, int64_t ldl, int64_t n,
                                                   const int *gstrip, double *W) {
-    __shared__ __align__(16) double Us[kD][kD];  // Us[j][i] = U(i, j): column j of U
+    __shared__ __align__(16) double Us[kD][kD];
     __shared__ double rd[kD];
-    const int sl = blockIdx.x, m = threadIdx.x;
+    const int sl = blockIdx.x;
     const int64_t r0 = (int64_t)gstrip[sl] * kD, lc = (int64_t)sl * kD;
     const int D = (int)imin64(kD, n - r0);
-    for (int idx = m; idx < kD * kD; idx += kD) {
-        const int j = idx / kD, i = idx % kD;  // consecutive threads: consecutive rows of column j
-        Us[j][i] = (i <= j && j < D) ? L[(r0 + i) + (lc + j) * ldl] : 0.0;
-    }
-    __syncthreads();
-    rd[m] = m < D ? 1.0 / Us[m][m] : 0.0;
-    __syncthreads();
-    const bool act = m < D;
-    double acc[kD];
-#pragma unroll
-    for (int i = 0; i < kD; ++i) acc[i] = i == m ? 1.0 : 0.0;
-#pragma unroll
-    for (int j = kD - 1; j >= 0; --j) {
-        if (act && j <= m) {
-            acc[j] *= rd[j];  // w_j
-#pragma unroll
-            for (int i = 0; i < j; ++i) acc[i] = fma(-Us[j][i], acc[j], acc[i]);
-        }
-    }
-    double *w = W + (int64_t)sl * kD * kD;
-#pragma unroll
-    for (int j = 0; j < kD; ++j) w[j * kD + m] = (act && j <= m) ? acc[j] : 0.0;
+    pinv_block(L + r0 + lc * ldl, ldl, D, W + (int64_t)sl * kD * kD, Us, rd);
 }
 
 // Every rank: residuals of its strips right of solve block g -= L_{rows of g, strip}^T P,
