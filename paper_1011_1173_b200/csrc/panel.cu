@@ -1294,13 +1294,15 @@ struct Aux {
     cudaStream_t s = nullptr;
     cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
 };
-std::map<int, Aux> g_aux;
-gcm_status_t aux_stream(cudaStream_t *s, cudaEvent_t **ready, cudaEvent_t **done) {
+// keyed by (device, call stream) like the workspaces: calls on different streams (host threads)
+// never share the auxiliary stream or its events
+std::map<std::pair<int, cudaStream_t>, Aux> g_aux;
+gcm_status_t aux_stream(cudaStream_t call, cudaStream_t *s, cudaEvent_t **ready, cudaEvent_t **done) {
     int dev = 0;
     gcm_status_t st = check_cuda(cudaGetDevice(&dev));
     if (st != GCM_OK) return st;
     std::lock_guard<std::mutex> lock(g_aux_mutex);
-    Aux &a = g_aux[dev];
+    Aux &a = g_aux[{dev, call}];
     if (!a.s) {
         st = check_cuda(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
         for (int i = 0; i < 2 && st == GCM_OK; ++i) {
@@ -1529,7 +1531,7 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         if (use_pchain) {
             cudaStream_t aux = nullptr;
             cudaEvent_t *ev_a = nullptr, *ev_b = nullptr;
-            st = aux_stream(&aux, &ev_a, &ev_b);
+            st = aux_stream(stream, &aux, &ev_a, &ev_b);
             if (st != GCM_OK) return st;
             // GCM_PCHAIN_RESERVE=<m>: SMs kept free of chain CTAs for the overlapped tail (default 0)
             const char *re = std::getenv("GCM_PCHAIN_RESERVE");
@@ -1541,7 +1543,7 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         } else {
             cudaStream_t aux = nullptr;
             cudaEvent_t *p_ready = nullptr, *rest_done = nullptr;
-            st = aux_stream(&aux, &p_ready, &rest_done);
+            st = aux_stream(stream, &aux, &p_ready, &rest_done);
             if (st != GCM_OK) return st;
             st = check_cuda(cudaEventRecord(p_ready[1], stream));  // the aux stream starts after this call's prologue
             if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(aux, p_ready[1], 0));

@@ -194,3 +194,27 @@ def test_panel_launch_chain_one_rank(gd, n, k, monkeypatch):
         torch.cuda.synchronize()
         assert col_scaled_max(upper(L.cpu().numpy()), upper(Lo)) <= 1e-12
         assert row_scaled_max(V.cpu().numpy(), Vo) <= 1e-11
+
+
+@pytest.mark.parametrize("pchain", ["1", "0"])
+def test_panel_two_streams(gd, pchain, monkeypatch):
+    """Two GCM_ALGO_PANEL calls in flight at once on two CUDA streams: each call has its own
+    workspace and auxiliary stream/events (keyed by device and call stream), so neither waits
+    on or overwrites the other's hand-offs."""
+    gcm, _ = gd
+    monkeypatch.setenv("GCM_PCHAIN", pchain)
+    cases = []
+    for i, (n, k) in enumerate([(1800, 16), (1500, 9)]):
+        Lbuf, Vbuf, _ = synth.paper_instance(n, k, 1, seed=100 + i, lower_fill=np.nan)
+        Lo, Vo = Lbuf.copy(), Vbuf.copy()
+        oracle.modify_a(Lo, Vo, 1)
+        cases.append((torch.from_numpy(Lbuf).cuda(), torch.from_numpy(Vbuf).cuda(), Lo, Vo))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for (L, V, _, _), st in zip(cases, streams):
+        with torch.cuda.stream(st):
+            gcm.modify(L, V, 1, algo="panel", stream=st)
+    torch.cuda.synchronize()
+    for L, V, Lo, Vo in cases:
+        assert col_scaled_max(upper(L.cpu().numpy()), upper(Lo)) <= 1e-12
+        assert row_scaled_max(V.cpu().numpy(), Vo) <= 1e-11
