@@ -101,3 +101,17 @@ def test_gloo_plan_covers_the_factor_once(tmp_path, world):
         assert sorted(tiles) == sorted((b, s) for s in range(NB) for b in range(s))
         assert sorted(diag) == list(range(NB))
         assert sorted(solve) == list(range(NBc))
+
+
+@pytest.mark.parametrize("n,nb", [(3000, 512), (1000, 256), (700, 64)])
+def test_one_rank_plan_sorted_by_row_block(n, nb):
+    """One rank (the persistent chain's overlapped tail takes Apply items row block by row block):
+    the plan's Apply items cover every tile (b, s), b < s, exactly once, and each of the two item
+    lists (TMA groups, then single tiles) is ordered by row block b."""
+    from paper_1011_1173_b200 import dist as gdist
+    pairs = gdist.plan(n, nb, 1, 0, "tiles")
+    NB = (n + 63) // 64
+    assert sorted(map(tuple, pairs.tolist())) == sorted((b, s) for s in range(NB) for b in range(s))
+    bs = pairs[:, 0]
+    runs = 1 + int(np.sum(bs[1:] < bs[:-1]))
+    assert runs <= 2
