@@ -37,9 +37,11 @@ if nt > 4:
     hp = hp[:nt]
     per = np.diff(hp[:, 0])
     print(f"helper CTA 40: {nt} tiles, period median {np.median(per):.0f} ns")
-    for i, nm in [(1, "P in smem"), (2, "tile landed"), (3, "MMA + epilogue")]:
+    for i, nm in [(1, "P in smem"), (2, "tile landed"), (3, "MMA (warp 0)")]:
         d = hp[2:, i] - hp[2:, i - 1]
         print(f"  {nm:16s} +{np.median(d):7.0f} ns (p90 {np.percentile(d, 90):7.0f})")
+    ep = hp[3:, 0] - hp[2:-1, 3]
+    print(f"  epilogue + next top +{np.median(ep):7.0f} ns")
     # when did P_b become visible vs the solver's publish of step b (tile b of this helper)
     pub = tr[:, 3]
     lag = [hp[q, 1] - pub[q] for q in range(min(nt, NB)) if pub[q] > 0]
