@@ -159,9 +159,10 @@ gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     // the chain-shortened path wins once there is more
     // than a handful of row blocks; tiny factors keep the two-kernel sweep; large factors
     // take the column-block (panel) algorithm, whose solve chain and residual updates run on
-    // the FP64 tensor cores (profiles/r02bj_crossover.txt: level with BLOCKED at n = 8000 for
-    // k <= 16 and n = 10000 for k = 32; n = 16000, k = 32: 2.65 vs 3.33 ms).
-    if (n >= (k <= 16 ? 8000 : 11000)) return GCM_ALGO_PANEL;
+    // the FP64 tensor cores and whose sweeps and Apply overlap the chain on parallel streams
+    // (profiles/r02bz_crossover.txt: level with BLOCKED at n ~ 6500; n = 10000, k = 32: 1.18 vs
+    // 1.47 ms).
+    if (n >= 6500) return GCM_ALGO_PANEL;
     return n >= 256 ? GCM_ALGO_BLOCKED : GCM_ALGO_SWEEP;
 }
 

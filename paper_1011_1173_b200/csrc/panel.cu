@@ -1290,9 +1290,13 @@ struct Exchange {
 // The library's auxiliary stream on the current device (the residual updates that overlap the
 // next diagonal solve) and two event pairs for the hand-offs between it and the call's stream.
 std::mutex g_aux_mutex;
+constexpr int kTailStreams = 8;
 struct Aux {
     cudaStream_t s = nullptr;
     cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+    // the persistent chain's overlapped tail: one stream per chunk, its prefix-Gram and done events
+    cudaStream_t par[kTailStreams] = {};
+    cudaEvent_t scan[kTailStreams] = {}, pdone[kTailStreams] = {};
 };
 // keyed by (device, call stream) like the workspaces: calls on different streams (host threads)
 // never share the auxiliary stream or its events
@@ -1309,12 +1313,24 @@ gcm_status_t aux_stream(cudaStream_t call, cudaStream_t *s, cudaEvent_t **ready,
             st = check_cuda(cudaEventCreateWithFlags(&a.ready[i], cudaEventDisableTiming));
             if (st == GCM_OK) st = check_cuda(cudaEventCreateWithFlags(&a.done[i], cudaEventDisableTiming));
         }
+        for (int i = 0; i < kTailStreams && st == GCM_OK; ++i) {
+            st = check_cuda(cudaStreamCreateWithFlags(&a.par[i], cudaStreamNonBlocking));
+            if (st == GCM_OK) st = check_cuda(cudaEventCreateWithFlags(&a.scan[i], cudaEventDisableTiming));
+            if (st == GCM_OK) st = check_cuda(cudaEventCreateWithFlags(&a.pdone[i], cudaEventDisableTiming));
+        }
         if (st != GCM_OK) return st;
     }
     *s = a.s;
     *ready = a.ready;
     *done = a.done;
     return GCM_OK;
+}
+// the tail streams and events of (device, call stream) (created by aux_stream)
+Aux *aux_of(cudaStream_t call) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) clear_stale_error();
+    std::lock_guard<std::mutex> lock(g_aux_mutex);
+    return &g_aux[{dev, call}];
 }
 
 // GCM_PANEL_TRACE=1 (debug): timing events around every solve block's kernels (solve, lookahead
@@ -1419,19 +1435,29 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
     gcm_status_t st = check_cuda(
         cudaFuncSetAttribute(papply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t2));
     if (st != GCM_OK) return st;
-    // row blocks per chunk: a chunk's sweeps and Apply are latency-bound waves, so few chunks
-    // (GCM_PCHAIN_CHUNKS, default 2)
+    // chunks (GCM_PCHAIN_CHUNKS, default 8): all but the last on their own tail streams, in
+    // parallel with each other and the chain (profiles/r02by_tail_chunks.txt)
     const char *ce = std::getenv("GCM_PCHAIN_CHUNKS");
-    const int want = ce ? std::max(1, std::atoi(ce)) : 2;
+    const int want = std::min(kTailStreams + 1, ce ? std::max(1, std::atoi(ce)) : 8);
     const int cs = std::max(4, (NB64 + want - 1) / want);
+    Aux *ax = aux_of(stream);
     ApplyMap map{q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff), q.plan.nloc};
-    auto chunk = [&](int B0, int B1, cudaStream_t s, bool wait) -> gcm_status_t {
+    auto chunk = [&](int B0, int B1, cudaStream_t s, bool wait, cudaEvent_t scan_wait,
+                     cudaEvent_t scan_rec) -> gcm_status_t {
         if (wait) {
             pwait_rows_kernel<<<1, 64, 0, s>>>(q.at<unsigned>(q.cv.rowcnt), B0, B1, NB64, NS);
             count_launch();
         }
         pgram_kernel<KB><<<B1 - B0, KB * KB <= 1024 ? KB * KB : 1024, 0, s>>>(q.Pbuf(), n, k, q.at<double>(q.cv.Q), B0);
+        if (scan_wait) {  // the previous chunk's prefix (G continues across chunks)
+            const gcm_status_t s2 = check_cuda(cudaStreamWaitEvent(s, scan_wait, 0));
+            if (s2 != GCM_OK) return s2;
+        }
         pscan_range_kernel<KB><<<1, KB * KB, 0, s>>>(q.at<double>(q.cv.Q), B0, B1, q.at<double>(q.cv.G));
+        if (scan_rec) {
+            const gcm_status_t s2 = check_cuda(cudaEventRecord(scan_rec, s));
+            if (s2 != GCM_OK) return s2;
+        }
         pdiag_kernel<KB><<<B1 - B0, kDiagThreads, pdiag_smem<KB>(), s>>>(
             q.L, q.ldl, n, q.V, std::max<int64_t>(q.plan.nloc, 1), k, sigma, q.Pbuf(), q.Ubuf(),
             q.at<double>(q.cv.G), q.panbuf(), q.at<unsigned long long>(q.cv.key), ebase, q.at<int>(q.cv.dlb) + B0,
@@ -1452,15 +1478,22 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
         }
         return check_cuda(cudaGetLastError());
     };
+    // chunk c (all but the last) on tail stream c: its sweeps and Apply run in parallel with the
+    // other chunks' (only the prefix-Gram scan is ordered across chunks, by events)
+    (void)aux;
+    (void)aux_done;
     const int nchunks = (NB64 + cs - 1) / cs;
-    if (nchunks > 1) {
-        st = check_cuda(cudaStreamWaitEvent(aux, armed, 0));
-        for (int c = 0; c + 1 < nchunks && st == GCM_OK; ++c) st = chunk(c * cs, (c + 1) * cs, aux, true);
-        if (st == GCM_OK) st = check_cuda(cudaEventRecord(aux_done, aux));
-        if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(stream, aux_done, 0));
-        if (st != GCM_OK) return st;
+    for (int c = 0; c + 1 < nchunks && st == GCM_OK; ++c) {
+        cudaStream_t s = ax->par[c];
+        st = check_cuda(cudaStreamWaitEvent(s, armed, 0));
+        if (st == GCM_OK)
+            st = chunk(c * cs, (c + 1) * cs, s, true, c > 0 ? ax->scan[c - 1] : nullptr, ax->scan[c]);
+        if (st == GCM_OK) st = check_cuda(cudaEventRecord(ax->pdone[c], s));
     }
-    return chunk((nchunks - 1) * cs, NB64, stream, false);  // after the chain (stream order)
+    if (st != GCM_OK) return st;
+    st = chunk((nchunks - 1) * cs, NB64, stream, false, nchunks > 1 ? ax->scan[nchunks - 2] : nullptr, nullptr);
+    for (int c = 0; c + 1 < nchunks && st == GCM_OK; ++c) st = check_cuda(cudaStreamWaitEvent(stream, ax->pdone[c], 0));
+    return st;
 }
 
 // one pass (<= 32 update columns) over all ranks of `rk` (Virtual: all R; else rk has one entry)
