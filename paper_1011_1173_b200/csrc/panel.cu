@@ -733,6 +733,11 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
 // (the solver on hand-offs of earlier tiles, helpers on P blocks the solver publishes without
 // waiting for them), so the cooperative grid cannot deadlock.
 constexpr int kPcT = 512;
+#ifndef GCM_PC_REL
+#define GCM_PC_REL 4
+#endif
+constexpr int kPcRel = GCM_PC_REL;  // helper tiles per rowcnt release
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 #ifdef GCM_PC_TRACE  // solver step timeline (globaltimer ns): tools/pchain_trace.py
 __device__ long long g_pc_trace[4096 * 4];
 __device__ __forceinline__ long long pc_now() {
@@ -762,7 +767,7 @@ struct PcShape {
     static constexpr int TPW = (8 * ET + 15) / 16;
     static constexpr int OWN = KB >= 32 ? 5 : 10;  // helper strips whose residual stays in shared memory
     static constexpr int NS = NE / 8;  // solver CTAs
-    static constexpr size_t solver_doubles = 4 * kD * LDW + 3 * kD * 12;  // 2 W, 2 lookahead tiles, q, r
+    static constexpr size_t solver_doubles = 4 * kD * LDW + 5 * kD * 12;  // 2 W, 2 lookahead tiles, 2 q, r, 2 hand-off
     static constexpr size_t helper_doubles = 2 * kD * LDW + kD * LDR + (OWN + 2) * kD * LDR;  // + spill slots
     static constexpr size_t doubles = solver_doubles > helper_doubles ? solver_doubles : helper_doubles;
 };
@@ -794,11 +799,12 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
     const int c = ct * 8 + gi;
     auto ecol = [&](int v, int h) { return (eg * TPW + v) * 8 + 2 * tg + h; };
     // L(rows of block rb, columns of block cb) -> dst[c][m] (column-major, stride LDW), zero outside
-    auto load_tile = [&](double *dst, int rb, int cb) {
+    auto load_tile = [&](double *dst, int rb, int cb, int tid = -1, int nthr = kPcT) {
+        if (tid < 0) tid = t;
         const int64_t r0 = (int64_t)rb * kD, c0 = (int64_t)cb * kD;
         const int Dr = (int)imin64(kD, n - r0), Dc = (int)imin64(kD, n - c0);
         if (v16) {
-            for (int idx = t; idx < kD * kD / 2; idx += kPcT) {
+            for (int idx = tid; idx < kD * kD / 2; idx += nthr) {
                 const int cc = idx >> 5, m = 2 * (idx & 31);
                 const int bytes = (cc < Dc && m < Dr) ? (Dr - m >= 2 ? 16 : 8) : 0;
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst + cc * LDW + m)),
@@ -806,7 +812,7 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                              : "memory");
             }
         } else {
-            for (int idx = t; idx < kD * kD; idx += kPcT) {
+            for (int idx = tid; idx < kD * kD; idx += nthr) {
                 const int cc = idx >> 6, m = idx & 63;
                 cp8(dst + cc * LDW + m, L + (r0 + m) + (c0 + cc) * ldl, cc < Dc && m < Dr);
             }
@@ -845,7 +851,7 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         auto load_w = [&](int b) {
             const double *src = Winv + (int64_t)b * kD * kD;
             double *dst = Ws + (b & 1) * kD * LDW;
-            for (int idx = t; idx < kD * kD / 2; idx += kPcT) {
+            for (int idx = t - 256; idx < kD * kD / 2; idx += 256) {  // issued by the poller warps
                 const int j = idx >> 5, m = 2 * (idx & 31);
                 cp16(dst + j * LDW + m, src + j * kD + m);
             }
@@ -857,68 +863,72 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
 #pragma unroll 4
             for (int m0 = 0; m0 < kD; m0 += 4) dmma_884(a2, la[m0], qb[m0 * LDQ]);
         };
-        // strip b's hand-off values of this lane (V for b < 2), issued a step ahead
-        unsigned long long rn[2];
-        auto issue_hand = [&](int b) {
+        // warps 8..15 poll strip b+1's hand-off (V for b + 1 < 2) from the top of step b into hs[(b+1) % 2]
+        // and store it as checkpoint (b, b+1): the poll runs under step b's MMA work, so at step b+1
+        // the value is in shared memory instead of one exposed L2 round trip away
+        double *hs = rb + kD * LDQ;         // [2][kD][LDQ]
+        const int pr = (t - 256) >> 2, pe = 2 * ((t - 256) & 3);  // poller: row, column pair
+        auto poll_hand = [&](int b) {
             const int64_t r0 = (int64_t)b * kD;
             const int Db = (int)imin64(kD, n - r0);
-            const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)sc * k + es;
+            const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)pr * k + es;
+            double *ck = b >= 1 ? chk + (chkoff[b] + b - 1) * kD * k + (int64_t)pr * k + es : nullptr;
+            unsigned long long u[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int e = 2 * tg + h;
-                rn[h] = (sc < Db && es + e < k) ? ld_relaxed_u64(src + e) : 0ull;
+                const int e = pe + h;
+                u[h] = (pr < Db && es + e < k) ? ld_relaxed_u64(src + e) : 0ull;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int e = pe + h;
+                if (b >= 2 && pr < Db && es + e < k && u[h] == kEmpty) u[h] = __double_as_longlong(ld_value(src + e));
+                const double r = __longlong_as_double((long long)u[h]);
+                hs[(b & 1) * kD * LDQ + pr * LDQ + e] = r;
+                if (ck && pr < Db && es + e < k) ck[e] = r;
             }
         };
-        load_w(0);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        if (sw) issue_hand(0);
-        int64_t ckn = chkoff[0];  // checkpoint offset of strip b, loaded a step ahead (a global load
-                                  // issued just before its use stalled the step on its latency)
+        if (!sw) {
+            load_w(0);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            poll_hand(0);
+        }
         for (int b = 0; b < NB; ++b) {
-            const int64_t ckb = ckn;
-            if (b + 1 < NB) ckn = chkoff[b + 1];
             const int64_t r0 = (int64_t)b * kD;
             const int Db = (int)imin64(kD, n - r0);
-            // W_b and L_{b-1,b} were issued at the top of step b - 1
+            // W_b and L_{b-1,b} were issued at the top of step b - 1; r_b was polled under step b - 1
             PC_MARK(b, 0);
             asm volatile("cp.async.wait_group 0;" ::: "memory");
             __syncthreads();  // also: step b - 1's reads of the buffers refilled next are done
             PC_MARK(b, 1);
-            if (b + 1 < NB) {  // the next step's W and lookahead tile fly under this whole step
-                load_w(b + 1);
-                load_tile(Lt + ((b + 1) & 1) * kD * LDW, b, b + 1);
-                asm volatile("cp.async.commit_group;" ::: "memory");
-            }
-            if (sw) {
-                // r_b: V for b < 2, else strip b's hand-off (its residual after P_{<= b-2};
-                // self-validating) = the checkpoint of tile (b - 1, b)
-                const double *src = (b < 2 ? res : hand) + r0 * k + (int64_t)sc * k + es;
-                double *ck1 = b >= 1 ? chk + (ckb + b - 1) * kD * k + (int64_t)sc * k + es : nullptr;
-                double acc[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int e = 2 * tg + h;
-                    unsigned long long u = rn[h];
-                    if (b >= 2 && sc < Db && es + e < k && u == kEmpty) u = __double_as_longlong(ld_value(src + e));
-                    const double r = __longlong_as_double((long long)u);
-                    acc[h] = -r;
-                    if (ck1 && sc < Db && es + e < k) ck1[e] = r;
+            if (!sw) {
+                if (b + 1 < NB) {  // the next step's W and lookahead tile fly under this whole step (the
+                                   // poller warps issue them: the MMA warps never stall on copy issue)
+                    load_w(b + 1);
+                    load_tile(Lt + ((b + 1) & 1) * kD * LDW, b, b + 1, t - 256, 256);
+                    asm volatile("cp.async.commit_group;" ::: "memory");
                 }
-                PC_MARK(b, 2);
-                if (b >= 1) mma8(acc, Lt + (b & 1) * kD * LDW, qh + ((b - 1) & 1) * kD * LDQ);
+                if (b >= 2 && t == 256) {  // tile (b-2, b-1): checkpoint written, L_{b-2,b-1} consumed
+                    fence_acq_rel_gpu();
+                    atomicAdd(rowcnt + (b - 2), 1u);
+                }
+                if (b + 1 < NB) poll_hand(b + 1);
+                continue;
+            }
+            // r_b = strip b's hand-off (its residual after P_{<= b-2}), minus L_{b-1,b}^T q_{b-1}
+            double acc[2];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) rb[sc * LDQ + 2 * tg + h] = -acc[h];  // r^{(b)}
-            }
-            __syncthreads();
-            if (b >= 1 && t == 0) {  // tile (b-1, b): checkpoint written, L_{b-1,b} consumed
-                __threadfence();
-                atomicAdd(rowcnt + (b - 1), 1u);
-            }
+            for (int h = 0; h < 2; ++h) acc[h] = -hs[(b & 1) * kD * LDQ + sc * LDQ + 2 * tg + h];
+            PC_MARK(b, 2);
+            if (b >= 1) mma8(acc, Lt + (b & 1) * kD * LDW, qh + ((b - 1) & 1) * kD * LDQ);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) rb[sc * LDQ + 2 * tg + h] = -acc[h];  // r^{(b)}
+            named_bar(1, 256);
             // q_b = W^T r^{(b)} (DMMA above the 8-row diagonal tiles, masked DFMA on them, so a
             // product 0 * r_j with j > m is never formed)
             const double *Wb = Ws + (b & 1) * kD * LDW;
             double *qv = qh + (b & 1) * kD * LDQ;
-            if (sw) {
+            {
                 const int m0 = warp * 8;
                 double qa[2] = {0.0, 0.0};
                 for (int j0 = 0; j0 < m0; j0 += 4) dmma_884(qa, Wb[(j0 + tg) * LDW + m0 + gi], rb[(j0 + tg) * LDQ + gi]);
@@ -940,9 +950,13 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                     qv[m * LDQ + e] = s;
                     if (m < Db && es + e < k) st_value(P + (r0 + m) * k + es + e, s);  // published
                 }
-                if (b + 1 < NB) issue_hand(b + 1);  // in flight under the next step's wait
             }
             PC_MARK(b, 3);
+        }
+        __syncthreads();
+        if (NB >= 2 && t == 256) {  // tile (NB-2, NB-1)
+            fence_acq_rel_gpu();
+            atomicAdd(rowcnt + (NB - 2), 1u);
         }
         return;
     }
@@ -983,8 +997,9 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
     It cur{0, 0};
     stage(cur, 0, false);  // (the residual slots' copies are in this first group)
     int buf = 0, pb = -1, seq = 0;
-    // P values of the next tile row, loaded one tile ahead (self-validating: a non-empty
-    // value is final; the rest are polled when that row's first tile starts)
+    int rel_b[kPcRel], nrel = 0;  // thread 0: tile rows whose rowcnt release is pending
+    // P values of the next tile row, loaded ahead (self-validating: a non-empty value is final;
+    // the rest are polled when that row's first tile starts)
     constexpr int PPT = (kD * NE + kPcT - 1) / kPcT;
     unsigned long long pn[PPT];
     int pn_b = -1;
@@ -1013,7 +1028,6 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
             unsigned long long u[PPT];
 #pragma unroll
             for (int q = 0; q < PPT; ++q) u[q] = pn[q];
-            if (valid(nx) && nx.b != b) issue_p(nx.b);  // the next row's P, under this tile
 #pragma unroll
             for (int q = 0; q < PPT; ++q) {
                 const int o = t + q * kPcT, m = o / NE, e = o % NE;
@@ -1023,8 +1037,6 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                 }
             }
             pb = b;
-        } else if (valid(nx) && nx.b != b && pn_b != nx.b) {
-            issue_p(nx.b);
         }
         PH_MARK(seq, 1);
         if (valid(nx)) asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -1034,23 +1046,16 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         double *Rt = Rs + (i < S::OWN ? i : S::OWN + buf) * kD * LDR;
         const int Dc = (int)imin64(kD, n - (int64_t)s * kD);
         if (mma_warp) {
-            double acc[TPW][2];
+            double acc[TPW][2], r_in[TPW][2];
 #pragma unroll
             for (int v = 0; v < TPW; ++v)
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) acc[v][hh] = -Rt[c * LDR + ecol(v, hh)];
+                for (int hh = 0; hh < 2; ++hh) {
+                    r_in[v][hh] = Rt[c * LDR + ecol(v, hh)];
+                    acc[v][hh] = -r_in[v][hh];
+                }
             mma_tile(acc, Lh + buf * kD * LDW, Ph);
             PH_MARK(seq, 3);
-            if (b >= 1) {  // checkpoint (b, s): the residual before this tile (still in Rt)
-                double *ck = chk + (cks + b) * kD * k + (int64_t)c * k;
-#pragma unroll
-                for (int v = 0; v < TPW; ++v)
-#pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int e = ecol(v, hh);
-                        if (c < Dc && e < k) ck[e] = Rt[c * LDR + e];
-                    }
-            }
             const bool hoff = b == s - 2;
             double *rg = res + (int64_t)s * kD * k + (int64_t)c * k;
             double *hg = hand + (int64_t)s * kD * k + (int64_t)c * k;
@@ -1066,12 +1071,31 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
                         if (hoff) st_value(hg + e, -acc[v][hh]);  // strip s's hand-off to the solver
                     }
                 }
+            if (b >= 1) {  // checkpoint (b, s): the residual before this tile (after the hand-off stores)
+                double *ck = chk + (cks + b) * kD * k + (int64_t)c * k;
+#pragma unroll
+                for (int v = 0; v < TPW; ++v)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int e = ecol(v, hh);
+                        if (c < Dc && e < k) ck[e] = r_in[v][hh];
+                    }
+            }
         }
-        __threadfence_block();  // spilled residuals: stores before a later tile's copies read them
+        // the next row's P, issued after this tile's MMA (issued at the tile's top it came back
+        // empty whenever the helpers trail the solver by less than a step, and was polled again)
+        if (valid(nx) && nx.b != b && pn_b != nx.b) issue_p(nx.b);
+        asm volatile("fence.acq_rel.cta;" ::: "memory");  // spilled residuals: stores before a later tile's copies read them
         __syncthreads();
-        if (t == 0) {  // tile (b, s): checkpoint written, L tile consumed (the overlapped Apply's cue)
-            __threadfence();
-            atomicAdd(rowcnt + b, 1u);
+        if (t == 0) {  // tile (b, s): checkpoint written, L tile consumed (the overlapped Apply's cue),
+                       // released every kPcRel tiles: one fence (an L2 round trip on this CTA's
+                       // critical path) per kPcRel tiles, the counts are fire-and-forget
+            rel_b[nrel++] = b;
+            if (nrel == kPcRel || !valid(nx)) {
+                fence_acq_rel_gpu();
+                for (int q = 0; q < nrel; ++q) atomicAdd(rowcnt + rel_b[q], 1u);
+                nrel = 0;
+            }
         }
         cur = nx;
         buf ^= 1;
