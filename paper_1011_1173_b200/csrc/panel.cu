@@ -96,6 +96,8 @@ struct Plan {
     int64_t sb;                             // solve-block height (<= nb, dsolve's shared-memory cap)
     int NSB;                                // solve blocks
     std::vector<int> first_strip_after;     // per solve block: first local strip right of it
+    unsigned char *img = nullptr;           // pinned host image of the device layout arrays (gstrip ..
+    size_t img_bytes = 0;                   //   tiles at their carve offsets): one async upload per call
 };
 
 // rows of one dsolve launch: its residuals live in shared memory (kDsMaxRows x KB doubles)
@@ -829,11 +831,23 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
     auto mma_tile = [&](double (&acc)[TPW][2], const double *A, const double *B) {
         const double *la = A + c * LDW + tg;
         const double *qb = B + tg * LDR + eg * TPW * 8 + gi;
-#pragma unroll 4
-        for (int m0 = 0; m0 < kD; m0 += 4) {
-            const double af = la[m0];
+        double acc2[TPW][2];  // two accumulator chains (k-steps m0 = 0, 8, .. and 4, 12, ..): half the
+                              // dependent DMMA latency on the chain's critical path
 #pragma unroll
-            for (int v = 0; v < TPW; ++v) dmma_884(acc[v], af, qb[m0 * LDR + v * 8]);
+        for (int v = 0; v < TPW; ++v) acc2[v][0] = acc2[v][1] = 0.0;
+#pragma unroll 2
+        for (int m0 = 0; m0 < kD; m0 += 8) {
+            const double af = la[m0], ag = la[m0 + 4];
+#pragma unroll
+            for (int v = 0; v < TPW; ++v) {
+                dmma_884(acc[v], af, qb[m0 * LDR + v * 8]);
+                dmma_884(acc2[v], ag, qb[(m0 + 4) * LDR + v * 8]);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < TPW; ++v) {
+            acc[v][0] += acc2[v][0];
+            acc[v][1] += acc2[v][1];
         }
     };
 
@@ -860,8 +874,14 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
         auto mma8 = [&](double (&a2)[2], const double *A, const double *B) {
             const double *la = A + sc * LDW + tg;
             const double *qb = B + tg * LDQ + gi;
-#pragma unroll 4
-            for (int m0 = 0; m0 < kD; m0 += 4) dmma_884(a2, la[m0], qb[m0 * LDQ]);
+            double b2[2] = {0.0, 0.0};  // second accumulator chain (as mma_tile)
+#pragma unroll 2
+            for (int m0 = 0; m0 < kD; m0 += 8) {
+                dmma_884(a2, la[m0], qb[m0 * LDQ]);
+                dmma_884(b2, la[m0 + 4], qb[(m0 + 4) * LDQ]);
+            }
+            a2[0] += b2[0];
+            a2[1] += b2[1];
         };
         // warps 8..15 poll strip b+1's hand-off (V for b + 1 < 2) from the top of step b into hs[(b+1) % 2]
         // and store it as checkpoint (b, b+1): the poll runs under step b's MMA work, so at step b+1
@@ -1104,14 +1124,23 @@ __global__ void __launch_bounds__(kPcT, 1) pchain_kernel(const double *__restric
 }
 
 // Q_b = P_b^T P_b per 64-row block (KB x KB, zero padded)
+// (the block's P rows are staged in shared memory by coalesced loads, all in flight at once: the
+// per-entry loop over global rows was a chain of 64 L2 latencies on the tail's critical path)
 template <int KB>
 __global__ void pgram_kernel(const double *__restrict__ P, int64_t n, int k, double *Q, int b0 = 0) {
+    __shared__ double Ps[kD][KB + 1];
     const int b = b0 + blockIdx.x;
+    const int64_t r0 = (int64_t)b * kD;
+    const int Db = (int)imin64(kD, n - r0);
+    for (int o = threadIdx.x; o < kD * KB; o += blockDim.x) {
+        const int m = o / KB, e = o % KB;
+        Ps[m][e] = (m < Db && e < k) ? P[(r0 + m) * k + e] : 0.0;
+    }
+    __syncthreads();
     for (int o = threadIdx.x; o < KB * KB; o += blockDim.x) {
         const int i = o / KB, j = o % KB;
         double s = 0.0;
-        if (i < k && j < k)
-            for (int64_t m = (int64_t)b * kD; m < n && m < (int64_t)(b + 1) * kD; ++m) s = fma(P[m * k + i], P[m * k + j], s);
+        for (int m = 0; m < Db; ++m) s = fma(Ps[m][i], Ps[m][j], s);
         Q[(int64_t)b * KB * KB + o] = s;
     }
 }
@@ -1784,7 +1813,32 @@ const Plan &get_plan(int64_t n, int64_t nb, int R, int r, int k, bool tma) {
     std::lock_guard<std::mutex> lock(g_plan_mutex);
     auto key = std::make_tuple(n, nb, R, r, k, tma);
     auto it = g_plans.find(key);
-    if (it == g_plans.end()) it = g_plans.emplace(key, make_plan(n, nb, R, r, k, tma)).first;
+    if (it == g_plans.end()) {
+        it = g_plans.emplace(key, make_plan(n, nb, R, r, k, tma)).first;
+        Plan &p = it->second;
+        const Carve c = carve(p);
+        const size_t bytes = c.total - c.gstrip;
+        void *h = nullptr;
+        // pageable uploads are staged by the host, one copy at a time (tens of us per call before
+        // the first kernel); a failed pinned allocation keeps that path (upload() below)
+        if (cudaHostAlloc(&h, bytes, cudaHostAllocDefault) == cudaSuccess) {
+            unsigned char *img = static_cast<unsigned char *>(h);
+            std::memset(img, 0, bytes);
+            auto put = [&](size_t off, const void *src, size_t n_bytes) {
+                if (n_bytes) std::memcpy(img + (off - c.gstrip), src, n_bytes);
+            };
+            put(c.gstrip, p.gstrip.data(), p.gstrip.size() * 4);
+            put(c.chkoff, p.chkoff.data(), p.chkoff.size() * 8);
+            put(c.dlb, p.dl_b.data(), p.dl_b.size() * 4);
+            put(c.dllc, p.dl_lc.data(), p.dl_lc.size() * 8);
+            put(c.full, p.full.data(), p.full.size() * 8);
+            put(c.tiles, p.tiles.data(), p.tiles.size() * 8);
+            p.img = img;
+            p.img_bytes = bytes;
+        } else {
+            (void)cudaGetLastError();
+        }
+    }
     return it->second;
 }
 
@@ -1792,6 +1846,7 @@ gcm_status_t upload(const Rank &q, cudaStream_t stream) {
     auto up = [&](size_t off, const void *src, size_t bytes) {
         return bytes ? check_cuda(cudaMemcpyAsync(q.ws + off, src, bytes, cudaMemcpyHostToDevice, stream)) : GCM_OK;
     };
+    if (q.plan.img) return up(q.cv.gstrip, q.plan.img, q.plan.img_bytes);  // one pinned async copy
     gcm_status_t st = up(q.cv.gstrip, q.plan.gstrip.data(), q.plan.gstrip.size() * 4);
     if (st == GCM_OK) st = up(q.cv.chkoff, q.plan.chkoff.data(), q.plan.chkoff.size() * 8);
     if (st == GCM_OK) st = up(q.cv.dlb, q.plan.dl_b.data(), q.plan.dl_b.size() * 4);
@@ -2135,5 +2190,11 @@ gcm_status_t gcm_modify_dist(gcm_comm_t, double *, int64_t, int64_t, int64_t, do
 #ifdef GCM_PC_TRACE
 extern "C" int gcm_debug_pc_trace(long long *host, int count) {
     return (int)cudaMemcpyFromSymbol(host, gcm::g_pc_trace, sizeof(long long) * count);
+}
+#endif
+#ifdef GCM_TRACE
+// this translation unit's copy of the diagonal-block phase marks (pdiag_kernel): tools/pdiag_phases.py
+extern "C" int gcm_debug_dtrace_panel(long long *host, int count) {
+    return (int)cudaMemcpyFromSymbol(host, gcm::g_dtrace, sizeof(long long) * count);
 }
 #endif
