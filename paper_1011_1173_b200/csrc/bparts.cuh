@@ -289,10 +289,16 @@ __device__ void bdiag_body(double *__restrict__ L, int64_t n, int64_t ldl, doubl
 __device__ __forceinline__ void pinv_block(const double *__restrict__ Lb, int64_t ldl, int D, double *w,
                                            double (*Us)[kD], double *rd) {
     const int m = threadIdx.x;
+    // the block by asynchronous copies, all 64 per thread in flight at once (zero-filled outside
+    // the triangle); a load-then-store loop waited one memory latency per few elements
     for (int idx = m; idx < kD * kD; idx += kD) {
         const int j = idx / kD, i = idx % kD;  // consecutive threads: consecutive rows of column j
-        Us[j][i] = (i <= j && j < D) ? Lb[i + (int64_t)j * ldl] : 0.0;
+        const bool ok = i <= j && j < D;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((unsigned)__cvta_generic_to_shared(&Us[j][i])),
+                     "l"(ok ? Lb + i + (int64_t)j * ldl : Lb), "r"(ok ? 8 : 0)
+                     : "memory");
     }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     rd[m] = m < D ? 1.0 / Us[m][m] : 0.0;
     __syncthreads();

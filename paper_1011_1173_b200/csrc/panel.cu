@@ -27,6 +27,8 @@
 // (~(2*64*k + 64 + k) doubles per 64-row block), both written by the producing kernel
 // itself.  Layout: 1-D block-cyclic over columns (gcm.h), V rows follow their columns.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -174,6 +176,38 @@ Plan make_plan(int64_t n, int64_t nb, int R, int r, int k, bool tma_groups) {
 }
 
 // workspace carve-up of one rank (byte offsets)
+// GCM_HOST_TRACE=1: host timestamps of the panel path's enqueue steps (stderr, one line per call)
+struct HostTrace {
+    bool on = std::getenv("GCM_HOST_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    char line[512];
+    int len = 0;
+    void mark(const char *what) {
+        if (!on || len > 440) return;
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        len += std::snprintf(line + len, sizeof(line) - len, " %s %.1f", what, us);
+    }
+    ~HostTrace() {
+        if (on) std::fprintf(stderr, "host_trace:%s\n", line);
+    }
+};
+thread_local HostTrace *g_ht = nullptr;
+inline void ht_mark(const char *what) {
+    if (g_ht) g_ht->mark(what);
+}
+
+// per-device one-time host setup (function attributes, occupancy queries): each of those calls
+// costs microseconds of host time on every modify call otherwise, before the first kernel
+struct DevOnce {
+    std::atomic<unsigned long long> mask{0};
+    bool first(int dev) const { return !(mask.load(std::memory_order_acquire) & (1ull << (dev & 63))); }
+    void done(int dev) { mask.fetch_or(1ull << (dev & 63), std::memory_order_release); }
+};
+inline int cur_device() {
+    int dev = 0;
+    return cudaGetDevice(&dev) == cudaSuccess ? dev : 0;
+}
+
 struct Carve {
     size_t P, res, chk, Winv, Q, G, U, panels, key, flags, ctr, sflag, rowcnt, gstrip, chkoff, dlb, dllc, full, tiles,
         total;
@@ -1344,12 +1378,22 @@ struct Exchange {
 // next diagonal solve) and two event pairs for the hand-offs between it and the call's stream.
 std::mutex g_aux_mutex;
 constexpr int kTailStreams = 8;
+constexpr size_t kTailGraphs = 4;  // e.g. one per sigma for a caller alternating update/downdate
 struct Aux {
     cudaStream_t s = nullptr;
     cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
     // the persistent chain's overlapped tail: one stream per chunk, its prefix-Gram and done events
     cudaStream_t par[kTailStreams] = {};
     cudaEvent_t scan[kTailStreams] = {}, pdone[kTailStreams] = {};
+    // the tail as a CUDA graph (pchain_tail), replayed while its arguments are unchanged
+    struct TailGraph {
+        std::vector<unsigned char> key;
+        cudaGraphExec_t exec = nullptr;
+        int launches = 0;
+    };
+    std::vector<TailGraph> tails;                   // most recent first, at most kTailGraphs
+    std::vector<std::vector<unsigned char>> seen;   // argument sets seen without a graph (same cap)
+    cudaEvent_t tfork = nullptr, tdone = nullptr;
 };
 // keyed by (device, call stream) like the workspaces: calls on different streams (host threads)
 // never share the auxiliary stream or its events
@@ -1444,17 +1488,25 @@ gcm_status_t pchain_launch(Rank &q, int64_t n, int k, int NB64, cudaStream_t str
     if (st == GCM_OK) st = check_cuda(cudaMemsetAsync(q.Pbuf(), 0xff, (size_t)n * k * 8, stream));
     if (st == GCM_OK) st = check_cuda(cudaMemsetAsync(rowcnt, 0, (size_t)NB64 * 4, stream));
     if (st != GCM_OK) return st;
+    ht_mark("memsets");
     if (armed) st = check_cuda(cudaEventRecord(armed, stream));  // the overlapped tail starts after this
     if (st != GCM_OK) return st;
     const size_t smem = pchain_smem<KB>();
-    st = check_cuda(cudaFuncSetAttribute(pchain_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (st != GCM_OK) return st;
-    int dev = 0, nsm = 0, per_sm = 0;
-    st = check_cuda(cudaGetDevice(&dev));
-    if (st == GCM_OK) st = check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    if (st == GCM_OK)
-        st = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pchain_kernel<KB>, kPcT, smem));
-    if (st != GCM_OK) return st;
+    static DevOnce once;
+    static int nsm_c[64], per_sm_c[64];
+    const int dev = cur_device();
+    if (once.first(dev)) {
+        int nsm = 0, per_sm = 0;
+        st = check_cuda(cudaFuncSetAttribute(pchain_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (st == GCM_OK) st = check_cuda(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        if (st == GCM_OK)
+            st = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pchain_kernel<KB>, kPcT, smem));
+        if (st != GCM_OK) return st;
+        nsm_c[dev & 63] = nsm;
+        per_sm_c[dev & 63] = per_sm;
+        once.done(dev);
+    }
+    const int nsm = nsm_c[dev & 63], per_sm = per_sm_c[dev & 63];
     if (per_sm < 1) return GCM_ECUDA;
     // the solver + one helper per strip that needs hand-offs (strips 2 ..), at most one CTA per SM
     constexpr int NS = PcShape<KB>::NS;
@@ -1485,9 +1537,14 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
                          cudaStream_t aux, cudaEvent_t armed, cudaEvent_t aux_done) {
     constexpr int NS = PcShape<KB>::NS;
     const size_t smem_t2 = t2_smem_bytes(KB);
-    gcm_status_t st = check_cuda(
-        cudaFuncSetAttribute(papply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t2));
-    if (st != GCM_OK) return st;
+    gcm_status_t st = GCM_OK;
+    static DevOnce once;
+    const int dev = cur_device();
+    if (once.first(dev)) {
+        st = check_cuda(cudaFuncSetAttribute(papply_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t2));
+        if (st != GCM_OK) return st;
+        once.done(dev);
+    }
     // chunks (GCM_PCHAIN_CHUNKS, default 8): all but the last on their own tail streams, in
     // parallel with each other and the chain (profiles/r02by_tail_chunks.txt)
     const char *ce = std::getenv("GCM_PCHAIN_CHUNKS");
@@ -1495,11 +1552,13 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
     const int cs = std::max(4, (NB64 + want - 1) / want);
     Aux *ax = aux_of(stream);
     ApplyMap map{q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff), q.plan.nloc};
+    int nl = 0;  // kernels enqueued (a graph replay counts its captured ones)
     auto chunk = [&](int B0, int B1, cudaStream_t s, bool wait, cudaEvent_t scan_wait,
                      cudaEvent_t scan_rec) -> gcm_status_t {
         if (wait) {
             pwait_rows_kernel<<<1, 64, 0, s>>>(q.at<unsigned>(q.cv.rowcnt), B0, B1, NB64, NS);
             count_launch();
+            ++nl;
         }
         pgram_kernel<KB><<<B1 - B0, KB * KB <= 1024 ? KB * KB : 1024, 0, s>>>(q.Pbuf(), n, k, q.at<double>(q.cv.Q), B0);
         if (scan_wait) {  // the previous chunk's prefix (G continues across chunks)
@@ -1516,18 +1575,21 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
             q.at<double>(q.cv.G), q.panbuf(), q.at<unsigned long long>(q.cv.key), ebase, q.at<int>(q.cv.dlb) + B0,
             q.at<int64_t>(q.cv.dllc) + B0);
         count_launch(3);
+        nl += 3;
         const int f0 = q.plan.full_off[B0], f1 = q.plan.full_off[B1];
         const int t0 = q.plan.tiles_off[B0], t1 = q.plan.tiles_off[B1];
         if (q.tma && f1 > f0) {
             papply_kernel<KB><<<(unsigned)(f1 - f0), kT2Threads, smem_t2, s>>>(
                 q.tm, n, k, q.at<double>(q.cv.chk), q.Ubuf(), q.panbuf(), NB64, q.at<int2>(q.cv.full) + f0, map);
             count_launch();
+            ++nl;
         }
         if (t1 > t0) {
             ptile_kernel<KB><<<(unsigned)(t1 - t0), kD, 0, s>>>(q.L, q.ldl, q.plan.nloc, k, q.at<double>(q.cv.chk),
                                                                q.Ubuf(), q.panbuf(), q.at<int2>(q.cv.tiles) + t0,
                                                                q.at<int64_t>(q.cv.chkoff));
             count_launch();
+            ++nl;
         }
         return check_cuda(cudaGetLastError());
     };
@@ -1536,6 +1598,93 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
     (void)aux;
     (void)aux_done;
     const int nchunks = (NB64 + cs - 1) / cs;
+    // The tail as ONE CUDA graph on the aux stream (GCM_TAIL_GRAPH=0: enqueued directly): its ~90
+    // launches and event operations cost ~250 us of host time per call -- longer than the chain
+    // runs at n = 5000, so the GPU waited on the host for the last chunks.  Captured once per
+    // argument set (buffers, sizes, tensor map) and replayed; every chunk polls its rows (the
+    // graph is not stream-ordered after the chain).
+    const char *ge = std::getenv("GCM_TAIL_GRAPH");
+    if (!(ge && ge[0] == '0') && ax->s) {
+        std::vector<unsigned char> key;
+        auto add = [&](const void *p, size_t bytes) {
+            const unsigned char *b = static_cast<const unsigned char *>(p);
+            key.insert(key.end(), b, b + bytes);
+        };
+        const int kb = KB;
+        add(&kb, sizeof kb), add(&n, sizeof n), add(&k, sizeof k), add(&sigma, sizeof sigma), add(&ebase, sizeof ebase);
+        add(&NB64, sizeof NB64), add(&nchunks, sizeof nchunks), add(&q.L, sizeof q.L), add(&q.ldl, sizeof q.ldl);
+        add(&q.V, sizeof q.V), add(&q.plan.nloc, sizeof q.plan.nloc), add(&q.ws, sizeof q.ws), add(&q.Pw, sizeof q.Pw);
+        add(&q.panw, sizeof q.panw), add(&q.Uw, sizeof q.Uw), add(&q.tma, sizeof q.tma), add(&q.tm, sizeof q.tm);
+        add(&q.cv, sizeof q.cv), add(&cs, sizeof cs), add(&q.plan.nb, sizeof q.plan.nb);
+        int hit = -1;
+        for (size_t i = 0; i < ax->tails.size(); ++i)
+            if (ax->tails[i].key == key) hit = (int)i;
+        // capture on the second call with one argument set (a caller whose buffers change every
+        // call keeps the direct path instead of paying a capture per call)
+        bool repeat = false;
+        if (hit < 0) {
+            for (auto it = ax->seen.begin(); it != ax->seen.end(); ++it)
+                if (*it == key) {
+                    repeat = true;
+                    ax->seen.erase(it);
+                    break;
+                }
+            if (!repeat) {
+                ax->seen.insert(ax->seen.begin(), key);
+                if (ax->seen.size() > kTailGraphs) ax->seen.pop_back();
+            }
+        }
+        if (repeat) {
+            if (!ax->tfork) st = check_cuda(cudaEventCreateWithFlags(&ax->tfork, cudaEventDisableTiming));
+            if (st == GCM_OK && !ax->tdone) st = check_cuda(cudaEventCreateWithFlags(&ax->tdone, cudaEventDisableTiming));
+            if (st != GCM_OK) return st;
+            cudaGraph_t g = nullptr;
+            cudaGraphExec_t exec = nullptr;
+            nl = 0;
+            bool cap = cudaStreamBeginCapture(ax->s, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+            gcm_status_t cs2 = cap ? check_cuda(cudaEventRecord(ax->tfork, ax->s)) : GCM_ECUDA;
+            for (int c = 0; c + 1 < nchunks && cs2 == GCM_OK; ++c) {
+                cs2 = check_cuda(cudaStreamWaitEvent(ax->par[c], ax->tfork, 0));
+                if (cs2 == GCM_OK)
+                    cs2 = chunk(c * cs, (c + 1) * cs, ax->par[c], true, c > 0 ? ax->scan[c - 1] : nullptr, ax->scan[c]);
+                if (cs2 == GCM_OK) cs2 = check_cuda(cudaEventRecord(ax->pdone[c], ax->par[c]));
+            }
+            if (cs2 == GCM_OK)
+                cs2 = chunk((nchunks - 1) * cs, NB64, ax->s, true, nchunks > 1 ? ax->scan[nchunks - 2] : nullptr, nullptr);
+            for (int c = 0; c + 1 < nchunks && cs2 == GCM_OK; ++c)
+                cs2 = check_cuda(cudaStreamWaitEvent(ax->s, ax->pdone[c], 0));
+            if (cap) {
+                const bool ended = cudaStreamEndCapture(ax->s, &g) == cudaSuccess;
+                if (!(cs2 == GCM_OK && ended && g && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess)) exec = nullptr;
+                if (g) cudaGraphDestroy(g);
+            }
+            count_launch(-nl);  // the capture's launches never ran; a replay counts them
+            if (exec) {
+                if (ax->tails.size() >= kTailGraphs) {
+                    cudaGraphExecDestroy(ax->tails.back().exec);
+                    ax->tails.pop_back();
+                }
+                Aux::TailGraph tg;
+                tg.key = key;
+                tg.exec = exec;
+                tg.launches = nl;
+                ax->tails.insert(ax->tails.begin(), std::move(tg));
+                hit = 0;
+            } else {  // capture unsupported or failed: enqueue directly (below)
+                clear_stale_error();
+            }
+        }
+        const bool ok = hit >= 0;
+        if (ok && hit > 0) std::swap(ax->tails[0], ax->tails[hit]);  // most recent first
+        if (ok) {
+            st = check_cuda(cudaStreamWaitEvent(ax->s, armed, 0));
+            if (st == GCM_OK) st = check_cuda(cudaGraphLaunch(ax->tails[0].exec, ax->s));
+            if (st == GCM_OK) st = check_cuda(cudaEventRecord(ax->tdone, ax->s));
+            if (st == GCM_OK) st = check_cuda(cudaStreamWaitEvent(stream, ax->tdone, 0));
+            count_launch(ax->tails[0].launches);
+            return st;
+        }
+    }
     for (int c = 0; c + 1 < nchunks && st == GCM_OK; ++c) {
         cudaStream_t s = ax->par[c];
         st = check_cuda(cudaStreamWaitEvent(s, armed, 0));
@@ -1575,27 +1724,34 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
         }
         return p;
     };
-    st = check_cuda(cudaFuncSetAttribute(dsolve_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)dsolve_smem<KB>()));
-    if (st == GCM_OK)
+    static DevOnce attr_once;
+    const int dev = cur_device();
+    if (attr_once.first(dev))
+        st = check_cuda(cudaFuncSetAttribute(dsolve_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)dsolve_smem<KB>()));
+    else
+        st = GCM_OK;
+    const bool set_attrs = attr_once.first(dev);
+    if (st == GCM_OK && set_attrs)
         st = check_cuda(cudaFuncSetAttribute(pupdate_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pupdate_smem<KB>()));
-    if (st == GCM_OK)
+    if (st == GCM_OK && set_attrs)
         st = check_cuda(cudaFuncSetAttribute(pupdate_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pupdate_smem<8>()));
-    if (st == GCM_OK)
+    if (st == GCM_OK && set_attrs)
         st = check_cuda(cudaFuncSetAttribute(pupdate_mma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pupdate_mma_smem<8>()));
     constexpr int KBM = KB >= 8 ? KB : 8;  // (KB = 4 keeps the DFMA kernel)
-    if (st == GCM_OK)
+    if (st == GCM_OK && set_attrs)
         st = check_cuda(cudaFuncSetAttribute(pupdate_mma_kernel<KBM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pupdate_mma_smem<KBM>()));
     // GCM_PU_DFMA=1: the residual updates on the DFMA kernel (A/B against the tensor-core one)
     const bool pu_mma = KB >= 8 && std::getenv("GCM_PU_DFMA") == nullptr;
-    if (st == GCM_OK)
+    if (st == GCM_OK && set_attrs)
         st = check_cuda(cudaFuncSetAttribute(pdiag_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pdiag_smem<KB>()));
     if (st != GCM_OK) return st;
+    if (set_attrs) attr_once.done(dev);
     // 1. residuals = V, tile (0, s) checkpoints
     for (auto &q : rk) {
         if (q.plan.nsl == 0) continue;
@@ -1604,6 +1760,7 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
                                                       q.at<double>(q.cv.res), q.at<double>(q.cv.chk));
         count_launch();
     }
+    ht_mark("pinit");
     // 2. the right-looking solve over column blocks
     {
         // (with the overlapped tail the scope holds the whole pass: 'pchain')
@@ -1622,9 +1779,12 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
             // GCM_PCHAIN_RESERVE=<m>: SMs kept free of chain CTAs for the overlapped tail (default 0)
             const char *re = std::getenv("GCM_PCHAIN_RESERVE");
             const int reserve = tail_overlap && re ? std::max(0, std::atoi(re)) : 0;
+            ht_mark("pinv");
             st = pchain_launch<KB>(rk[0], n, k, NB64, stream, tail_overlap ? ev_a[0] : nullptr, reserve);
+            ht_mark("pchain");
             if (st == GCM_OK && tail_overlap)
                 st = pchain_tail<KB>(rk[0], n, k, sigma, ebase, NB64, stream, aux, ev_a[0], ev_b[0]);
+            ht_mark("tail");
             if (st != GCM_OK) return st;
         } else {
             cudaStream_t aux = nullptr;
@@ -1861,6 +2021,12 @@ gcm_status_t upload(const Rank &q, cudaStream_t stream) {
 // one rank.  d_info receives the global first failure.
 gcm_status_t panel_modify(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int64_t k, int sigma,
                           gcm_info_t *d_info, Exchange x, cudaStream_t stream) {
+    HostTrace ht;
+    struct HtScope {
+        HostTrace *prev;
+        explicit HtScope(HostTrace *h) : prev(g_ht) { g_ht = h->on ? h : nullptr; }
+        ~HtScope() { g_ht = prev; }
+    } ht_scope(&ht);
     gcm_status_t st = GCM_OK;
     const int kc0 = (int)std::min<int64_t>(k, kPassK);
     // workspace: one carve per rank, back to back (sized for the widest pass)
@@ -1878,8 +2044,10 @@ gcm_status_t panel_modify(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, i
         base[i] = total;
         total += rk[i].cv.total;
     }
+    ht_mark("plan");
     Workspace *ws = nullptr;
     st = get_workspace(stream, total, 1, &ws);
+    ht_mark("ws");
     if (st != GCM_OK) return st;
     char *wsb = reinterpret_cast<char *>(ws->panels);
     if (x.mode == Mode::Virtual) {  // one key per rank + the min
@@ -1893,6 +2061,7 @@ gcm_status_t panel_modify(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, i
         st = check_cuda(cudaMemsetAsync(q.ws + q.cv.key, 0xff, 8, stream));
         if (st != GCM_OK) return st;
     }
+    ht_mark("upload");
     for (int64_t e0 = 0; e0 < k; e0 += kPassK) {
         const int kc = (int)std::min<int64_t>(kPassK, k - e0);
         unsigned *ep = x.epoch ? x.epoch : &ws->epoch;
