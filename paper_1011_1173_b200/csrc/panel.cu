@@ -270,8 +270,16 @@ __device__ __forceinline__ void wait_flag_sys(const unsigned *f, unsigned epoch)
 
 // -------------------------------------------------------------------------- kernels
 // residual of every local strip = its V rows; checkpoint of tile (0, s) likewise
+// (persistent chain: also arms P and the hand-offs with all-ones and zeroes rowcnt -- three
+// memsets' worth of host calls before the chain's launch)
 __global__ void pinit_kernel(const double *__restrict__ V, int64_t ldv, int64_t nloc, int k, const int *gstrip,
-                             const int64_t *chkoff, double *res, double *chk) {
+                             const int64_t *chkoff, double *res, double *chk, unsigned long long *arm_p = nullptr,
+                             int64_t n_p = 0, unsigned long long *arm_h = nullptr, int64_t n_h = 0,
+                             unsigned *zero = nullptr, int n_z = 0) {
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = gt; i < n_p; i += gs) arm_p[i] = kEmpty;
+    for (int64_t i = gt; i < n_h; i += gs) arm_h[i] = kEmpty;
+    for (int64_t i = gt; i < n_z; i += gs) zero[i] = 0u;
     const int sl = blockIdx.x;
     const int64_t lc0 = (int64_t)sl * kD;
     double *r = res + (int64_t)sl * kD * k;
@@ -1384,7 +1392,7 @@ struct Aux {
     cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
     // the persistent chain's overlapped tail: one stream per chunk, its prefix-Gram and done events
     cudaStream_t par[kTailStreams] = {};
-    cudaEvent_t scan[kTailStreams] = {}, pdone[kTailStreams] = {};
+    cudaEvent_t scan[kTailStreams] = {}, pdone[kTailStreams] = {}, wdone[kTailStreams] = {};
     // the tail as a CUDA graph (pchain_tail), replayed while its arguments are unchanged
     struct TailGraph {
         std::vector<unsigned char> key;
@@ -1414,6 +1422,7 @@ gcm_status_t aux_stream(cudaStream_t call, cudaStream_t *s, cudaEvent_t **ready,
             st = check_cuda(cudaStreamCreateWithFlags(&a.par[i], cudaStreamNonBlocking));
             if (st == GCM_OK) st = check_cuda(cudaEventCreateWithFlags(&a.scan[i], cudaEventDisableTiming));
             if (st == GCM_OK) st = check_cuda(cudaEventCreateWithFlags(&a.pdone[i], cudaEventDisableTiming));
+            if (st == GCM_OK) st = check_cuda(cudaEventCreateWithFlags(&a.wdone[i], cudaEventDisableTiming));
         }
         if (st != GCM_OK) return st;
     }
@@ -1483,11 +1492,9 @@ template <int KB>
 gcm_status_t pchain_launch(Rank &q, int64_t n, int k, int NB64, cudaStream_t stream, cudaEvent_t armed, int reserve) {
     double *hand = q.at<double>(q.cv.sflag);
     unsigned *rowcnt = q.at<unsigned>(q.cv.rowcnt);
-    // P and the hand-offs start all-ones: the "not yet written" pattern consumers poll for
-    gcm_status_t st = check_cuda(cudaMemsetAsync(hand, 0xff, (size_t)NB64 * kD * k * 8, stream));
-    if (st == GCM_OK) st = check_cuda(cudaMemsetAsync(q.Pbuf(), 0xff, (size_t)n * k * 8, stream));
-    if (st == GCM_OK) st = check_cuda(cudaMemsetAsync(rowcnt, 0, (size_t)NB64 * 4, stream));
-    if (st != GCM_OK) return st;
+    // P and the hand-offs start all-ones (the "not yet written" pattern consumers poll for) and
+    // rowcnt zero: armed by this pass's pinit_kernel
+    gcm_status_t st = GCM_OK;
     ht_mark("memsets");
     if (armed) st = check_cuda(cudaEventRecord(armed, stream));  // the overlapped tail starts after this
     if (st != GCM_OK) return st;
@@ -1553,12 +1560,23 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
     Aux *ax = aux_of(stream);
     ApplyMap map{q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff), q.plan.nloc};
     int nl = 0;  // kernels enqueued (a graph replay counts its captured ones)
-    auto chunk = [&](int B0, int B1, cudaStream_t s, bool wait, cudaEvent_t scan_wait,
+    // chunk ci's row wait starts after chunk ci-1's has returned: at most ONE spinning CTA can be
+    // resident before the cooperative chain is, and the chain's grid leaves an SM for it (a
+    // spinner per chunk could take the SMs a full-width chain grid needs: deadlock)
+    auto chunk = [&](int ci, int B0, int B1, cudaStream_t s, bool wait, cudaEvent_t scan_wait,
                      cudaEvent_t scan_rec) -> gcm_status_t {
         if (wait) {
+            if (ci > 0) {
+                const gcm_status_t s0 = check_cuda(cudaStreamWaitEvent(s, ax->wdone[ci - 1], 0));
+                if (s0 != GCM_OK) return s0;
+            }
             pwait_rows_kernel<<<1, 64, 0, s>>>(q.at<unsigned>(q.cv.rowcnt), B0, B1, NB64, NS);
             count_launch();
             ++nl;
+            if (ci < kTailStreams) {
+                const gcm_status_t s1 = check_cuda(cudaEventRecord(ax->wdone[ci], s));
+                if (s1 != GCM_OK) return s1;
+            }
         }
         pgram_kernel<KB><<<B1 - B0, KB * KB <= 1024 ? KB * KB : 1024, 0, s>>>(q.Pbuf(), n, k, q.at<double>(q.cv.Q), B0);
         if (scan_wait) {  // the previous chunk's prefix (G continues across chunks)
@@ -1646,11 +1664,11 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
             for (int c = 0; c + 1 < nchunks && cs2 == GCM_OK; ++c) {
                 cs2 = check_cuda(cudaStreamWaitEvent(ax->par[c], ax->tfork, 0));
                 if (cs2 == GCM_OK)
-                    cs2 = chunk(c * cs, (c + 1) * cs, ax->par[c], true, c > 0 ? ax->scan[c - 1] : nullptr, ax->scan[c]);
+                    cs2 = chunk(c, c * cs, (c + 1) * cs, ax->par[c], true, c > 0 ? ax->scan[c - 1] : nullptr, ax->scan[c]);
                 if (cs2 == GCM_OK) cs2 = check_cuda(cudaEventRecord(ax->pdone[c], ax->par[c]));
             }
             if (cs2 == GCM_OK)
-                cs2 = chunk((nchunks - 1) * cs, NB64, ax->s, true, nchunks > 1 ? ax->scan[nchunks - 2] : nullptr, nullptr);
+                cs2 = chunk(nchunks - 1, (nchunks - 1) * cs, NB64, ax->s, true, nchunks > 1 ? ax->scan[nchunks - 2] : nullptr, nullptr);
             for (int c = 0; c + 1 < nchunks && cs2 == GCM_OK; ++c)
                 cs2 = check_cuda(cudaStreamWaitEvent(ax->s, ax->pdone[c], 0));
             if (cap) {
@@ -1689,11 +1707,11 @@ gcm_status_t pchain_tail(Rank &q, int64_t n, int k, int sigma, int64_t ebase, in
         cudaStream_t s = ax->par[c];
         st = check_cuda(cudaStreamWaitEvent(s, armed, 0));
         if (st == GCM_OK)
-            st = chunk(c * cs, (c + 1) * cs, s, true, c > 0 ? ax->scan[c - 1] : nullptr, ax->scan[c]);
+            st = chunk(c, c * cs, (c + 1) * cs, s, true, c > 0 ? ax->scan[c - 1] : nullptr, ax->scan[c]);
         if (st == GCM_OK) st = check_cuda(cudaEventRecord(ax->pdone[c], s));
     }
     if (st != GCM_OK) return st;
-    st = chunk((nchunks - 1) * cs, NB64, stream, false, nchunks > 1 ? ax->scan[nchunks - 2] : nullptr, nullptr);
+    st = chunk(nchunks - 1, (nchunks - 1) * cs, NB64, stream, false, nchunks > 1 ? ax->scan[nchunks - 2] : nullptr, nullptr);
     for (int c = 0; c + 1 < nchunks && st == GCM_OK; ++c) st = check_cuda(cudaStreamWaitEvent(stream, ax->pdone[c], 0));
     return st;
 }
@@ -1755,9 +1773,13 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
     // 1. residuals = V, tile (0, s) checkpoints
     for (auto &q : rk) {
         if (q.plan.nsl == 0) continue;
-        pinit_kernel<<<q.plan.nsl, kPT, 0, stream>>>(q.V, std::max<int64_t>(q.plan.nloc, 1), q.plan.nloc, k,
-                                                      q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff),
-                                                      q.at<double>(q.cv.res), q.at<double>(q.cv.chk));
+        const bool arm = use_pchain;  // the persistent chain's P / hand-off / rowcnt arming
+        pinit_kernel<<<q.plan.nsl, kPT, 0, stream>>>(
+            q.V, std::max<int64_t>(q.plan.nloc, 1), q.plan.nloc, k, q.at<int>(q.cv.gstrip), q.at<int64_t>(q.cv.chkoff),
+            q.at<double>(q.cv.res), q.at<double>(q.cv.chk),
+            arm ? reinterpret_cast<unsigned long long *>(q.Pbuf()) : nullptr, arm ? n * k : 0,
+            arm ? q.at<unsigned long long>(q.cv.sflag) : nullptr, arm ? (int64_t)NB64 * kD * k : 0,
+            arm ? q.at<unsigned>(q.cv.rowcnt) : nullptr, arm ? NB64 : 0);
         count_launch();
     }
     ht_mark("pinit");
@@ -1778,7 +1800,8 @@ gcm_status_t panel_pass(std::vector<Rank> &rk, int R, int64_t n, int64_t nb, int
             if (st != GCM_OK) return st;
             // GCM_PCHAIN_RESERVE=<m>: SMs kept free of chain CTAs for the overlapped tail (default 0)
             const char *re = std::getenv("GCM_PCHAIN_RESERVE");
-            const int reserve = tail_overlap && re ? std::max(0, std::atoi(re)) : 0;
+            // (the overlapped tail: at least one SM for its single spinning row-wait CTA)
+            const int reserve = tail_overlap ? std::max(1, re ? std::atoi(re) : 0) : 0;
             ht_mark("pinv");
             st = pchain_launch<KB>(rk[0], n, k, NB64, stream, tail_overlap ? ev_a[0] : nullptr, reserve);
             ht_mark("pchain");
