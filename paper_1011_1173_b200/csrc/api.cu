@@ -160,9 +160,9 @@ gcm_algo_t pick_algo(int64_t n, int64_t k, gcm_algo_t algo) {
     // than a handful of row blocks; tiny factors keep the two-kernel sweep; large factors
     // take the column-block (panel) algorithm, whose solve chain and residual updates run on
     // the FP64 tensor cores and whose sweeps and Apply overlap the chain on parallel streams
-    // (profiles/r02bz_crossover.txt: level with BLOCKED at n ~ 6500; n = 10000, k = 32: 1.18 vs
-    // 1.47 ms).
-    if (n >= 6500) return GCM_ALGO_PANEL;
+    // (profiles/r02cq_crossover.txt: level with BLOCKED at n ~ 4700 for k <= 16, ~ 6000 for
+    // k = 32; n = 5000, k = 16: 0.329 vs 0.342 ms; n = 10000, k = 32: 1.08 vs 1.48 ms).
+    if (n >= 6500 || (n >= 4700 && k <= 16)) return GCM_ALGO_PANEL;
     return n >= 256 ? GCM_ALGO_BLOCKED : GCM_ALGO_SWEEP;
 }
 
