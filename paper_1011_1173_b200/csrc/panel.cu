@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(kDsT, 1) dsolve_kernel(const double *__restric
 // waiting for them), so the cooperative grid cannot deadlock.
 constexpr int kPcT = 512;
 #ifndef GCM_PC_REL
-#define GCM_PC_REL 4
+#define GCM_PC_REL 8
 #endif
 constexpr int kPcRel = GCM_PC_REL;  // helper tiles per rowcnt release
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
